@@ -1,0 +1,197 @@
+/*
+ * prgd.h — C-ABI of the B200 (sm_100a) PRGD hot path for low-TT-rank tensor
+ * completion (arXiv 2501.13385, "Fast and Provable Tensor-Train Format Tensor
+ * Completion via Preconditioned Riemannian Gradient Descent").
+ *
+ * Problem (`model: Low TT`):
+ *     min_T  f(T) = 1/2 <T - T*, P_Omega(T - T*)>   s.t.  rank_tt(T) = r,
+ * solved by Alg. 2.  One call of tt_prgd_step is one pass of
+ * the loop body (lines 214-218) without trimming.
+ *
+ * Conventions (all functions):
+ *  - d >= 2 modes, mode sizes n[0..d-1] (paper: d_1..d_m), TT ranks r[0..d] with
+ *    r[0] = r[d] = 1 (paper: r_0..r_m).  Indices are 0-based.
+ *  - Cores are float64, C-order [r[k]][n[k]][r[k+1]] (T_k in
+ *    R^{r_{k-1} x d_k x r_k}).
+ *  - Pointers named h_* are HOST pointers.  The library copies in/out; the caller
+ *    keeps ownership of its buffers and may reuse them when the call returns.
+ *    Device memory is owned by the context (allocated through the allocator hook
+ *    when one is installed, else cudaMalloc) and released by tt_destroy.
+ *  - Every function returns a tt_status.  On a non-OK status the context (if any)
+ *    keeps a message readable with tt_last_error; the context stays usable
+ *    unless the status is TT_ERR_CUDA.
+ *  - Work is enqueued on the context's stream (tt_set_stream; default: a stream
+ *    the library creates).  Calls that return data to the host synchronise that
+ *    stream; tt_prgd_step does not (device-side numeric faults are reported by the
+ *    next synchronising call as TT_ERR_NUMERIC).
+ *  - A context is not thread-safe; distinct contexts are independent.
+ *  - Device kernels only: there is no CPU fallback.  Without a usable sm_100
+ *    device tt_create returns TT_ERR_CUDA.
+ */
+#ifndef PRGD_H
+#define PRGD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PRGD_API __attribute__((visibility("default")))
+#else
+#define PRGD_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum tt_status {
+  TT_OK = 0,
+  TT_ERR_ARG = -1,          /* bad argument (null pointer, size, enum, out of range k) */
+  TT_ERR_RANK = -2,         /* infeasible TT ranks (see tt_create) */
+  TT_ERR_INDEX = -3,        /* an observed or queried index outside [0, n_k) */
+  TT_ERR_STATE = -4,        /* call needs observations / cores not set yet */
+  TT_ERR_NUMERIC = -5,      /* NaN/Inf, or Cholesky breakdown of a right Gram P_k */
+  TT_ERR_CUDA = -6,         /* CUDA runtime error (no device, launch failure) */
+  TT_ERR_OOM = -7,          /* device allocation failed */
+  TT_ERR_UNSUPPORTED = -8   /* valid but outside this build's limits (see tt_plan) */
+} tt_status;
+
+typedef struct tt_ctx tt_ctx;
+
+/* eps rules of the data-driven metric G_{l,k} = eps I + diag(M_k(G) M_k(G)^T)
+ * (PAPER.md:161-165):
+ *   TT_EPS_VEE   eps_l = ||G_l||_vee^2 = max_{k,j} ||M_k(G_l)(j,:)||^2, per iteration
+ *                (default).  eps_l = 0 (exact fit) makes the step a no-op.
+ *   TT_EPS_FIXED eps given by tt_set_metric (> 0), constant.
+ *   TT_EPS_NONE  W = I: the RGD iteration through the same path.
+ * step rules (A12):
+ *   TT_STEP_THEORY alpha_l = step_size * eps_l^{1/2} / p (Thm 4.1 with step_size =
+ *                  1.001; with TT_EPS_NONE: step_size / p).  Default.
+ *   TT_STEP_RAW    alpha_l = step_size. */
+enum { TT_EPS_VEE = 0, TT_EPS_FIXED = 1, TT_EPS_NONE = 2 };
+enum { TT_STEP_THEORY = 0, TT_STEP_RAW = 1 };
+
+/* ------------------------------------------------------------------ lifecycle */
+
+/* Create a context for order-d tensors of mode sizes n[d] and TT ranks r[d+1].
+ * Ranks must satisfy r[0] = r[d] = 1, r[k] >= 1 and the feasibility bounds
+ * r[k] <= min(prod_{i<k} n_i, prod_{i>=k} n_i), r[k] <= r[k-1] n[k-1],
+ * r[k-1] <= n[k-1] r[k] (TT_ERR_RANK otherwise).  Build limits
+ * (TT_ERR_UNSUPPORTED): r[k] <= 32, and some prefix split K with
+ * prod(n[0..K-1]) and prod(n[K..d-1]) both <= 2^30 (see tt_plan).
+ * Cores start at zero; observations unset.  *out receives the context. */
+PRGD_API int tt_create(int d, const int64_t* n, const int64_t* r, tt_ctx** out);
+
+/* Release all device memory and the context.  NULL is a no-op. */
+PRGD_API int tt_destroy(tt_ctx* ctx);
+
+/* Use `stream` (a cudaStream_t, e.g. PyTorch's current stream) for all work.
+ * NULL restores the library's own stream. */
+PRGD_API int tt_set_stream(tt_ctx* ctx, void* stream);
+
+/* Route device allocations through alloc(bytes, user) / free(ptr, user) (e.g.
+ * PyTorch's caching allocator).  Must be called before tt_set_observations and
+ * before any core is set; otherwise TT_ERR_STATE. */
+PRGD_API int tt_set_allocator(tt_ctx* ctx, void* (*alloc)(size_t bytes, void* user),
+                     void (*release)(void* ptr, void* user), void* user);
+
+/* ------------------------------------------------------------------ data */
+
+/* Set the observed set Omega: h_idx[m][d] sample-major int32
+ * multi-indices (0-based), h_vals[m] the observed values y_s.  Omega is a set:
+ * duplicate multi-indices are the caller's error (not detected).  Validates every
+ * index (TT_ERR_INDEX), copies to the device and builds the one-time bucketing
+ * (A0: stable LSD counting sorts into prefix and suffix order).  m = 0 is
+ * allowed (empty Omega).  m must be < 2^31.  Sets p = m / prod(n) (reading R3). */
+PRGD_API int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals, int64_t m);
+
+/* Copy core k (0 <= k < d) in/out, [r[k]][n[k]][r[k+1]] C-order float64.
+ * Cores may be in any gauge; after tt_prgd_step cores 0..d-2 are left-orthogonal
+ * (L(T_k)^T L(T_k) = I) and core d-1 carries the norm.
+ * tt_get_core synchronises the stream. */
+PRGD_API int tt_set_core(tt_ctx* ctx, int k, const double* h_core);
+PRGD_API int tt_get_core(tt_ctx* ctx, int k, double* h_core_out);
+
+/* Metric / step rules, see the enums above.  eps is used by TT_EPS_FIXED only
+ * (must be > 0 then).  Defaults: TT_EPS_VEE, TT_STEP_THEORY. */
+PRGD_API int tt_set_metric(tt_ctx* ctx, int eps_rule, double eps, int step_rule);
+
+/* ------------------------------------------------------------------ the hot path */
+
+/* One PRGD iteration (Alg. 2; no Trim):
+ *   G_l = P_Omega(T_l - y)                           A1-A2 (pass A over Omega)
+ *   weights, eps_l, phi = (eps + h)^{1/(4d)}         A3
+ *   That = W^{1/2} T_l left-orthogonalised, P_k      A4-A6
+ *   Y_k = (That^{<=k-1} (x) I)^T (W^{-1/2}G)^{<k>} (That^{>=k+1})^T   A7-A9 (pass B)
+ *   closed-form projection, unweighting              A10-A11
+ *   alpha_l, rank-2r W_l, TT-rounding SVD_r^tt(W_l)  A12-A14
+ * Enqueued asynchronously; step_size as in the step rule.  Returns TT_ERR_STATE
+ * without observations (m = 0 included) or before any core was set.
+ * With eps_l = 0 under TT_EPS_VEE the iterate is left unchanged (reading R4). */
+PRGD_API int tt_prgd_step(tt_ctx* ctx, double step_size);
+
+/* Evaluate the CURRENT iterate at h_idx[count][d] (A1) into
+ * h_out[count].  Validates indices (TT_ERR_INDEX).  count = 0 is a no-op.
+ * Synchronises. */
+PRGD_API int tt_eval_at(tt_ctx* ctx, const int32_t* h_idx, int64_t count, double* h_out);
+
+/* ||P_Omega(T_cur) - y||_2 at the CURRENT iterate (0 for empty Omega).
+ * Synchronises; reports pending TT_ERR_NUMERIC. */
+PRGD_API int tt_residual_norm(tt_ctx* ctx, double* out);
+
+/* Wait for all enqueued work; report pending device faults (TT_ERR_NUMERIC). */
+PRGD_API int tt_sync(tt_ctx* ctx);
+
+/* Message for the last non-OK status on ctx (static "..." string for NULL ctx). */
+PRGD_API const char* tt_last_error(const tt_ctx* ctx);
+
+/* ------------------------------------------------------------------ introspection */
+
+/* Host-only planning (no device needed): validates (d, n, r) like tt_create and
+ * returns the prefix/suffix split K_L (1..d-1) used by the bucketing and the
+ * dense partial-product tables: N_L = prod(n[0..K_L-1]), N_R = prod(n[K_L..d-1]).
+ * Any output pointer may be NULL. */
+PRGD_API int tt_plan(int d, const int64_t* n, const int64_t* r, int* K_L, int64_t* N_L, int64_t* N_R);
+
+/* Counters: launches = kernels this context launched since creation (graph nodes
+ * counted per replay); steps = tt_prgd_step calls. */
+typedef struct tt_stats {
+  int64_t launches;
+  int64_t steps;
+  int64_t launches_per_step;
+  int32_t K_L;
+  int32_t graphs;           /* 1 when the step runs as a captured CUDA graph */
+} tt_stats;
+PRGD_API int tt_get_stats(tt_ctx* ctx, tt_stats* out);
+
+/* Profiling: when on, steps run as direct launches with a CUDA-event pair around
+ * every kernel group; tt_get_profile returns the accumulated milliseconds per
+ * group (names via tt_profile_name) and the number of steps accumulated, then
+ * resets.  Off by default (steps run as one captured graph). */
+PRGD_API int tt_set_profiling(tt_ctx* ctx, int on);
+PRGD_API int tt_get_profile(tt_ctx* ctx, double* h_ms, int cap, int* n_groups, int64_t* n_steps);
+PRGD_API const char* tt_profile_name(int group);
+
+/* Debug readback of internal device state into host memory (tests only):
+ * what = TT_DBG_* below, k = mode where relevant, cap = capacity in elements.
+ * Returns the element count in *count.  Synchronises. */
+enum {
+  TT_DBG_PERM_PRE = 1,   /* int32[m]   sample ids in prefix order            (A0) */
+  TT_DBG_OFFS_L = 2,     /* int64[N_L+1] prefix bucket offsets               (A0) */
+  TT_DBG_PERM_SUF = 3,   /* int32[m]   sample ids in suffix order            (A0) */
+  TT_DBG_OFFS_R = 4,     /* int64[N_R+1] suffix bucket offsets               (A0) */
+  TT_DBG_RESID = 5,      /* double[m]  g_s in ORIGINAL sample order          (A2) */
+  TT_DBG_H = 6,          /* double[n_k] h_{k,j} of the last pass A           (A3) */
+  TT_DBG_PHI = 7,        /* double[n_k] phi_{k,j} of the last step           (A3) */
+  TT_DBG_EPS = 8,        /* double[4]  eps, sum g^2, alpha, p                (A3, A12) */
+  TT_DBG_U = 9,          /* double[core k] U_k of the last step              (A5) */
+  TT_DBG_P = 10,         /* double[r_k+1 ^2] P_{k+1} (right Gram) of last step (A6) */
+  TT_DBG_Y = 11,         /* double[core k] Y_k of the last step              (A9) */
+  TT_DBG_AHAT = 12       /* double[core k] Ahat_k of the last step           (A10) */
+};
+PRGD_API int tt_debug_get(tt_ctx* ctx, int what, int k, void* h_out, int64_t cap, int64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PRGD_H */

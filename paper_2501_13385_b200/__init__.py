@@ -1,0 +1,269 @@
+"""B200-native PRGD hot path for low-TT-rank tensor completion (arXiv 2501.13385).
+
+Thin ctypes binding over the C-ABI in include/prgd.h (argument marshalling only:
+every step of the path runs in the CUDA kernels of libprgd.so).  PyTorch, when
+present, supplies device memory (caching allocator) and the CUDA stream.
+
+There is no CPU fallback: if libprgd.so is missing, `load()` raises; if no
+sm_100 device is visible, creating a context raises PRGDError(TT_ERR_CUDA).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libprgd.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "prgd.h")
+
+TT_OK, TT_ERR_ARG, TT_ERR_RANK, TT_ERR_INDEX, TT_ERR_STATE = 0, -1, -2, -3, -4
+TT_ERR_NUMERIC, TT_ERR_CUDA, TT_ERR_OOM, TT_ERR_UNSUPPORTED = -5, -6, -7, -8
+STATUS_NAMES = {0: "TT_OK", -1: "TT_ERR_ARG", -2: "TT_ERR_RANK", -3: "TT_ERR_INDEX",
+                -4: "TT_ERR_STATE", -5: "TT_ERR_NUMERIC", -6: "TT_ERR_CUDA", -7: "TT_ERR_OOM",
+                -8: "TT_ERR_UNSUPPORTED"}
+EPS_RULES = {"vee": 0, "fixed": 1, "none": 2}
+STEP_RULES = {"theory": 0, "raw": 1}
+DBG = {"perm_pre": 1, "offs_l": 2, "perm_suf": 3, "offs_r": 4, "resid": 5, "h": 6, "phi": 7,
+       "eps": 8, "u": 9, "p": 10, "y": 11, "ahat": 12}
+
+
+class PRGDError(RuntimeError):
+    def __init__(self, code: int, msg: str = ""):
+        self.code = code
+        super().__init__(f"{STATUS_NAMES.get(code, code)}: {msg}")
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("launches", ctypes.c_int64), ("steps", ctypes.c_int64),
+                ("launches_per_step", ctypes.c_int64), ("K_L", ctypes.c_int32),
+                ("graphs", ctypes.c_int32)]
+
+
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libprgd.so (built by `python -m paper_2501_13385_b200.build`)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run __graft_entry__.build() "
+                          "(no CPU fallback exists)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    sig = {
+        "tt_create": (ctypes.c_int, [ctypes.c_int, i64p, i64p, ctypes.POINTER(P)]),
+        "tt_destroy": (ctypes.c_int, [P]),
+        "tt_set_stream": (ctypes.c_int, [P, P]),
+        "tt_set_allocator": (ctypes.c_int, [P, ALLOC_FN, FREE_FN, P]),
+        "tt_set_observations": (ctypes.c_int, [P, P, P, ctypes.c_int64]),
+        "tt_set_core": (ctypes.c_int, [P, ctypes.c_int, P]),
+        "tt_get_core": (ctypes.c_int, [P, ctypes.c_int, P]),
+        "tt_set_metric": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_double, ctypes.c_int]),
+        "tt_prgd_step": (ctypes.c_int, [P, ctypes.c_double]),
+        "tt_eval_at": (ctypes.c_int, [P, P, ctypes.c_int64, P]),
+        "tt_residual_norm": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_double)]),
+        "tt_sync": (ctypes.c_int, [P]),
+        "tt_last_error": (ctypes.c_char_p, [P]),
+        "tt_plan": (ctypes.c_int, [ctypes.c_int, i64p, i64p, ctypes.POINTER(ctypes.c_int),
+                                   i64p, i64p]),
+        "tt_get_stats": (ctypes.c_int, [P, ctypes.POINTER(_Stats)]),
+        "tt_set_profiling": (ctypes.c_int, [P, ctypes.c_int]),
+        "tt_get_profile": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_double), ctypes.c_int,
+                                          ctypes.POINTER(ctypes.c_int), i64p]),
+        "tt_profile_name": (ctypes.c_char_p, [ctypes.c_int]),
+        "tt_debug_get": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, ctypes.c_int64, i64p]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _i64(seq) -> ctypes.Array:
+    return (ctypes.c_int64 * len(seq))(*[int(v) for v in seq])
+
+
+def plan(n: Sequence[int], r: Sequence[int]):
+    """Host-only split planning (tt_plan): returns (K_L, N_L, N_R)."""
+    lib = load()
+    kl = ctypes.c_int()
+    nl, nr = ctypes.c_int64(), ctypes.c_int64()
+    rc = lib.tt_plan(len(n), _i64(n), _i64(r), ctypes.byref(kl), ctypes.byref(nl), ctypes.byref(nr))
+    if rc != TT_OK:
+        raise PRGDError(rc, "tt_plan")
+    return kl.value, nl.value, nr.value
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+class TTContext:
+    """One PRGD problem on the current CUDA device.
+
+    use_torch: route device allocations through PyTorch's caching allocator and run
+    on a dedicated torch.cuda.Stream (exposed as .stream)."""
+
+    def __init__(self, n: Sequence[int], r: Sequence[int], use_torch: bool = True):
+        self.lib = load()
+        self.n = tuple(int(v) for v in n)
+        self.r = tuple(int(v) for v in r)
+        self.d = len(self.n)
+        self._h = ctypes.c_void_p()
+        rc = self.lib.tt_create(self.d, _i64(self.n), _i64(self.r), ctypes.byref(self._h))
+        if rc != TT_OK:
+            raise PRGDError(rc, "tt_create")
+        self.stream = None
+        self._keep = []
+        if use_torch:
+            self._attach_torch()
+
+    # -- plumbing: PyTorch device memory and stream
+    def _attach_torch(self):
+        import torch
+        if not torch.cuda.is_available():
+            return
+        dev = torch.cuda.current_device()
+        self.stream = torch.cuda.Stream(device=dev)
+        stream = self.stream
+
+        def _alloc(nbytes, _user):
+            return torch.cuda.caching_allocator_alloc(int(nbytes), device=dev, stream=stream)
+
+        def _free(ptr, _user):
+            torch.cuda.caching_allocator_delete(ptr)
+
+        fa, ff = ALLOC_FN(_alloc), FREE_FN(_free)
+        self._keep += [fa, ff]
+        self._check(self.lib.tt_set_allocator(self._h, fa, ff, None), "tt_set_allocator")
+        self._check(self.lib.tt_set_stream(self._h, ctypes.c_void_p(stream.cuda_stream)),
+                    "tt_set_stream")
+
+    def _check(self, rc, what):
+        if rc != TT_OK:
+            msg = self.lib.tt_last_error(self._h)
+            raise PRGDError(rc, f"{what}: {msg.decode() if msg else ''}")
+
+    def close(self):
+        if self._h:
+            self.lib.tt_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- data
+    def set_observations(self, idx: np.ndarray, vals: np.ndarray):
+        idx = np.ascontiguousarray(idx, dtype=np.int32)
+        vals = np.ascontiguousarray(vals, dtype=np.float64)
+        m = vals.shape[0]
+        if m and idx.shape != (m, self.d):
+            raise ValueError("idx must be [m, d]")
+        self._check(self.lib.tt_set_observations(self._h, _ptr(idx), _ptr(vals), m),
+                    "tt_set_observations")
+
+    def set_core(self, k: int, core: np.ndarray):
+        core = np.ascontiguousarray(core, dtype=np.float64)
+        if core.shape != (self.r[k], self.n[k], self.r[k + 1]):
+            raise ValueError(f"core {k} must have shape {(self.r[k], self.n[k], self.r[k + 1])}")
+        self._check(self.lib.tt_set_core(self._h, k, _ptr(core)), "tt_set_core")
+
+    def set_cores(self, cores):
+        for k, c in enumerate(cores):
+            self.set_core(k, c)
+
+    def get_core(self, k: int) -> np.ndarray:
+        out = np.empty((self.r[k], self.n[k], self.r[k + 1]))
+        self._check(self.lib.tt_get_core(self._h, k, _ptr(out)), "tt_get_core")
+        return out
+
+    def get_cores(self):
+        return [self.get_core(k) for k in range(self.d)]
+
+    def set_metric(self, eps_rule: str = "vee", eps: float = 0.0, step_rule: str = "theory"):
+        self._check(self.lib.tt_set_metric(self._h, EPS_RULES[eps_rule], float(eps),
+                                           STEP_RULES[step_rule]), "tt_set_metric")
+
+    # -- hot path
+    def step(self, step_size: float = 1.0):
+        self._check(self.lib.tt_prgd_step(self._h, float(step_size)), "tt_prgd_step")
+
+    def eval_at(self, idx: np.ndarray) -> np.ndarray:
+        idx = np.ascontiguousarray(idx, dtype=np.int32)
+        out = np.empty(idx.shape[0])
+        self._check(self.lib.tt_eval_at(self._h, _ptr(idx), idx.shape[0], _ptr(out)), "tt_eval_at")
+        return out
+
+    def residual_norm(self) -> float:
+        v = ctypes.c_double()
+        self._check(self.lib.tt_residual_norm(self._h, ctypes.byref(v)), "tt_residual_norm")
+        return v.value
+
+    def sync(self):
+        self._check(self.lib.tt_sync(self._h), "tt_sync")
+
+    # -- introspection
+    def stats(self) -> dict:
+        s = _Stats()
+        self._check(self.lib.tt_get_stats(self._h, ctypes.byref(s)), "tt_get_stats")
+        return {f: getattr(s, f) for f, _ in _Stats._fields_}
+
+    def set_profiling(self, on: bool):
+        self._check(self.lib.tt_set_profiling(self._h, 1 if on else 0), "tt_set_profiling")
+
+    def get_profile(self) -> dict:
+        buf = (ctypes.c_double * 64)()
+        ng, ns = ctypes.c_int(), ctypes.c_int64()
+        self._check(self.lib.tt_get_profile(self._h, buf, 64, ctypes.byref(ng), ctypes.byref(ns)),
+                    "tt_get_profile")
+        names = [self.lib.tt_profile_name(i).decode() for i in range(ng.value)]
+        return {"steps": ns.value, "ms": {nm: buf[i] for i, nm in enumerate(names)}}
+
+    def debug(self, what: str, k: int = 0) -> np.ndarray:
+        """Read back internal device state (tt_debug_get; tests only)."""
+        code = DBG[what]
+        dt = np.int32 if code in (1, 3) else (np.int64 if code in (2, 4) else np.float64)
+        out = np.empty(max(self._debug_size(code, k), 4), dtype=dt)
+        cnt = ctypes.c_int64()
+        self._check(self.lib.tt_debug_get(self._h, code, k, _ptr(out), out.shape[0],
+                                          ctypes.byref(cnt)), f"tt_debug_get({what})")
+        return out[:cnt.value]
+
+    def _debug_size(self, code, k):
+        if code in (1, 3, 5):
+            return self._m_query()
+        if code in (2, 4):
+            kl, nl, nr = plan(self.n, self.r)
+            return (nl if code == 2 else nr) + 1
+        if code in (6, 7):
+            return self.n[k]
+        if code == 8:
+            return 4
+        if code in (9, 11, 12):
+            return self.r[k] * self.n[k] * self.r[k + 1]
+        if code == 10:
+            return self.r[k + 1] ** 2
+        return 0
+
+    def _m_query(self):
+        kl, nl, nr = plan(self.n, self.r)
+        offs = np.empty(nl + 1, dtype=np.int64)
+        cnt = ctypes.c_int64()
+        rc = self.lib.tt_debug_get(self._h, 2, 0, _ptr(offs), offs.shape[0], ctypes.byref(cnt))
+        if rc != TT_OK or cnt.value == 0:
+            return 0
+        return int(offs[-1])

@@ -1,0 +1,1012 @@
+// api.cu — the C-ABI of include/prgd.h: context, planning, device memory, the
+// per-iteration orchestration (two captured CUDA graphs) and debug readback.
+//
+// One iteration = G_B ("update": weights, orthogonalisation, pass B, backward
+// recursions, projection + rounding) followed by G_A ("evaluate": C tables, pass A,
+// marginals) of the new iterate, so tt_residual_norm after a step costs nothing and
+// every step does exactly one pass A and one pass B over Omega.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/prgd.h"
+#include "prgd_internal.cuh"
+
+using namespace prgd;
+
+namespace {
+
+constexpr int kNumGroups = 11;
+const char* kGroupNames[kNumGroups] = {
+    "tables_C",   "passA_prefix", "passA_suffix", "marginals",   "weights_psi", "dense_orth",
+    "tables_U",   "passB_prefix", "passB_suffix", "backward_Y", "dense_round"};
+
+constexpr int64_t kSplit = 256;        // max samples per virtual row
+constexpr int64_t kWarpTarget = 256;   // samples (+1 per row) per warp
+constexpr int64_t kMaxVrowsPerWarp = 32;
+
+int64_t sat_mul(int64_t a, int64_t b) {
+  const int64_t cap = (int64_t)1 << 62;
+  if (a == 0 || b == 0) return 0;
+  if (a > cap / b) return cap;
+  return a * b;
+}
+
+struct Plan {
+  int KL = 0;
+  int64_t NL = 0, NR = 0;
+};
+
+int validate_and_plan(int d, const int64_t* n, const int64_t* r, Plan* pl, std::string* msg) {
+  if (d < 2 || d > kMaxD || !n || !r) {
+    *msg = "need 2 <= d <= 64 and non-null n, r";
+    return TT_ERR_ARG;
+  }
+  for (int k = 0; k < d; ++k)
+    if (n[k] < 1 || n[k] > (1 << 30)) {
+      *msg = "mode sizes must be in [1, 2^30]";
+      return TT_ERR_ARG;
+    }
+  if (r[0] != 1 || r[d] != 1) {
+    *msg = "r[0] and r[d] must be 1";
+    return TT_ERR_RANK;
+  }
+  for (int k = 1; k < d; ++k) {
+    if (r[k] < 1) {
+      *msg = "ranks must be >= 1";
+      return TT_ERR_RANK;
+    }
+    int64_t left = 1, right = 1;
+    for (int i = 0; i < k; ++i) left = sat_mul(left, n[i]);
+    for (int i = k; i < d; ++i) right = sat_mul(right, n[i]);
+    if (r[k] > std::min(left, right) || r[k] > sat_mul(r[k - 1], n[k - 1]) ||
+        r[k] > sat_mul(r[k + 1], n[k])) {
+      *msg = "infeasible TT rank r[" + std::to_string(k) + "]";
+      return TT_ERR_RANK;
+    }
+  }
+  for (int k = 1; k < d; ++k)
+    if (r[k] > kMaxRank) {
+      *msg = "TT ranks above 32 are not supported by this build";
+      return TT_ERR_UNSUPPORTED;
+    }
+  int best = -1;
+  int64_t bestv = 0, bNL = 0, bNR = 0;
+  for (int kl = 1; kl < d; ++kl) {
+    int64_t NL = 1, NR = 1;
+    for (int i = 0; i < kl; ++i) NL = sat_mul(NL, n[i]);
+    for (int i = kl; i < d; ++i) NR = sat_mul(NR, n[i]);
+    int64_t v = std::max(NL, NR);
+    if (best < 0 || v < bestv) {
+      best = kl;
+      bestv = v;
+      bNL = NL;
+      bNR = NR;
+    }
+  }
+  if (bestv > ((int64_t)1 << 30)) {
+    *msg = "no prefix/suffix split with both table sizes <= 2^30 rows";
+    return TT_ERR_UNSUPPORTED;
+  }
+  pl->KL = best;
+  pl->NL = bNL;
+  pl->NR = bNR;
+  return TT_OK;
+}
+
+}  // namespace
+
+struct tt_ctx {
+  int d = 0;
+  std::vector<int64_t> n, r;
+  std::vector<int> n_i, ldr;
+  Plan plan;
+  std::vector<int64_t> NLk, NRk;   // NLk[k] = prod n[0..k-1] (k=0..KL), NRk[k] = prod n[k..d-1]
+  std::string err;
+
+  void* (*halloc)(size_t, void*) = nullptr;
+  void (*hfree)(void*, void*) = nullptr;
+  void* huser = nullptr;
+  std::vector<void*> base_allocs, obs_allocs;
+
+  cudaStream_t own_stream = nullptr, stream = nullptr;
+
+  bool base_ready = false;
+  int* n_dev = nullptr;
+  double *C = nullptr, *U = nullptr, *Y = nullptr, *Ahat = nullptr, *phi = nullptr, *h = nullptr;
+  double *P = nullptr, *L = nullptr, *B = nullptr, *work = nullptr;
+  int64_t work_len = 0;
+  std::vector<int64_t> core_off, phi_off, b_off, p_off;
+  Scalars* sc = nullptr;
+  Scalars* sc_host = nullptr;
+  std::vector<double*> LT, EL, RT, FR;
+  double *HL = nullptr, *HR = nullptr, *psiL = nullptr, *psiR = nullptr, *Ypart = nullptr;
+  int64_t Ypart_cap = 0;
+
+  bool obs_set = false;
+  int64_t m = 0;
+  double p = 0.0;
+  int32_t *Spre = nullptr, *sid_pre = nullptr, *pos_suf = nullptr, *Psuf = nullptr,
+          *sid_suf = nullptr;
+  double *ypre = nullptr, *g = nullptr;
+  int64_t *offsL = nullptr, *offsR = nullptr;
+  SegPlan planL, planR;
+
+  std::vector<char> core_set;
+  bool evalValid = false, tablesC = false;
+  int eps_rule = TT_EPS_VEE, step_rule = TT_STEP_THEORY;
+  double eps_fixed = 0.0;
+
+  cudaGraphExec_t gA = nullptr, gB = nullptr;
+  int64_t nA = 0, nB = 0;
+  int64_t launches = 0, steps = 0;
+
+  bool profiling = false;
+  cudaEvent_t ev[2 * kNumGroups] = {};
+  bool ev_ready = false;
+  double prof_ms[kNumGroups] = {};
+  int64_t prof_steps = 0;
+  bool capturing = false;
+};
+
+namespace {
+
+int fail(tt_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+int cuda_fail(tt_ctx* c, cudaError_t e, const char* where) {
+  return fail(c, TT_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                                  \
+  do {                                                            \
+    cudaError_t e_ = (call);                                      \
+    if (e_ != cudaSuccess) return cuda_fail(ctx, e_, #call);      \
+  } while (0)
+
+void* dalloc(tt_ctx* ctx, size_t bytes, std::vector<void*>& list) {
+  if (bytes == 0) bytes = 16;
+  bytes = (bytes + 255) & ~(size_t)255;
+  void* p = nullptr;
+  if (ctx->halloc) {
+    p = ctx->halloc(bytes, ctx->huser);
+  } else if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    p = nullptr;
+  }
+  if (p) list.push_back(p);
+  return p;
+}
+
+void dfree_all(tt_ctx* ctx, std::vector<void*>& list) {
+  for (void* p : list) {
+    if (ctx->hfree) ctx->hfree(p, ctx->huser);
+    else cudaFree(p);
+  }
+  list.clear();
+}
+
+template <class T>
+bool A(tt_ctx* ctx, T** out, int64_t count, std::vector<void*>& list) {
+  *out = static_cast<T*>(dalloc(ctx, (size_t)std::max<int64_t>(count, 1) * sizeof(T), list));
+  return *out != nullptr;
+}
+
+void drop_graphs(tt_ctx* ctx) {
+  if (ctx->gA) cudaGraphExecDestroy(ctx->gA);
+  if (ctx->gB) cudaGraphExecDestroy(ctx->gB);
+  ctx->gA = ctx->gB = nullptr;
+}
+
+int ensure_base(tt_ctx* ctx) {
+  if (ctx->base_ready) return TT_OK;
+  const int d = ctx->d;
+  auto& L = ctx->base_allocs;
+  const int KL = ctx->plan.KL;
+  // offsets
+  ctx->core_off.assign(d + 1, 0);
+  ctx->phi_off.assign(d + 1, 0);
+  ctx->b_off.assign(d + 1, 0);
+  ctx->p_off.assign(d + 1, 0);
+  int64_t maxb = 1, maxcore = 1, maxgram = 1;
+  for (int k = 0; k < d; ++k) {
+    const int64_t sz = ctx->r[k] * ctx->n[k] * ctx->r[k + 1];
+    ctx->core_off[k + 1] = ctx->core_off[k] + sz;
+    ctx->phi_off[k + 1] = ctx->phi_off[k] + ctx->n[k];
+    const int64_t rb0 = (k == 0) ? 1 : 2 * ctx->r[k];
+    const int64_t rb1 = (k == d - 1) ? 1 : 2 * ctx->r[k + 1];
+    ctx->b_off[k + 1] = ctx->b_off[k] + rb0 * ctx->n[k] * rb1;
+    ctx->p_off[k + 1] = ctx->p_off[k] + ctx->r[k + 1] * ctx->r[k + 1];
+    maxb = std::max(maxb, rb0 * ctx->n[k] * rb1);
+    maxcore = std::max(maxcore, sz);
+    maxgram = std::max(maxgram, ctx->r[k] * ctx->n[k] * ctx->r[k + 1]);
+  }
+  ctx->work_len = 2 * std::max(maxb, maxcore) + maxgram + 4096;
+  bool ok = A(ctx, &ctx->n_dev, d, L) && A(ctx, &ctx->C, ctx->core_off[d], L) &&
+            A(ctx, &ctx->U, ctx->core_off[d], L) && A(ctx, &ctx->Y, ctx->core_off[d], L) &&
+            A(ctx, &ctx->Ahat, ctx->core_off[d], L) && A(ctx, &ctx->phi, ctx->phi_off[d], L) &&
+            A(ctx, &ctx->h, ctx->phi_off[d], L) && A(ctx, &ctx->P, ctx->p_off[d], L) &&
+            A(ctx, &ctx->L, ctx->p_off[d], L) && A(ctx, &ctx->B, ctx->b_off[d], L) &&
+            A(ctx, &ctx->work, ctx->work_len, L) && A(ctx, &ctx->sc, 1, L);
+  if (!ok) return fail(ctx, TT_ERR_OOM, "device allocation failed (base buffers)");
+  // tables
+  ctx->LT.assign(KL + 1, nullptr);
+  ctx->EL.assign(KL + 1, nullptr);
+  ctx->RT.assign(d + 1, nullptr);
+  ctx->FR.assign(d + 1, nullptr);
+  for (int k = 1; k <= KL; ++k) {
+    const int64_t sz = ctx->NLk[k] * ctx->ldr[k];
+    if (!A(ctx, &ctx->LT[k], sz, L) || !A(ctx, &ctx->EL[k], sz, L))
+      return fail(ctx, TT_ERR_OOM, "device allocation failed (left tables)");
+  }
+  for (int k = KL; k < d; ++k) {
+    const int64_t sz = ctx->NRk[k] * ctx->ldr[k];
+    if (!A(ctx, &ctx->RT[k], sz, L) || !A(ctx, &ctx->FR[k], sz, L))
+      return fail(ctx, TT_ERR_OOM, "device allocation failed (right tables)");
+  }
+  if (!A(ctx, &ctx->HL, ctx->plan.NL, L) || !A(ctx, &ctx->HR, ctx->plan.NR, L) ||
+      !A(ctx, &ctx->psiL, ctx->plan.NL, L) || !A(ctx, &ctx->psiR, ctx->plan.NR, L))
+    return fail(ctx, TT_ERR_OOM, "device allocation failed (H / psi)");
+  int64_t ycap = 1;
+  for (int k = 0; k < KL; ++k)
+    ycap = std::max(ycap, Y_partial_need(ctx->NLk[k], (int)ctx->r[k], (int)ctx->n[k], (int)ctx->r[k + 1]));
+  for (int k = KL; k < d; ++k)
+    ycap = std::max(ycap, Y_partial_need(k + 1 < d ? ctx->NRk[k + 1] : 1, (int)ctx->r[k],
+                                         (int)ctx->n[k], (int)ctx->r[k + 1]));
+  ctx->Ypart_cap = ycap;
+  if (!A(ctx, &ctx->Ypart, ycap, L)) return fail(ctx, TT_ERR_OOM, "device allocation failed (Y)");
+  if (cudaMallocHost(&ctx->sc_host, sizeof(Scalars)) != cudaSuccess)
+    return fail(ctx, TT_ERR_OOM, "pinned allocation failed");
+  std::memset(ctx->sc_host, 0, sizeof(Scalars));
+  CK(cudaMemcpyAsync(ctx->n_dev, ctx->n_i.data(), d * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(ctx->C, 0, ctx->core_off[d] * sizeof(double), ctx->stream));
+  CK(cudaMemsetAsync(ctx->sc, 0, sizeof(Scalars), ctx->stream));
+  CK(cudaMemsetAsync(ctx->h, 0, ctx->phi_off[d] * sizeof(double), ctx->stream));
+  dense_init();
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->base_ready = true;
+  return TT_OK;
+}
+
+DenseArgs dense_args(tt_ctx* ctx) {
+  DenseArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.d = ctx->d;
+  for (int k = 0; k < ctx->d; ++k) a.n[k] = (int)ctx->n[k];
+  for (int k = 0; k <= ctx->d; ++k) {
+    a.r[k] = (int)ctx->r[k];
+    a.core_off[k] = ctx->core_off[k];
+    a.phi_off[k] = ctx->phi_off[k];
+    a.b_off[k] = ctx->b_off[k];
+    a.p_off[k] = ctx->p_off[k];
+  }
+  a.C = ctx->C;
+  a.U = ctx->U;
+  a.Y = ctx->Y;
+  a.Ahat = ctx->Ahat;
+  a.phi = ctx->phi;
+  a.P = ctx->P;
+  a.L = ctx->L;
+  a.B = ctx->B;
+  a.work = ctx->work;
+  a.work_len = ctx->work_len;
+  a.sc = ctx->sc;
+  a.smem_doubles = dense_smem_doubles();
+  return a;
+}
+
+// ------------------------------------------------------------------ profiling groups
+void grp(tt_ctx* ctx, int id, bool begin) {
+  if (!ctx->profiling || ctx->capturing || !ctx->ev_ready) return;
+  cudaEventRecord(ctx->ev[2 * id + (begin ? 0 : 1)], ctx->stream);
+}
+
+// ------------------------------------------------------------------ enqueue pieces
+void enqueue_tables(tt_ctx* ctx, bool useU, int64_t* lc) {
+  const int d = ctx->d, KL = ctx->plan.KL;
+  cudaStream_t s = ctx->stream;
+  const double* cores = useU ? ctx->U : ctx->C;
+  const Scalars* sc = useU ? ctx->sc : nullptr;
+  // left levels 1..KL
+  for (int k = 0; k < KL; ++k) {
+    const double* in = k == 0 ? nullptr : ctx->LT[k];
+    const int ldin = ctx->ldr[k];
+    const double* rs = (useU && k + 1 == KL) ? ctx->psiL : nullptr;
+    launch_table_left(s, in, ldin, cores + ctx->core_off[k], (int)ctx->r[k], (int)ctx->n[k],
+                      (int)ctx->r[k + 1], ctx->LT[k + 1], ctx->ldr[k + 1], ctx->NLk[k + 1], rs,
+                      sc, lc);
+  }
+  // right levels d-1..KL
+  for (int k = d - 1; k >= KL; --k) {
+    const double* in = k == d - 1 ? nullptr : ctx->RT[k + 1];
+    const int ldin = ctx->ldr[k + 1];
+    const double* rs = (useU && k == KL) ? ctx->psiR : nullptr;
+    launch_table_right(s, in, ldin, cores + ctx->core_off[k], (int)ctx->r[k], (int)ctx->n[k],
+                       (int)ctx->r[k + 1], ctx->RT[k], ctx->ldr[k], ctx->NRk[k], rs, sc, lc);
+  }
+}
+
+void enqueue_evaluate(tt_ctx* ctx, int64_t* lc) {
+  const int d = ctx->d, KL = ctx->plan.KL;
+  cudaStream_t s = ctx->stream;
+  grp(ctx, 0, true);
+  enqueue_tables(ctx, false, lc);
+  grp(ctx, 0, false);
+  if (ctx->obs_set && ctx->m > 0) {
+    grp(ctx, 1, true);
+    SegArgs a{};
+    a.plan = &ctx->planL;
+    a.mode = kSDDMM;
+    a.ld = ctx->ldr[KL];
+    a.col = ctx->Spre;
+    a.y = ctx->ypre;
+    a.g = ctx->g;
+    a.rowtab = ctx->LT[KL];
+    a.coltab = ctx->RT[KL];
+    a.out = ctx->HL;
+    launch_seg(s, a, nullptr, lc);
+    grp(ctx, 1, false);
+    grp(ctx, 2, true);
+    SegArgs b{};
+    b.plan = &ctx->planR;
+    b.mode = kGSQ;
+    b.ld = ctx->ldr[KL];
+    b.perm = ctx->pos_suf;
+    b.g = ctx->g;
+    b.out = ctx->HR;
+    launch_seg(s, b, nullptr, lc);
+    grp(ctx, 2, false);
+    grp(ctx, 3, true);
+    launch_marginals(s, ctx->HL, ctx->plan.NL, KL, ctx->n_i.data(), true, ctx->h, lc);
+    launch_marginals(s, ctx->HR, ctx->plan.NR, d - KL, ctx->n_i.data() + KL, false,
+                     ctx->h + ctx->phi_off[KL], lc);
+    launch_gather_sq_sum(s, ctx->h, ctx->n_i[0], ctx->sc, lc);
+    grp(ctx, 3, false);
+  }
+}
+
+void enqueue_update(tt_ctx* ctx, int64_t* lc) {
+  const int d = ctx->d, KL = ctx->plan.KL;
+  cudaStream_t s = ctx->stream;
+  grp(ctx, 4, true);
+  launch_weights(s, ctx->h, d, ctx->n_i.data(), ctx->phi_off[d], ctx->eps_rule, ctx->eps_fixed,
+                 ctx->step_rule, ctx->phi, ctx->sc, lc);
+  launch_psi(s, ctx->phi, ctx->phi_off.data(), KL, d, ctx->n_i.data(), ctx->plan.NL,
+             ctx->plan.NR, ctx->psiL, ctx->psiR, ctx->sc, lc);
+  grp(ctx, 4, false);
+  DenseArgs da = dense_args(ctx);
+  grp(ctx, 5, true);
+  launch_dense_orth(s, da, lc);
+  grp(ctx, 5, false);
+  grp(ctx, 6, true);
+  enqueue_tables(ctx, true, lc);
+  grp(ctx, 6, false);
+  grp(ctx, 7, true);
+  SegArgs a{};
+  a.plan = &ctx->planL;
+  a.mode = kSPMM;
+  a.ld = ctx->ldr[KL];
+  a.col = ctx->Spre;
+  a.g = ctx->g;
+  a.coltab = ctx->RT[KL];
+  a.rowscale = ctx->psiL;
+  a.out = ctx->EL[KL];
+  launch_seg(s, a, ctx->sc, lc);
+  grp(ctx, 7, false);
+  grp(ctx, 8, true);
+  SegArgs b{};
+  b.plan = &ctx->planR;
+  b.mode = kSPMM;
+  b.ld = ctx->ldr[KL];
+  b.col = ctx->Psuf;
+  b.perm = ctx->pos_suf;
+  b.g = ctx->g;
+  b.coltab = ctx->LT[KL];
+  b.rowscale = ctx->psiR;
+  b.out = ctx->FR[KL];
+  launch_seg(s, b, ctx->sc, lc);
+  grp(ctx, 8, false);
+  grp(ctx, 9, true);
+  for (int k = KL - 1; k >= 0; --k) {
+    const double* Atab = k >= 1 ? ctx->LT[k] : nullptr;
+    launch_Y(s, true, Atab, ctx->ldr[k], ctx->EL[k + 1], ctx->ldr[k + 1], ctx->NLk[k],
+             (int)ctx->r[k], (int)ctx->n[k], (int)ctx->r[k + 1], ctx->Y + ctx->core_off[k],
+             ctx->Ypart, ctx->Ypart_cap, ctx->sc, lc);
+    if (k >= 1)
+      launch_E_down(s, ctx->EL[k + 1], ctx->ldr[k + 1], ctx->U + ctx->core_off[k], (int)ctx->r[k],
+                    (int)ctx->n[k], (int)ctx->r[k + 1], ctx->EL[k], ctx->ldr[k], ctx->NLk[k],
+                    ctx->sc, lc);
+  }
+  for (int k = KL; k < d; ++k) {
+    const double* Btab = k + 1 < d ? ctx->RT[k + 1] : nullptr;
+    const int64_t nsum = k + 1 < d ? ctx->NRk[k + 1] : 1;
+    launch_Y(s, false, Btab, ctx->ldr[k + 1], ctx->FR[k], ctx->ldr[k], nsum, (int)ctx->r[k],
+             (int)ctx->n[k], (int)ctx->r[k + 1], ctx->Y + ctx->core_off[k], ctx->Ypart,
+             ctx->Ypart_cap, ctx->sc, lc);
+    if (k + 1 < d)
+      launch_F_up(s, ctx->FR[k], ctx->ldr[k], ctx->U + ctx->core_off[k], (int)ctx->r[k],
+                  (int)ctx->n[k], (int)ctx->r[k + 1], ctx->FR[k + 1], ctx->ldr[k + 1],
+                  ctx->NRk[k + 1], ctx->sc, lc);
+  }
+  grp(ctx, 9, false);
+  grp(ctx, 10, true);
+  launch_dense_round(s, da, lc);
+  grp(ctx, 10, false);
+}
+
+// Run a piece either as a captured graph (cached) or directly (profiling).
+int run_piece(tt_ctx* ctx, bool update) {
+  cudaGraphExec_t* ge = update ? &ctx->gB : &ctx->gA;
+  int64_t* nl = update ? &ctx->nB : &ctx->nA;
+  if (ctx->profiling) {
+    int64_t lc = 0;
+    if (update) enqueue_update(ctx, &lc);
+    else enqueue_evaluate(ctx, &lc);
+    ctx->launches += lc;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
+    return TT_OK;
+  }
+  if (!*ge) {
+    cudaGraph_t graph;
+    int64_t lc = 0;
+    ctx->capturing = true;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    if (update) enqueue_update(ctx, &lc);
+    else enqueue_evaluate(ctx, &lc);
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+    ctx->capturing = false;
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "graph capture");
+    e = cudaGraphInstantiate(ge, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "graph instantiate");
+    *nl = lc;
+  }
+  CK(cudaGraphLaunch(*ge, ctx->stream));
+  ctx->launches += *nl;
+  return TT_OK;
+}
+
+int read_scalars(tt_ctx* ctx) {
+  CK(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->sc_host->err) {
+    int bits = ctx->sc_host->err;
+    int zero = 0;
+    CK(cudaMemcpyAsync(&ctx->sc->err, &zero, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    std::string what;
+    if (bits & kErrNaN) what += " non-finite values;";
+    if (bits & kErrChol) what += " Cholesky breakdown of a right Gram P_k;";
+    if (bits & kErrSVD) what += " Jacobi SVD did not converge;";
+    return fail(ctx, TT_ERR_NUMERIC, "numeric fault:" + what);
+  }
+  return TT_OK;
+}
+
+int collect_profile(tt_ctx* ctx, int g0, int g1) {
+  if (!ctx->profiling || !ctx->ev_ready) return TT_OK;
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int gi = g0; gi <= g1; ++gi) {
+    float ms = 0.f;
+    if (cudaEventQuery(ctx->ev[2 * gi + 1]) == cudaSuccess &&
+        cudaEventElapsedTime(&ms, ctx->ev[2 * gi], ctx->ev[2 * gi + 1]) == cudaSuccess)
+      ctx->prof_ms[gi] += ms;
+  }
+  cudaGetLastError();
+  return TT_OK;
+}
+
+void build_plan_host(const std::vector<int64_t>& offs, int64_t nrows, std::vector<int32_t>& vrow_row,
+                     std::vector<int64_t>& vrow_begin, std::vector<int32_t>& vrow_cnt,
+                     std::vector<int32_t>& vrow_part, std::vector<int64_t>& warp_vbegin,
+                     std::vector<int32_t>& split_row, std::vector<int64_t>& split_first,
+                     int64_t* npart) {
+  int64_t np = 0;
+  for (int64_t P = 0; P < nrows; ++P) {
+    const int64_t b = offs[P], cnt = offs[P + 1] - offs[P];
+    if (cnt <= kSplit) {
+      vrow_row.push_back((int32_t)P);
+      vrow_begin.push_back(b);
+      vrow_cnt.push_back((int32_t)cnt);
+      vrow_part.push_back(-1);
+    } else {
+      split_row.push_back((int32_t)P);
+      split_first.push_back(np);
+      for (int64_t o = 0; o < cnt; o += kSplit) {
+        vrow_row.push_back((int32_t)P);
+        vrow_begin.push_back(b + o);
+        vrow_cnt.push_back((int32_t)std::min<int64_t>(kSplit, cnt - o));
+        vrow_part.push_back((int32_t)np++);
+      }
+    }
+  }
+  split_first.push_back(np);
+  *npart = np;
+  warp_vbegin.push_back(0);
+  int64_t acc = 0, nv = 0;
+  for (size_t v = 0; v < vrow_row.size(); ++v) {
+    acc += vrow_cnt[v] + 1;
+    ++nv;
+    if (acc >= kWarpTarget || nv >= kMaxVrowsPerWarp) {
+      warp_vbegin.push_back((int64_t)v + 1);
+      acc = 0;
+      nv = 0;
+    }
+  }
+  if (warp_vbegin.back() != (int64_t)vrow_row.size()) warp_vbegin.push_back((int64_t)vrow_row.size());
+}
+
+template <class T>
+int upload(tt_ctx* ctx, T** dst, const std::vector<T>& src) {
+  if (!A(ctx, dst, (int64_t)src.size(), ctx->obs_allocs)) return fail(ctx, TT_ERR_OOM, "device allocation failed (plan)");
+  if (!src.empty())
+    CK(cudaMemcpyAsync(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+  return TT_OK;
+}
+
+int make_plan(tt_ctx* ctx, const std::vector<int64_t>& offs, int64_t nrows, int ld, SegPlan* pl) {
+  std::vector<int32_t> vrow_row, vrow_cnt, vrow_part, split_row;
+  std::vector<int64_t> vrow_begin, warp_vbegin, split_first;
+  int64_t npart = 0;
+  build_plan_host(offs, nrows, vrow_row, vrow_begin, vrow_cnt, vrow_part, warp_vbegin, split_row,
+                  split_first, &npart);
+  *pl = SegPlan();
+  pl->nrows = nrows;
+  pl->nvrows = (int64_t)vrow_row.size();
+  pl->nwarps = (int64_t)warp_vbegin.size() - 1;
+  pl->nsplit = (int64_t)split_row.size();
+  pl->npart = npart;
+  int rc;
+  if ((rc = upload(ctx, &pl->vrow_row, vrow_row)) || (rc = upload(ctx, &pl->vrow_begin, vrow_begin)) ||
+      (rc = upload(ctx, &pl->vrow_cnt, vrow_cnt)) || (rc = upload(ctx, &pl->vrow_part, vrow_part)) ||
+      (rc = upload(ctx, &pl->warp_vbegin, warp_vbegin)) || (rc = upload(ctx, &pl->split_row, split_row)) ||
+      (rc = upload(ctx, &pl->split_first, split_first)))
+    return rc;
+  if (!A(ctx, &pl->part, std::max<int64_t>(npart, 1) * ld, ctx->obs_allocs))
+    return fail(ctx, TT_ERR_OOM, "device allocation failed (partials)");
+  return TT_OK;
+}
+
+bool all_cores_set(tt_ctx* ctx) {
+  for (char c : ctx->core_set)
+    if (!c) return false;
+  return true;
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+int tt_plan(int d, const int64_t* n, const int64_t* r, int* K_L, int64_t* N_L, int64_t* N_R) {
+  Plan pl;
+  std::string msg;
+  int rc = validate_and_plan(d, n, r, &pl, &msg);
+  if (rc != TT_OK) return rc;
+  if (K_L) *K_L = pl.KL;
+  if (N_L) *N_L = pl.NL;
+  if (N_R) *N_R = pl.NR;
+  return TT_OK;
+}
+
+int tt_create(int d, const int64_t* n, const int64_t* r, tt_ctx** out) {
+  if (!out) return TT_ERR_ARG;
+  *out = nullptr;
+  Plan pl;
+  std::string msg;
+  int rc = validate_and_plan(d, n, r, &pl, &msg);
+  if (rc != TT_OK) return rc;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return TT_ERR_CUDA;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major != 10 || prop.minor != 0)
+    return TT_ERR_CUDA;
+  tt_ctx* ctx = new tt_ctx();
+  ctx->d = d;
+  ctx->n.assign(n, n + d);
+  ctx->r.assign(r, r + d + 1);
+  ctx->n_i.resize(d);
+  for (int k = 0; k < d; ++k) ctx->n_i[k] = (int)n[k];
+  ctx->ldr.resize(d + 1);
+  for (int k = 0; k <= d; ++k) ctx->ldr[k] = pad_rank((int)r[k]);
+  ctx->plan = pl;
+  ctx->NLk.assign(pl.KL + 1, 1);
+  for (int k = 1; k <= pl.KL; ++k) ctx->NLk[k] = ctx->NLk[k - 1] * n[k - 1];
+  ctx->NRk.assign(d + 1, 1);
+  for (int k = d - 1; k >= pl.KL; --k) ctx->NRk[k] = ctx->NRk[k + 1] * n[k];
+  ctx->core_set.assign(d, 0);
+  if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return TT_ERR_CUDA;
+  }
+  ctx->stream = ctx->own_stream;
+  *out = ctx;
+  return TT_OK;
+}
+
+int tt_destroy(tt_ctx* ctx) {
+  if (!ctx) return TT_OK;
+  cudaStreamSynchronize(ctx->stream);
+  drop_graphs(ctx);
+  dfree_all(ctx, ctx->obs_allocs);
+  dfree_all(ctx, ctx->base_allocs);
+  if (ctx->sc_host) cudaFreeHost(ctx->sc_host);
+  if (ctx->ev_ready)
+    for (auto& e : ctx->ev) cudaEventDestroy(e);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+  return TT_OK;
+}
+
+int tt_set_stream(tt_ctx* ctx, void* stream) {
+  if (!ctx) return TT_ERR_ARG;
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  drop_graphs(ctx);
+  return TT_OK;
+}
+
+int tt_set_allocator(tt_ctx* ctx, void* (*alloc)(size_t, void*), void (*release)(void*, void*),
+                     void* user) {
+  if (!ctx) return TT_ERR_ARG;
+  if (ctx->base_ready || ctx->obs_set)
+    return fail(ctx, TT_ERR_STATE, "allocator must be installed before any data is set");
+  if ((alloc == nullptr) != (release == nullptr))
+    return fail(ctx, TT_ERR_ARG, "alloc and release must both be set or both NULL");
+  ctx->halloc = alloc;
+  ctx->hfree = release;
+  ctx->huser = user;
+  return TT_OK;
+}
+
+int tt_set_metric(tt_ctx* ctx, int eps_rule, double eps, int step_rule) {
+  if (!ctx) return TT_ERR_ARG;
+  if (eps_rule < TT_EPS_VEE || eps_rule > TT_EPS_NONE || step_rule < TT_STEP_THEORY ||
+      step_rule > TT_STEP_RAW)
+    return fail(ctx, TT_ERR_ARG, "unknown eps or step rule");
+  if (eps_rule == TT_EPS_FIXED && !(eps > 0.0 && std::isfinite(eps)))
+    return fail(ctx, TT_ERR_ARG, "TT_EPS_FIXED needs a finite eps > 0");
+  ctx->eps_rule = eps_rule;
+  ctx->eps_fixed = eps;
+  ctx->step_rule = step_rule;
+  drop_graphs(ctx);   // rules are baked into the captured update graph
+  return TT_OK;
+}
+
+int tt_set_core(tt_ctx* ctx, int k, const double* h_core) {
+  if (!ctx) return TT_ERR_ARG;
+  if (k < 0 || k >= ctx->d || !h_core) return fail(ctx, TT_ERR_ARG, "bad core index or NULL");
+  int rc = ensure_base(ctx);
+  if (rc) return rc;
+  const int64_t sz = ctx->core_off[k + 1] - ctx->core_off[k];
+  CK(cudaMemcpyAsync(ctx->C + ctx->core_off[k], h_core, sz * sizeof(double), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->core_set[k] = 1;
+  ctx->evalValid = false;
+  ctx->tablesC = false;
+  return TT_OK;
+}
+
+int tt_get_core(tt_ctx* ctx, int k, double* h_core_out) {
+  if (!ctx) return TT_ERR_ARG;
+  if (k < 0 || k >= ctx->d || !h_core_out) return fail(ctx, TT_ERR_ARG, "bad core index or NULL");
+  int rc = ensure_base(ctx);
+  if (rc) return rc;
+  const int64_t sz = ctx->core_off[k + 1] - ctx->core_off[k];
+  CK(cudaMemcpyAsync(h_core_out, ctx->C + ctx->core_off[k], sz * sizeof(double),
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  return read_scalars(ctx);
+}
+
+int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals, int64_t m) {
+  if (!ctx) return TT_ERR_ARG;
+  if (m < 0 || m >= ((int64_t)1 << 31)) return fail(ctx, TT_ERR_ARG, "m must be in [0, 2^31)");
+  if (m > 0 && (!h_idx || !h_vals)) return fail(ctx, TT_ERR_ARG, "NULL idx or vals");
+  int rc = ensure_base(ctx);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  drop_graphs(ctx);
+  dfree_all(ctx, ctx->obs_allocs);
+  ctx->obs_set = false;
+  ctx->evalValid = false;
+  ctx->m = 0;
+  const int d = ctx->d, KL = ctx->plan.KL;
+  const int64_t NL = ctx->plan.NL, NR = ctx->plan.NR;
+  auto& OL = ctx->obs_allocs;
+  std::vector<void*> tmp;
+  int32_t* idx_dev = nullptr;
+  double* y_orig = nullptr;
+  uint64_t *kpre = nullptr, *ksuf = nullptr, *ktmp = nullptr;
+  uint32_t *vals = nullptr, *vals2 = nullptr, *vtmp = nullptr;
+  int32_t* inv = nullptr;
+  int* hist = nullptr;
+  const int64_t hl = radix_hist_len(m);
+  bool ok = A(ctx, &idx_dev, m * d, tmp) && A(ctx, &y_orig, m, tmp) && A(ctx, &kpre, m, tmp) &&
+            A(ctx, &ksuf, m, tmp) && A(ctx, &ktmp, m, tmp) && A(ctx, &vals, m, tmp) &&
+            A(ctx, &vals2, m, tmp) && A(ctx, &vtmp, m, tmp) && A(ctx, &inv, m, tmp) &&
+            A(ctx, &hist, hl, tmp) && A(ctx, &ctx->Spre, m, OL) && A(ctx, &ctx->ypre, m, OL) &&
+            A(ctx, &ctx->g, m, OL) && A(ctx, &ctx->sid_pre, m, OL) && A(ctx, &ctx->pos_suf, m, OL) &&
+            A(ctx, &ctx->Psuf, m, OL) && A(ctx, &ctx->sid_suf, m, OL) &&
+            A(ctx, &ctx->offsL, NL + 1, OL) && A(ctx, &ctx->offsR, NR + 1, OL);
+  auto cleanup = [&]() { dfree_all(ctx, tmp); };
+  if (!ok) {
+    cleanup();
+    dfree_all(ctx, OL);
+    return fail(ctx, TT_ERR_OOM, "device allocation failed (observations)");
+  }
+  int bitsP = 1, bitsS = 1;
+  while (((int64_t)1 << bitsP) < NL) ++bitsP;
+  while (((int64_t)1 << bitsS) < NR) ++bitsS;
+  cudaStream_t s = ctx->stream;
+  int64_t lc = 0;
+  if (m > 0) {
+    CK(cudaMemcpyAsync(idx_dev, h_idx, (size_t)m * d * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(y_orig, h_vals, (size_t)m * sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(&ctx->sc->index_err, 0, sizeof(int), s));
+    launch_make_keys(s, idx_dev, m, d, ctx->n_dev, KL, bitsP, bitsS, kpre, ksuf, vals, ctx->sc, &lc);
+    CK(cudaMemcpyAsync(vals2, vals, (size_t)m * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (ctx->sc_host->index_err) {
+      cleanup();
+      dfree_all(ctx, OL);
+      return fail(ctx, TT_ERR_INDEX, "an observed index is outside [0, n_k)");
+    }
+    uint64_t* ko;
+    uint32_t* vo;
+    radix_sort_pairs(s, kpre, vals, ktmp, vtmp, m, bitsP + bitsS, hist, hl, &ko, &vo, &lc);
+    launch_after_sort_pre(s, ko, vo, m, bitsS, NL, y_orig, ctx->Spre, ctx->ypre, ctx->sid_pre, inv,
+                          ctx->offsL, &lc);
+    radix_sort_pairs(s, ksuf, vals2, ktmp, vtmp, m, bitsP + bitsS, hist, hl, &ko, &vo, &lc);
+    launch_after_sort_suf(s, ko, vo, m, bitsP, NR, inv, ctx->pos_suf, ctx->Psuf, ctx->sid_suf,
+                          ctx->offsR, &lc);
+  } else {
+    CK(cudaMemsetAsync(ctx->offsL, 0, (NL + 1) * sizeof(int64_t), s));
+    CK(cudaMemsetAsync(ctx->offsR, 0, (NR + 1) * sizeof(int64_t), s));
+  }
+  ctx->launches += lc;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(ctx, e, "bucketing kernels");
+  }
+  std::vector<int64_t> hoffsL(NL + 1), hoffsR(NR + 1);
+  CK(cudaMemcpyAsync(hoffsL.data(), ctx->offsL, (NL + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hoffsR.data(), ctx->offsR, (NR + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  cleanup();
+  if ((rc = make_plan(ctx, hoffsL, NL, ctx->ldr[KL], &ctx->planL))) return rc;
+  if ((rc = make_plan(ctx, hoffsR, NR, ctx->ldr[KL], &ctx->planR))) return rc;
+  ctx->m = m;
+  double nstar = 1.0;
+  for (int k = 0; k < d; ++k) nstar *= (double)ctx->n[k];
+  ctx->p = (double)m / nstar;
+  CK(cudaMemcpyAsync(&ctx->sc->p, &ctx->p, sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  ctx->obs_set = true;
+  return TT_OK;
+}
+
+int tt_prgd_step(tt_ctx* ctx, double step_size) {
+  if (!ctx) return TT_ERR_ARG;
+  if (!ctx->obs_set || ctx->m == 0) return fail(ctx, TT_ERR_STATE, "no observations set (nonempty Omega required)");
+  if (!all_cores_set(ctx)) return fail(ctx, TT_ERR_STATE, "all cores must be set before stepping");
+  if (!std::isfinite(step_size)) return fail(ctx, TT_ERR_ARG, "step_size must be finite");
+  if (ctx->profiling && !ctx->ev_ready) {
+    for (auto& e : ctx->ev) cudaEventCreate(&e);
+    ctx->ev_ready = true;
+  }
+  int64_t lc = 0;
+  launch_set_step(ctx->stream, ctx->sc, step_size, &lc);
+  ctx->launches += lc;
+  int rc;
+  if (!ctx->evalValid) {
+    if ((rc = run_piece(ctx, false))) return rc;
+    if (ctx->profiling) collect_profile(ctx, 0, 3);
+  }
+  if ((rc = run_piece(ctx, true))) return rc;
+  if (ctx->profiling) collect_profile(ctx, 4, 10);
+  if ((rc = run_piece(ctx, false))) return rc;
+  if (ctx->profiling) {
+    collect_profile(ctx, 0, 3);
+    ++ctx->prof_steps;
+  }
+  ctx->evalValid = true;
+  ctx->tablesC = true;
+  ++ctx->steps;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "step");
+  return TT_OK;
+}
+
+int tt_eval_at(tt_ctx* ctx, const int32_t* h_idx, int64_t count, double* h_out) {
+  if (!ctx) return TT_ERR_ARG;
+  if (count < 0) return fail(ctx, TT_ERR_ARG, "count < 0");
+  if (count == 0) return TT_OK;
+  if (!h_idx || !h_out) return fail(ctx, TT_ERR_ARG, "NULL idx or out");
+  int rc = ensure_base(ctx);
+  if (rc) return rc;
+  int64_t lc = 0;
+  if (!ctx->tablesC) {
+    enqueue_tables(ctx, false, &lc);
+    ctx->tablesC = true;
+  }
+  std::vector<void*> tmp;
+  int32_t* qidx = nullptr;
+  double* qout = nullptr;
+  if (!A(ctx, &qidx, count * ctx->d, tmp) || !A(ctx, &qout, count, tmp)) {
+    dfree_all(ctx, tmp);
+    return fail(ctx, TT_ERR_OOM, "device allocation failed (queries)");
+  }
+  cudaStream_t s = ctx->stream;
+  CK(cudaMemsetAsync(&ctx->sc->index_err, 0, sizeof(int), s));
+  CK(cudaMemcpyAsync(qidx, h_idx, (size_t)count * ctx->d * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  const int KL = ctx->plan.KL;
+  launch_eval_queries(s, qidx, count, ctx->d, ctx->n_i.data(), KL, ctx->LT[KL], ctx->RT[KL],
+                      ctx->ldr[KL], (int)ctx->r[KL], qout, ctx->sc, &lc);
+  ctx->launches += lc;
+  CK(cudaMemcpyAsync(h_out, qout, (size_t)count * sizeof(double), cudaMemcpyDeviceToHost, s));
+  rc = read_scalars(ctx);
+  dfree_all(ctx, tmp);
+  if (rc) return rc;
+  if (ctx->sc_host->index_err) return fail(ctx, TT_ERR_INDEX, "a queried index is outside [0, n_k)");
+  return TT_OK;
+}
+
+int tt_residual_norm(tt_ctx* ctx, double* out) {
+  if (!ctx || !out) return TT_ERR_ARG;
+  if (!ctx->obs_set || ctx->m == 0) {
+    *out = 0.0;
+    return TT_OK;
+  }
+  int rc;
+  if (!ctx->evalValid) {
+    if ((rc = run_piece(ctx, false))) return rc;
+    ctx->evalValid = true;
+    ctx->tablesC = true;
+  }
+  if ((rc = read_scalars(ctx))) return rc;
+  *out = std::sqrt(ctx->sc_host->sumsq);
+  return TT_OK;
+}
+
+int tt_sync(tt_ctx* ctx) {
+  if (!ctx) return TT_ERR_ARG;
+  if (!ctx->base_ready) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    return TT_OK;
+  }
+  return read_scalars(ctx);
+}
+
+const char* tt_last_error(const tt_ctx* ctx) {
+  if (!ctx) return "no context";
+  return ctx->err.c_str();
+}
+
+int tt_get_stats(tt_ctx* ctx, tt_stats* out) {
+  if (!ctx || !out) return TT_ERR_ARG;
+  out->launches = ctx->launches;
+  out->steps = ctx->steps;
+  out->launches_per_step = ctx->nA + ctx->nB + 1;
+  out->K_L = ctx->plan.KL;
+  out->graphs = ctx->profiling ? 0 : 1;
+  return TT_OK;
+}
+
+int tt_set_profiling(tt_ctx* ctx, int on) {
+  if (!ctx) return TT_ERR_ARG;
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->profiling = on != 0;
+  for (double& v : ctx->prof_ms) v = 0.0;
+  ctx->prof_steps = 0;
+  return TT_OK;
+}
+
+int tt_get_profile(tt_ctx* ctx, double* h_ms, int cap, int* n_groups, int64_t* n_steps) {
+  if (!ctx) return TT_ERR_ARG;
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (n_groups) *n_groups = kNumGroups;
+  if (n_steps) *n_steps = ctx->prof_steps;
+  if (h_ms)
+    for (int i = 0; i < kNumGroups && i < cap; ++i) h_ms[i] = ctx->prof_ms[i];
+  for (double& v : ctx->prof_ms) v = 0.0;
+  ctx->prof_steps = 0;
+  return TT_OK;
+}
+
+const char* tt_profile_name(int group) {
+  if (group < 0 || group >= kNumGroups) return "";
+  return kGroupNames[group];
+}
+
+int tt_debug_get(tt_ctx* ctx, int what, int k, void* h_out, int64_t cap, int64_t* count) {
+  if (!ctx || !h_out || !count) return TT_ERR_ARG;
+  int rc = ensure_base(ctx);
+  if (rc) return rc;
+  cudaStream_t s = ctx->stream;
+  const int d = ctx->d;
+  auto need_k = [&]() { return k >= 0 && k < d; };
+  const void* src = nullptr;
+  int64_t cnt = 0;
+  size_t esz = sizeof(double);
+  switch (what) {
+    case TT_DBG_PERM_PRE: src = ctx->sid_pre; cnt = ctx->m; esz = 4; break;
+    case TT_DBG_PERM_SUF: src = ctx->sid_suf; cnt = ctx->m; esz = 4; break;
+    case TT_DBG_OFFS_L: src = ctx->offsL; cnt = ctx->obs_set ? ctx->plan.NL + 1 : 0; esz = 8; break;
+    case TT_DBG_OFFS_R: src = ctx->offsR; cnt = ctx->obs_set ? ctx->plan.NR + 1 : 0; esz = 8; break;
+    case TT_DBG_H:
+    case TT_DBG_PHI:
+      if (!need_k()) return fail(ctx, TT_ERR_ARG, "bad k");
+      src = (what == TT_DBG_H ? ctx->h : ctx->phi) + ctx->phi_off[k];
+      cnt = ctx->n[k];
+      break;
+    case TT_DBG_U:
+    case TT_DBG_Y:
+    case TT_DBG_AHAT: {
+      if (!need_k()) return fail(ctx, TT_ERR_ARG, "bad k");
+      const double* base = what == TT_DBG_U ? ctx->U : (what == TT_DBG_Y ? ctx->Y : ctx->Ahat);
+      src = base + ctx->core_off[k];
+      cnt = ctx->core_off[k + 1] - ctx->core_off[k];
+      break;
+    }
+    case TT_DBG_P:
+      if (!need_k()) return fail(ctx, TT_ERR_ARG, "bad k");
+      src = ctx->P + ctx->p_off[k];
+      cnt = ctx->r[k + 1] * ctx->r[k + 1];
+      break;
+    case TT_DBG_EPS: {
+      if ((rc = read_scalars(ctx))) return rc;
+      if (cap < 4) return fail(ctx, TT_ERR_ARG, "capacity too small");
+      double* o = static_cast<double*>(h_out);
+      o[0] = ctx->sc_host->eps;
+      o[1] = ctx->sc_host->sumsq;
+      o[2] = ctx->sc_host->alpha;
+      o[3] = ctx->sc_host->p;
+      *count = 4;
+      return TT_OK;
+    }
+    case TT_DBG_RESID: {
+      if (!ctx->obs_set) return fail(ctx, TT_ERR_STATE, "no observations");
+      if (cap < ctx->m) return fail(ctx, TT_ERR_ARG, "capacity too small");
+      if (!ctx->evalValid && ctx->m > 0) {
+        if ((rc = run_piece(ctx, false))) return rc;
+        ctx->evalValid = true;
+        ctx->tablesC = true;
+      }
+      std::vector<double> gp(ctx->m);
+      std::vector<int32_t> sp(ctx->m);
+      if (ctx->m > 0) {
+        CK(cudaMemcpyAsync(gp.data(), ctx->g, ctx->m * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(sp.data(), ctx->sid_pre, ctx->m * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      }
+      if ((rc = read_scalars(ctx))) return rc;
+      double* o = static_cast<double*>(h_out);
+      for (int64_t t = 0; t < ctx->m; ++t) o[sp[t]] = gp[t];
+      *count = ctx->m;
+      return TT_OK;
+    }
+    default:
+      return fail(ctx, TT_ERR_ARG, "unknown debug item");
+  }
+  if (cnt > cap) return fail(ctx, TT_ERR_ARG, "capacity too small");
+  if (cnt > 0 && src) CK(cudaMemcpyAsync(h_out, src, cnt * esz, cudaMemcpyDeviceToHost, s));
+  *count = cnt;
+  CK(cudaStreamSynchronize(s));
+  return TT_OK;
+}
+
+}  // extern "C"

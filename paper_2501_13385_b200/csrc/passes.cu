@@ -1,0 +1,434 @@
+// passes.cu — the two passes over Omega and the weight computation.
+//
+// Pass A, prefix side (A1-A2, SDDMM): for every bucket P and sample s in it,
+//   v_s = T^{<=KL-1}(P) . T^{>=KL}(:, S(s)),  g_s = v_s - y_s,  H_L[P] = sum g_s^2
+// Pass A, suffix side (A3 input): H_R[S] = sum_{s in S} g_s^2.
+// Marginals (A3): h_{k,j} = sum of H over table rows whose k-th digit is j
+//   (= ||M_k(G)(j,:)||^2).
+// Weights (A3, A12): eps, w = eps + h, phi = w^{1/(4d)}, alpha.
+// Pass B (A7-A9 boundary, SpMM):
+//   E_KL[P] = psi_L[P] sum_{s in P} g_s Ttil^{>=KL}(:, S(s))
+//   F_KL[S] = psi_R[S] sum_{s in S} g_s Ttil^{<=KL-1}(P(s))
+// with psi = prod phi^{-1} over the prefix (suffix) digits, so that
+// psi_L psi_R g_s = ghat_s = (W^{-1/2} G)_s.
+//
+// Work decomposition: a warp owns a run of "virtual rows" (<= kSplit samples of one
+// bucket); LPS lanes per sample gather one table row (2 fp64 per lane, 16-byte
+// loads); results of split buckets go to partial slots reduced in order by
+// k_seg_fix, so every sum has a fixed order (deterministic).
+#include "prgd_internal.cuh"
+
+namespace prgd {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+struct SegDev {
+  int64_t nwarps;
+  const int32_t* vrow_row;
+  const int64_t* vrow_begin;
+  const int32_t* vrow_cnt;
+  const int32_t* vrow_part;
+  const int64_t* warp_vbegin;
+  double* part;
+  int ld;
+  const int32_t* col;
+  const int32_t* perm;
+  const double* y;
+  double* g;
+  const double* rowtab;
+  const double* coltab;
+  const double* rowscale;
+  double* out;
+};
+
+__device__ __forceinline__ double2 ld2(const double* p) {
+  return __ldg(reinterpret_cast<const double2*>(p));
+}
+
+template <int LPS, int MODE>
+__global__ void __launch_bounds__(256) k_seg(SegDev a, const Scalars* sc) {
+  if (sc && sc->noop) return;
+  constexpr int G = 32 / LPS;
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / LPS, sub = lane - grp * LPS;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (warp >= a.nwarps) return;
+  const int ld = a.ld;
+  const int64_t v0 = a.warp_vbegin[warp], v1 = a.warp_vbegin[warp + 1];
+  for (int64_t v = v0; v < v1; ++v) {
+    const int32_t row = a.vrow_row[v];
+    const int64_t beg = a.vrow_begin[v];
+    const int cnt = a.vrow_cnt[v];
+    double2 rv = make_double2(0.0, 0.0);
+    if (MODE == kSDDMM) rv = ld2(a.rowtab + (int64_t)row * ld + 2 * sub);
+    double accs = 0.0;
+    double2 accv = make_double2(0.0, 0.0);
+    for (int tb = 0; tb < cnt; tb += G) {
+      const int t = tb + grp;
+      const bool valid = t < cnt;
+      const int64_t s = beg + t;
+      if (MODE == kSDDMM) {
+        double2 b = make_double2(0.0, 0.0);
+        double yv = 0.0;
+        if (valid) {
+          b = ld2(a.coltab + (int64_t)a.col[s] * ld + 2 * sub);
+          yv = a.y[s];
+        }
+        double part = fma(rv.x, b.x, rv.y * b.y);
+#pragma unroll
+        for (int o = LPS / 2; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
+        const double gv = part - yv;
+        if (valid && sub == 0) {
+          a.g[s] = gv;
+          accs = fma(gv, gv, accs);
+        }
+      } else if (MODE == kGSQ) {
+        if (valid) {
+          const double gv = a.g[a.perm[s]];
+          accs = fma(gv, gv, accs);
+        }
+      } else {
+        if (valid) {
+          const double gv = a.perm ? a.g[a.perm[s]] : a.g[s];
+          const double2 b = ld2(a.coltab + (int64_t)a.col[s] * ld + 2 * sub);
+          accv.x = fma(gv, b.x, accv.x);
+          accv.y = fma(gv, b.y, accv.y);
+        }
+      }
+    }
+    const int32_t pslot = a.vrow_part[v];
+    if (MODE != kSPMM) {
+#pragma unroll
+      for (int o = LPS; o < 32; o <<= 1) accs += __shfl_xor_sync(kFull, accs, o);
+      if (lane == 0) {
+        if (pslot < 0) a.out[row] = accs;
+        else a.part[pslot] = accs;
+      }
+    } else {
+#pragma unroll
+      for (int o = LPS; o < 32; o <<= 1) {
+        accv.x += __shfl_xor_sync(kFull, accv.x, o);
+        accv.y += __shfl_xor_sync(kFull, accv.y, o);
+      }
+      if (grp == 0) {
+        double* dst;
+        if (pslot < 0) {
+          const double f = a.rowscale ? a.rowscale[row] : 1.0;
+          accv.x *= f;
+          accv.y *= f;
+          dst = a.out + (int64_t)row * ld + 2 * sub;
+        } else {
+          dst = a.part + (int64_t)pslot * ld + 2 * sub;
+        }
+        *reinterpret_cast<double2*>(dst) = accv;
+      }
+    }
+  }
+}
+
+// Sum the partial slots of split buckets in slot order.
+__global__ void k_seg_fix(int vec, int64_t nsplit, const int32_t* __restrict__ split_row,
+                          const int64_t* __restrict__ split_first, const double* __restrict__ part,
+                          int ld, const double* __restrict__ rowscale, double* __restrict__ out,
+                          const Scalars* sc) {
+  if (sc && sc->noop) return;
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int w = vec ? ld : 1;
+  int64_t i = e / w;
+  int c = (int)(e - i * w);
+  if (i >= nsplit) return;
+  const int32_t row = split_row[i];
+  double acc = 0.0;
+  for (int64_t sl = split_first[i]; sl < split_first[i + 1]; ++sl)
+    acc += vec ? part[sl * ld + c] : part[sl];
+  if (vec) {
+    if (rowscale) acc *= rowscale[row];
+    out[(int64_t)row * ld + c] = acc;
+  } else {
+    out[row] = acc;
+  }
+}
+
+struct MargArgs {
+  int nm;
+  int n[kMaxD];
+  int64_t stride[kMaxD];
+  int64_t out_off[kMaxD];
+  int64_t blk_off[kMaxD + 1];
+  int64_t N;
+};
+
+// One block per (mode, slice j): h[j] = sum_{hi, lo} H[(hi*n + j)*stride + lo], fixed order.
+__global__ void k_marginals(const double* __restrict__ H, MargArgs ma, double* __restrict__ h) {
+  __shared__ double red[256];
+  int b = blockIdx.x;
+  int m = 0;
+  while (m + 1 < ma.nm && ma.blk_off[m + 1] <= b) ++m;
+  const int j = b - (int)ma.blk_off[m];
+  const int64_t st = ma.stride[m];
+  const int64_t span = (int64_t)ma.n[m] * st;
+  const int64_t nhi = ma.N / span;
+  const int64_t total = nhi * st;
+  double acc = 0.0;
+  for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+    int64_t hi = e / st, lo = e - hi * st;
+    acc += H[hi * span + (int64_t)j * st + lo];
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) h[ma.out_off[m] + j] = red[0];
+}
+
+__global__ void k_weights(const double* __restrict__ h, int d, int64_t nsum, int n0, int eps_rule,
+                          double eps_fixed, int step_rule, double* __restrict__ phi, Scalars* sc) {
+  __shared__ double rs[256], rm[256];
+  double s = 0.0, mx = 0.0;
+  for (int64_t e = threadIdx.x; e < n0; e += blockDim.x) s += h[e];   // mode-0 marginal: sum g^2
+  for (int64_t e = threadIdx.x; e < nsum; e += blockDim.x) mx = fmax(mx, h[e]);
+  rs[threadIdx.x] = s;
+  rm[threadIdx.x] = mx;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      rs[threadIdx.x] += rs[threadIdx.x + o];
+      rm[threadIdx.x] = fmax(rm[threadIdx.x], rm[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  const double sumsq = rs[0];
+  double eps = 0.0;
+  if (eps_rule == 0) eps = rm[0];          // ||G||_vee^2
+  else if (eps_rule == 1) eps = eps_fixed;
+  const bool bad = !isfinite(sumsq) || !isfinite(eps);
+  const bool noop = bad || (eps_rule == 0 && eps == 0.0);
+  const double ex = 1.0 / (4.0 * d);
+  if (!noop) {
+    for (int64_t e = threadIdx.x; e < nsum; e += blockDim.x)
+      phi[e] = eps_rule == 2 ? 1.0 : pow(eps + h[e], ex);
+  }
+  if (threadIdx.x == 0) {
+    sc->sumsq = sumsq;
+    sc->eps = eps;
+    double alpha = sc->step_size;
+    if (step_rule == 0) alpha = eps_rule == 2 ? sc->step_size / sc->p : sc->step_size * sqrt(eps) / sc->p;
+    sc->alpha = alpha;
+    sc->noop = noop ? 1 : 0;
+    if (bad) atomicOr(&sc->err, (int)kErrNaN);
+  }
+}
+
+struct PsiArgs {
+  int d, KL;
+  int n[kMaxD];
+  int64_t phi_off[kMaxD];
+  int64_t NL, NR;
+};
+
+__global__ void k_psi(const double* __restrict__ phi, PsiArgs pa, double* __restrict__ psiL,
+                      double* __restrict__ psiR, const Scalars* sc) {
+  if (sc && sc->noop) return;
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < pa.NL) {
+    int64_t P = e;
+    double v = 1.0;
+    for (int k = pa.KL - 1; k >= 0; --k) {
+      int64_t q = P / pa.n[k];
+      int xk = (int)(P - q * pa.n[k]);
+      P = q;
+      v /= phi[pa.phi_off[k] + xk];
+    }
+    psiL[e] = v;
+  } else if (e < pa.NL + pa.NR) {
+    int64_t S = e - pa.NL;
+    const int64_t S0 = S;
+    double v = 1.0;
+    for (int k = pa.KL; k < pa.d; ++k) {
+      int64_t q = S / pa.n[k];
+      int xk = (int)(S - q * pa.n[k]);
+      S = q;
+      v /= phi[pa.phi_off[k] + xk];
+    }
+    psiR[S0] = v;
+  }
+}
+
+struct QArgs {
+  int d, KL, ld, rb;
+  int n[kMaxD];
+};
+
+__global__ void k_eval_queries(const int32_t* __restrict__ idx, int64_t count, QArgs q,
+                               const double* __restrict__ tabL, const double* __restrict__ tabR,
+                               double* __restrict__ out, Scalars* sc) {
+  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= count) return;
+  const int32_t* x = idx + s * q.d;
+  int64_t P = 0, S = 0;
+  bool bad = false;
+  for (int k = 0; k < q.KL; ++k) {
+    int xk = x[k];
+    bad |= (xk < 0) | (xk >= q.n[k]);
+    P = P * q.n[k] + (xk < 0 ? 0 : xk);
+  }
+  for (int k = q.d - 1; k >= q.KL; --k) {
+    int xk = x[k];
+    bad |= (xk < 0) | (xk >= q.n[k]);
+    S = S * q.n[k] + (xk < 0 ? 0 : xk);
+  }
+  if (bad) {
+    atomicOr(&sc->index_err, 1);
+    out[s] = 0.0;
+    return;
+  }
+  const double* a = tabL + P * q.ld;
+  const double* b = tabR + S * q.ld;
+  double v = 0.0;
+  for (int i = 0; i < q.rb; ++i) v = fma(a[i], b[i], v);
+  out[s] = v;
+}
+
+__global__ void k_set_step(Scalars* sc, double step) { sc->step_size = step; }
+
+// sum g^2 = sum_j h_{0,j} (the mode-0 marginal), fixed-order block reduction.
+__global__ void k_sumsq(const double* __restrict__ h0, int n0, Scalars* sc) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int e = threadIdx.x; e < n0; e += blockDim.x) s += h0[e];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sc->sumsq = red[0];
+}
+
+inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+template <int LPS>
+void seg_dispatch_mode(cudaStream_t s, int mode, const SegDev& dv, unsigned grid,
+                       const Scalars* sc) {
+  if (mode == kSDDMM) k_seg<LPS, kSDDMM><<<grid, 256, 0, s>>>(dv, sc);
+  else if (mode == kGSQ) k_seg<1, kGSQ><<<grid, 256, 0, s>>>(dv, sc);
+  else k_seg<LPS, kSPMM><<<grid, 256, 0, s>>>(dv, sc);
+}
+
+}  // namespace
+
+void launch_seg(cudaStream_t s, const SegArgs& a, const Scalars* sc, int64_t* launches) {
+  const SegPlan& p = *a.plan;
+  if (p.nwarps == 0) return;
+  SegDev dv;
+  dv.nwarps = p.nwarps;
+  dv.vrow_row = p.vrow_row;
+  dv.vrow_begin = p.vrow_begin;
+  dv.vrow_cnt = p.vrow_cnt;
+  dv.vrow_part = p.vrow_part;
+  dv.warp_vbegin = p.warp_vbegin;
+  dv.part = p.part;
+  dv.ld = a.ld;
+  dv.col = a.col;
+  dv.perm = a.perm;
+  dv.y = a.y;
+  dv.g = a.g;
+  dv.rowtab = a.rowtab;
+  dv.coltab = a.coltab;
+  dv.rowscale = a.rowscale;
+  dv.out = a.out;
+  unsigned grid = blocks_for(p.nwarps * 32, 256);
+  switch (a.ld / 2) {
+    case 1: seg_dispatch_mode<1>(s, a.mode, dv, grid, sc); break;
+    case 2: seg_dispatch_mode<2>(s, a.mode, dv, grid, sc); break;
+    case 4: seg_dispatch_mode<4>(s, a.mode, dv, grid, sc); break;
+    case 8: seg_dispatch_mode<8>(s, a.mode, dv, grid, sc); break;
+    default: seg_dispatch_mode<16>(s, a.mode, dv, grid, sc); break;
+  }
+  ++*launches;
+  if (p.nsplit > 0) {
+    const int vec = a.mode == kSPMM ? 1 : 0;
+    int64_t n = p.nsplit * (vec ? a.ld : 1);
+    k_seg_fix<<<blocks_for(n, 256), 256, 0, s>>>(vec, p.nsplit, p.split_row, p.split_first,
+                                                 p.part, a.ld, a.rowscale, a.out, sc);
+    ++*launches;
+  }
+}
+
+// n_modes / strides are passed in n_dev_modes as host pointer to an int array of
+// [nm] sizes (host!), msd_first: left side (first mode most significant).
+void launch_marginals(cudaStream_t s, const double* H, int64_t N, int nm, const int* n_host,
+                      bool msd_first, double* h_out, int64_t* launches) {
+  MargArgs ma;
+  ma.nm = nm;
+  ma.N = N;
+  int64_t off = 0;
+  ma.blk_off[0] = 0;
+  for (int m = 0; m < nm; ++m) {
+    ma.n[m] = n_host[m];
+    int64_t st = 1;
+    if (msd_first) {
+      for (int i = m + 1; i < nm; ++i) st *= n_host[i];
+    } else {
+      for (int i = 0; i < m; ++i) st *= n_host[i];
+    }
+    ma.stride[m] = st;
+    ma.out_off[m] = off;
+    off += n_host[m];
+    ma.blk_off[m + 1] = off;
+  }
+  k_marginals<<<(unsigned)off, 256, 0, s>>>(H, ma, h_out);
+  ++*launches;
+}
+
+void launch_weights(cudaStream_t s, const double* h, int d, const int* n_host, int64_t nsum,
+                    int eps_rule, double eps_fixed, int step_rule, double* phi, Scalars* sc,
+                    int64_t* launches) {
+  k_weights<<<1, 256, 0, s>>>(h, d, nsum, n_host[0], eps_rule, eps_fixed, step_rule, phi, sc);
+  ++*launches;
+}
+
+void launch_psi(cudaStream_t s, const double* phi, const int64_t* phi_off_host, int KL, int d,
+                const int* n_host, int64_t NL, int64_t NR, double* psiL, double* psiR,
+                const Scalars* sc, int64_t* launches) {
+  PsiArgs pa;
+  pa.d = d;
+  pa.KL = KL;
+  for (int k = 0; k < d; ++k) {
+    pa.n[k] = n_host[k];
+    pa.phi_off[k] = phi_off_host[k];
+  }
+  pa.NL = NL;
+  pa.NR = NR;
+  k_psi<<<blocks_for(NL + NR, 256), 256, 0, s>>>(phi, pa, psiL, psiR, sc);
+  ++*launches;
+}
+
+void launch_eval_queries(cudaStream_t s, const int32_t* idx, int64_t count, int d,
+                         const int* n_host, int KL, const double* tabL, const double* tabR,
+                         int ld, int rb, double* out, Scalars* sc, int64_t* launches) {
+  if (count <= 0) return;
+  QArgs q;
+  q.d = d;
+  q.KL = KL;
+  q.ld = ld;
+  q.rb = rb;
+  for (int k = 0; k < d; ++k) q.n[k] = n_host[k];
+  k_eval_queries<<<blocks_for(count, 256), 256, 0, s>>>(idx, count, q, tabL, tabR, out, sc);
+  ++*launches;
+}
+
+void launch_set_step(cudaStream_t s, Scalars* sc, double step, int64_t* launches) {
+  k_set_step<<<1, 1, 0, s>>>(sc, step);
+  ++*launches;
+}
+
+void launch_gather_sq_sum(cudaStream_t s, const double* h0, int n0, Scalars* sc, int64_t* launches) {
+  k_sumsq<<<1, 256, 0, s>>>(h0, n0, sc);
+  ++*launches;
+}
+
+}  // namespace prgd

@@ -1,0 +1,159 @@
+// prgd_internal.cuh — shared types and kernel entry points of libprgd (sm_100a).
+//
+// Data layout in HBM:
+//   cores        C_k [r_k][n_k][r_{k+1}] fp64, concatenated (core_off[k]); 0-based cores.
+//   Omega        prefix order (bucketed by P = mixed radix of x_0..x_{KL-1}, x_0 most
+//                significant): Spre[t] (int32 suffix index), ypre[t], g[t], sid_pre[t].
+//                suffix order (bucketed by S = mixed radix of x_KL..x_{d-1}, x_{d-1}
+//                most significant): pos_suf[u] (prefix position), Psuf[u].
+//   tables       left level k (1..KL): rows prod n[0..k-1], row stride ld = pad(r_k):
+//                the left part T^{<=k-1}(x).  Right level k (KL..d-1):
+//                rows prod n[k..d-1] (x_k least significant), stride pad(r_k): the
+//                right part T^{>=k}(:, x) stored as rows.
+//                E_k (left, pass-B accumulations) and F_k (right) use the same shapes.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace prgd {
+
+constexpr int kMaxD = 64;
+constexpr int kMaxRank = 32;
+constexpr int kDenseThreads = 512;
+
+// Device-side scalars of one context (one allocation).
+struct Scalars {
+  double eps;        // eps_l of the last weights computation
+  double sumsq;      // sum_s g_s^2 at the iterate of the last pass A
+  double alpha;      // alpha_l of the last step
+  double p;          // M / prod(n)
+  double step_size;  // set by k_set_step before each update
+  int noop;          // 1: skip the rest of this update (eps = 0 or a fault)
+  int err;           // nonzero: numeric fault (sticky until read by the host)
+  int index_err;     // set by index validation kernels
+  int pad;
+};
+
+enum ErrBits { kErrNaN = 1, kErrChol = 2, kErrSVD = 4 };
+
+// CSR-like "virtual row" plan of one bucketing side (host-built, device copy).
+struct SegPlan {
+  int64_t nrows = 0;        // real rows (N_L or N_R)
+  int64_t nvrows = 0;
+  int64_t nwarps = 0;
+  int64_t nsplit = 0;       // rows split over several vrows
+  int64_t npart = 0;        // partial slots
+  int32_t* vrow_row = nullptr;
+  int64_t* vrow_begin = nullptr;
+  int32_t* vrow_cnt = nullptr;
+  int32_t* vrow_part = nullptr;    // -1: whole row, else partial slot
+  int64_t* warp_vbegin = nullptr;  // [nwarps+1]
+  int32_t* split_row = nullptr;    // [nsplit]
+  int64_t* split_first = nullptr;  // [nsplit+1] partial slot ranges
+  double* part = nullptr;          // [npart * ld] partial results
+};
+
+// Parameters of the dense (single-CTA) sweep kernels; all pointers device.
+struct DenseArgs {
+  int d;
+  int n[kMaxD];
+  int r[kMaxD + 1];
+  int64_t core_off[kMaxD + 1];   // offsets of C / U / Y / Ahat (same shapes)
+  int64_t phi_off[kMaxD + 1];    // offsets into phi (sum n)
+  int64_t b_off[kMaxD + 1];      // offsets of the rank-2r cores B
+  int64_t p_off[kMaxD + 1];      // offsets of P_k / chol(P_k), r_{k+1}^2 each
+  double* C;       // current cores (input of orth, output of round)
+  double* U;       // left-orthogonal cores of That
+  double* Y;       // contractions Y_k
+  double* Ahat;    // projected variations (debug / reuse)
+  double* phi;     // phi_{k,j}
+  double* P;       // right Grams
+  double* L;       // Cholesky factors
+  double* B;       // rank-2r cores (rounding workspace)
+  double* work;    // global scratch (>= 2 * max B core + extras)
+  int64_t work_len;
+  Scalars* sc;
+  int smem_doubles;  // dynamic shared memory available to the kernel, in doubles
+};
+
+// ------------------------------------------------------------------ kernels (launchers)
+// sort.cu
+void launch_make_keys(cudaStream_t s, const int32_t* idx, int64_t m, int d, const int* n_dev,
+                      int KL, int bitsP, int bitsS, uint64_t* kpre, uint64_t* ksuf,
+                      uint32_t* vals, Scalars* sc, int64_t* launches);
+void radix_sort_pairs(cudaStream_t s, uint64_t* keys, uint32_t* vals, uint64_t* keys_tmp,
+                      uint32_t* vals_tmp, int64_t m, int bits, int* hist_buf, int64_t hist_len,
+                      uint64_t** keys_out, uint32_t** vals_out, int64_t* launches);
+int64_t radix_hist_len(int64_t m);
+void launch_after_sort_pre(cudaStream_t s, const uint64_t* keys, const uint32_t* sids, int64_t m,
+                           int bitsS, int64_t NL, const double* y_orig, int32_t* Spre,
+                           double* ypre, int32_t* sid_pre, int32_t* inv, int64_t* offsL,
+                           int64_t* launches);
+void launch_after_sort_suf(cudaStream_t s, const uint64_t* keys, const uint32_t* sids, int64_t m,
+                           int bitsP, int64_t NR, const int32_t* inv, int32_t* pos_suf,
+                           int32_t* Psuf, int32_t* sid_suf, int64_t* offsR, int64_t* launches);
+
+// tables.cu
+void launch_table_left(cudaStream_t s, const double* in, int ld_in, const double* core, int r0,
+                       int nk, int r1, double* out, int ld_out, int64_t rows_out,
+                       const double* rowscale, const Scalars* sc, int64_t* launches);
+void launch_table_right(cudaStream_t s, const double* in, int ld_in, const double* core, int r0,
+                        int nk, int r1, double* out, int ld_out, int64_t rows_out,
+                        const double* rowscale, const Scalars* sc, int64_t* launches);
+void launch_E_down(cudaStream_t s, const double* Ein, int ld_in, const double* core, int r0,
+                   int nk, int r1, double* Eout, int ld_out, int64_t rows_out,
+                   const Scalars* sc, int64_t* launches);
+void launch_F_up(cudaStream_t s, const double* Fin, int ld_in, const double* core, int r0, int nk,
+                 int r1, double* Fout, int ld_out, int64_t rows_out, const Scalars* sc,
+                 int64_t* launches);
+// Y_k[i,j,c] = sum_p A[p,i] E[p*nk+j, c]   (left)   or
+// Y_k[i,j,c] = sum_q F[j+nk*q, i] B[q, c]  (right); split-K with deterministic reduce.
+void launch_Y(cudaStream_t s, bool left, const double* A, int ldA, const double* E, int ldE,
+              int64_t nsum, int r0, int nk, int r1, double* Y, double* partial,
+              int64_t partial_cap, const Scalars* sc, int64_t* launches);
+int64_t Y_partial_need(int64_t nsum, int r0, int nk, int r1);
+
+// passes.cu
+enum SegMode { kSDDMM = 0, kGSQ = 1, kSPMM = 2 };
+struct SegArgs {
+  const SegPlan* plan;  // host copy (device pointers inside)
+  int mode;
+  int ld;               // row stride of the tables / outputs (pad(r))
+  const int32_t* col;   // per-sample column / gather index (SDDMM, SPMM)
+  const int32_t* perm;  // per-sample index into g (GSQ, SPMM suffix side) or null
+  const double* y;      // SDDMM
+  double* g;            // SDDMM writes, GSQ/SPMM read
+  const double* rowtab; // SDDMM row vectors
+  const double* coltab; // gathered table
+  const double* rowscale;  // SPMM output scale (psi) or null
+  double* out;          // SDDMM/GSQ: scalar per row; SPMM: vector per row (ld)
+};
+void launch_seg(cudaStream_t s, const SegArgs& a, const Scalars* sc, int64_t* launches);
+// n_host / phi_off_host are HOST arrays (values are passed by kernel argument).
+void launch_marginals(cudaStream_t s, const double* H, int64_t N, int nmodes, const int* n_host,
+                      bool msd_first, double* h_out, int64_t* launches);
+void launch_weights(cudaStream_t s, const double* h, int d, const int* n_host, int64_t nsum,
+                    int eps_rule, double eps_fixed, int step_rule, double* phi, Scalars* sc,
+                    int64_t* launches);
+void launch_psi(cudaStream_t s, const double* phi, const int64_t* phi_off_host, int KL, int d,
+                const int* n_host, int64_t NL, int64_t NR, double* psiL, double* psiR,
+                const Scalars* sc, int64_t* launches);
+void launch_eval_queries(cudaStream_t s, const int32_t* idx, int64_t count, int d, const int* n_host,
+                         int KL, const double* tabL, const double* tabR, int ld, int rb,
+                         double* out, Scalars* sc, int64_t* launches);
+void launch_set_step(cudaStream_t s, Scalars* sc, double step, int64_t* launches);
+void launch_gather_sq_sum(cudaStream_t s, const double* h0, int n0, Scalars* sc, int64_t* launches);
+
+// dense.cu
+void launch_dense_orth(cudaStream_t s, const DenseArgs& a, int64_t* launches);
+void launch_dense_round(cudaStream_t s, const DenseArgs& a, int64_t* launches);
+int dense_smem_doubles();
+void dense_init();   // sets the dynamic shared-memory attribute (call once, outside capture)
+
+inline int pad_rank(int r) {
+  int p = 2;
+  while (p < r) p <<= 1;
+  return p;
+}
+
+}  // namespace prgd

@@ -1,0 +1,243 @@
+// sort.cu — A0: one-time bucketing of Omega ("A0").
+//
+// Each sample s gets a prefix index P(s) (mixed radix of x_0..x_{KL-1}, x_0 most
+// significant) and a suffix index S(s) (mixed radix of x_KL..x_{d-1}, x_{d-1} most
+// significant).  Prefix order = stable sort by key (P << bitsS) | S, suffix order =
+// stable sort by (S << bitsP) | P: an LSD radix sort whose passes are stable
+// counting sorts of 8-bit digits (histogram -> exclusive scan -> stable scatter).
+// The result is unique (stable sorts are), so it is compared bit-exactly with the
+// oracle's numpy argsort(kind="stable") on the same keys.
+#include "prgd_internal.cuh"
+
+namespace prgd {
+
+namespace {
+constexpr int kRsThreads = 256;
+constexpr int kRsWarps = kRsThreads / 32;
+constexpr int kRsSub = 512;                     // items per warp per tile
+constexpr int kRsTile = kRsSub * kRsWarps;      // 4096 items per block
+
+__global__ void k_make_keys(const int32_t* __restrict__ idx, int64_t m, int d,
+                            const int* __restrict__ n, int KL, int bitsP, int bitsS,
+                            uint64_t* __restrict__ kpre, uint64_t* __restrict__ ksuf,
+                            uint32_t* __restrict__ vals, Scalars* sc) {
+  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= m) return;
+  const int32_t* x = idx + s * d;
+  uint64_t P = 0, S = 0;
+  bool bad = false;
+  for (int k = 0; k < KL; ++k) {
+    int xk = x[k];
+    bad |= (xk < 0) | (xk >= n[k]);
+    P = P * (uint64_t)n[k] + (uint64_t)(xk < 0 ? 0 : xk);
+  }
+  for (int k = d - 1; k >= KL; --k) {
+    int xk = x[k];
+    bad |= (xk < 0) | (xk >= n[k]);
+    S = S * (uint64_t)n[k] + (uint64_t)(xk < 0 ? 0 : xk);
+  }
+  if (bad) {
+    atomicOr(&sc->index_err, 1);
+    P = 0;
+    S = 0;
+  }
+  kpre[s] = (P << bitsS) | S;
+  ksuf[s] = (S << bitsP) | P;
+  vals[s] = (uint32_t)s;
+}
+
+__global__ void k_rs_hist(const uint64_t* __restrict__ keys, int64_t m, int shift,
+                          int* __restrict__ hist, int64_t nblocks) {
+  __shared__ int cnt[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  int64_t base = (int64_t)blockIdx.x * kRsTile;
+  for (int i = threadIdx.x; i < kRsTile; i += blockDim.x) {
+    int64_t t = base + i;
+    if (t < m) atomicAdd(&cnt[(keys[t] >> shift) & 255u], 1);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    hist[(int64_t)i * nblocks + blockIdx.x] = cnt[i];
+}
+
+// Exclusive scan of hist[0..len) in (digit, block) order; one block.
+__global__ void k_rs_scan(int* __restrict__ hist, int64_t len) {
+  __shared__ long long tot[1024];
+  int64_t chunk = (len + blockDim.x - 1) / blockDim.x;
+  int64_t b = threadIdx.x * chunk;
+  int64_t e = b + chunk < len ? b + chunk : len;
+  long long s = 0;
+  for (int64_t i = b; i < e; ++i) s += hist[i];
+  tot[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long run = 0;
+    for (int i = 0; i < (int)blockDim.x; ++i) {
+      long long t = tot[i];
+      tot[i] = run;
+      run += t;
+    }
+  }
+  __syncthreads();
+  long long run = tot[threadIdx.x];
+  for (int64_t i = b; i < e; ++i) {
+    int v = hist[i];
+    hist[i] = (int)run;
+    run += v;
+  }
+}
+
+// Stable scatter: within a tile, warp w owns items [w*512, (w+1)*512) and walks them
+// 32 at a time in order; __match_any_sync ranks equal digits by lane.
+__global__ void k_rs_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                             uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                             int64_t m, int shift, const int* __restrict__ hist,
+                             int64_t nblocks) {
+  __shared__ int wcnt[kRsWarps][257];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kRsWarps * 257; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kRsTile + (int64_t)w * kRsSub;
+  for (int step = 0; step < kRsSub / 32; ++step) {
+    int64_t t = base + step * 32 + lane;
+    if (t < m) atomicAdd(&wcnt[w][(kin[t] >> shift) & 255u], 1);
+  }
+  __syncthreads();
+  for (int dg = threadIdx.x; dg < 256; dg += blockDim.x) {
+    int run = hist[(int64_t)dg * nblocks + blockIdx.x];
+    for (int w2 = 0; w2 < kRsWarps; ++w2) {
+      int c = wcnt[w2][dg];
+      wcnt[w2][dg] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int step = 0; step < kRsSub / 32; ++step) {
+    int64_t t = base + step * 32 + lane;
+    bool valid = t < m;
+    uint64_t key = valid ? kin[t] : 0ull;
+    uint32_t val = valid ? vin[t] : 0u;
+    int dg = valid ? (int)((key >> shift) & 255u) : 256;
+    unsigned peers = __match_any_sync(0xffffffffu, dg);
+    int rank = __popc(peers & ((1u << lane) - 1u));
+    int leader = __ffs(peers) - 1;
+    int pos = wcnt[w][dg];
+    if (valid) {
+      kout[pos + rank] = key;
+      vout[pos + rank] = val;
+    }
+    __syncwarp();
+    if (lane == leader) wcnt[w][dg] = pos + __popc(peers);
+    __syncwarp();
+  }
+}
+
+__global__ void k_after_pre(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ sids,
+                            int64_t m, int bitsS, int64_t NL, const double* __restrict__ y_orig,
+                            int32_t* __restrict__ Spre, double* __restrict__ ypre,
+                            int32_t* __restrict__ sid_pre, int32_t* __restrict__ inv,
+                            int64_t* __restrict__ offsL) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  const uint64_t mask = (1ull << bitsS) - 1ull;
+  uint64_t key = keys[t];
+  int64_t P = (int64_t)(key >> bitsS);
+  uint32_t sid = sids[t];
+  Spre[t] = (int32_t)(key & mask);
+  ypre[t] = y_orig[sid];
+  sid_pre[t] = (int32_t)sid;
+  inv[sid] = (int32_t)t;
+  int64_t Pprev = t == 0 ? -1 : (int64_t)(keys[t - 1] >> bitsS);
+  for (int64_t q = Pprev + 1; q <= P; ++q) offsL[q] = t;
+  if (t == m - 1)
+    for (int64_t q = P + 1; q <= NL; ++q) offsL[q] = m;
+}
+
+__global__ void k_after_suf(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ sids,
+                            int64_t m, int bitsP, int64_t NR, const int32_t* __restrict__ inv,
+                            int32_t* __restrict__ pos_suf, int32_t* __restrict__ Psuf,
+                            int32_t* __restrict__ sid_suf, int64_t* __restrict__ offsR) {
+  int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= m) return;
+  const uint64_t mask = (1ull << bitsP) - 1ull;
+  uint64_t key = keys[u];
+  int64_t S = (int64_t)(key >> bitsP);
+  uint32_t sid = sids[u];
+  Psuf[u] = (int32_t)(key & mask);
+  pos_suf[u] = inv[sid];
+  sid_suf[u] = (int32_t)sid;
+  int64_t Sprev = u == 0 ? -1 : (int64_t)(keys[u - 1] >> bitsP);
+  for (int64_t q = Sprev + 1; q <= S; ++q) offsR[q] = u;
+  if (u == m - 1)
+    for (int64_t q = S + 1; q <= NR; ++q) offsR[q] = m;
+}
+
+inline unsigned grid_for(int64_t n, int threads) {
+  return (unsigned)((n + threads - 1) / threads);
+}
+}  // namespace
+
+int64_t radix_hist_len(int64_t m) {
+  int64_t nb = (m + kRsTile - 1) / kRsTile;
+  if (nb < 1) nb = 1;
+  return 256 * nb;
+}
+
+void launch_make_keys(cudaStream_t s, const int32_t* idx, int64_t m, int d, const int* n_dev,
+                      int KL, int bitsP, int bitsS, uint64_t* kpre, uint64_t* ksuf,
+                      uint32_t* vals, Scalars* sc, int64_t* launches) {
+  if (m <= 0) return;
+  k_make_keys<<<grid_for(m, 256), 256, 0, s>>>(idx, m, d, n_dev, KL, bitsP, bitsS, kpre, ksuf,
+                                                vals, sc);
+  ++*launches;
+}
+
+void radix_sort_pairs(cudaStream_t s, uint64_t* keys, uint32_t* vals, uint64_t* keys_tmp,
+                      uint32_t* vals_tmp, int64_t m, int bits, int* hist, int64_t hist_len,
+                      uint64_t** keys_out, uint32_t** vals_out, int64_t* launches) {
+  uint64_t* kin = keys;
+  uint32_t* vin = vals;
+  uint64_t* ko = keys_tmp;
+  uint32_t* vo = vals_tmp;
+  if (m > 0) {
+    int64_t nblocks = (m + kRsTile - 1) / kRsTile;
+    (void)hist_len;
+    for (int shift = 0; shift < bits; shift += 8) {
+      k_rs_hist<<<(unsigned)nblocks, kRsThreads, 0, s>>>(kin, m, shift, hist, nblocks);
+      k_rs_scan<<<1, 1024, 0, s>>>(hist, 256 * nblocks);
+      k_rs_scatter<<<(unsigned)nblocks, kRsThreads, 0, s>>>(kin, vin, ko, vo, m, shift, hist,
+                                                            nblocks);
+      *launches += 3;
+      uint64_t* tk = kin;
+      kin = ko;
+      ko = tk;
+      uint32_t* tv = vin;
+      vin = vo;
+      vo = tv;
+    }
+  }
+  *keys_out = kin;
+  *vals_out = vin;
+}
+
+void launch_after_sort_pre(cudaStream_t s, const uint64_t* keys, const uint32_t* sids, int64_t m,
+                           int bitsS, int64_t NL, const double* y_orig, int32_t* Spre,
+                           double* ypre, int32_t* sid_pre, int32_t* inv, int64_t* offsL,
+                           int64_t* launches) {
+  if (m <= 0) return;
+  k_after_pre<<<grid_for(m, 256), 256, 0, s>>>(keys, sids, m, bitsS, NL, y_orig, Spre, ypre,
+                                                sid_pre, inv, offsL);
+  ++*launches;
+}
+
+void launch_after_sort_suf(cudaStream_t s, const uint64_t* keys, const uint32_t* sids, int64_t m,
+                           int bitsP, int64_t NR, const int32_t* inv, int32_t* pos_suf,
+                           int32_t* Psuf, int32_t* sid_suf, int64_t* offsR, int64_t* launches) {
+  if (m <= 0) return;
+  k_after_suf<<<grid_for(m, 256), 256, 0, s>>>(keys, sids, m, bitsP, NR, inv, pos_suf, Psuf,
+                                                sid_suf, offsR);
+  ++*launches;
+}
+
+}  // namespace prgd

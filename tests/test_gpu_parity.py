@@ -1,0 +1,190 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same
+seeded inputs.  Tolerances: bucketing bit-exact; evaluation /
+residual entrywise <= 1e-13 relative to max|v|; one step <= 1e-11 relative
+Frobenius (tensor, gauge-free, via the block-TT QR-sweep norm); 50 steps <= 1e-8."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2501_13385_b200 as p
+    p.load()
+    return p
+
+
+def problem(cfg, m=None, **kw):
+    pr = synth.make_problem(cfg, m=m, **kw)
+    clean = oracle.eval_at(pr.truth, pr.idx)
+    y = pr.observations(clean)
+    init = pr.init if pr.init is not None else oracle.spectral_init(pr.idx, y, pr.n, pr.r)
+    return pr, y, init
+
+
+def context(pkg, pr, y, init):
+    ctx = pkg.TTContext(pr.n, pr.r)
+    ctx.set_observations(pr.idx, y)
+    ctx.set_cores(init)
+    return ctx
+
+
+# Sizes the oracle finishes in seconds; each spans many buckets, split buckets
+# (cfg3's 256 prefix rows hold ~3k samples each) and ragged tails.
+CASES = [
+    (1, None, {}),
+    (2, None, {}),
+    (3, 200_000, {}),
+    (4, 200_000, {}),
+    (5, 400_000, {}),
+]
+
+
+@pytest.mark.parametrize("cfg,m,kw", CASES)
+def test_bucketing_bit_exact(pkg, cfg, m, kw):
+    pr, y, init = problem(cfg, m, **kw)
+    ctx = context(pkg, pr, y, init)
+    KL, NL, NR = pkg.plan(pr.n, pr.r)
+    assert KL == oracle.split_point(pr.n)
+    o = oracle.stable_order(pr.idx, pr.n, KL)
+    assert np.array_equal(ctx.debug("perm_pre"), o["perm_pre"].astype(np.int32))
+    assert np.array_equal(ctx.debug("perm_suf"), o["perm_suf"].astype(np.int32))
+    assert np.array_equal(ctx.debug("offs_l"), o["offs_L"].astype(np.int64))
+    assert np.array_equal(ctx.debug("offs_r"), o["offs_R"].astype(np.int64))
+    ctx.close()
+
+
+@pytest.mark.parametrize("cfg,m,kw", CASES)
+def test_eval_residual_and_weights(pkg, cfg, m, kw):
+    pr, y, init = problem(cfg, m, **kw)
+    ctx = context(pkg, pr, y, init)
+    rng = np.random.default_rng(7)
+    held = np.stack([rng.integers(0, nk, 5000) for nk in pr.n], axis=1).astype(np.int32)
+    for q in (pr.idx[:20000], held):
+        got = ctx.eval_at(q)
+        ref = oracle.eval_at(init, q)
+        assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref))
+    g_ref = oracle.residual(init, pr.idx, y)
+    g = ctx.debug("resid")
+    assert np.max(np.abs(g - g_ref)) <= 1e-13 * max(np.max(np.abs(y)), 1e-300)
+    res = ctx.residual_norm()
+    assert abs(res - np.linalg.norm(g_ref)) <= 1e-12 * np.linalg.norm(g_ref)
+    ctx.step(1.0)
+    _, info = oracle.prgd_step(init, pr.idx, y, pr.n, pr.r, 1.0, return_info=True)
+    eps = ctx.debug("eps")
+    assert eps[0] == pytest.approx(info["eps"], rel=1e-12)
+    assert eps[3] == pytest.approx(info["p"], rel=1e-15)
+    assert eps[2] == pytest.approx(info["alpha"], rel=1e-12)
+    for k in range(pr.d):
+        np.testing.assert_allclose(ctx.debug("phi", k), info["phi"][k], rtol=1e-13)
+    ctx.close()
+
+
+@pytest.mark.parametrize("cfg,m,kw", CASES)
+def test_one_step_parity(pkg, cfg, m, kw):
+    pr, y, init = problem(cfg, m, **kw)
+    ctx = context(pkg, pr, y, init)
+    ctx.step(1.0)
+    got = ctx.get_cores()
+    ref, info = oracle.prgd_step(init, pr.idx, y, pr.n, pr.r, 1.0, return_info=True)
+    # stage parity (Householder sign conventions match LAPACK, so U is gauge-identical)
+    for k in range(pr.d):
+        U = ctx.debug("u", k).reshape(info["U"][k].shape)
+        np.testing.assert_allclose(U, info["U"][k], rtol=0, atol=1e-11 * np.abs(info["U"][k]).max())
+        Yk = ctx.debug("y", k).reshape(info["Y"][k].shape)
+        np.testing.assert_allclose(Yk, info["Y"][k], rtol=0, atol=1e-10 * np.abs(info["Y"][k]).max())
+    err = oracle.tt_diff_norm(got, ref)
+    assert err <= 1e-11, err
+    # output gauge: cores 0..d-2 left-orthogonal (A14)
+    for k in range(pr.d - 1):
+        Lk = got[k].reshape(-1, got[k].shape[2])
+        np.testing.assert_allclose(Lk.T @ Lk, np.eye(Lk.shape[1]), atol=1e-12)
+    ctx.close()
+
+
+@pytest.mark.parametrize("cfg,m,steps", [(1, None, 50), (2, None, 50), (4, 100_000, 50)])
+def test_many_steps_parity(pkg, cfg, m, steps):
+    pr, y, init = problem(cfg, m)
+    ctx = context(pkg, pr, y, init)
+    T = init
+    for _ in range(steps):
+        ctx.step(1.0)
+        T = oracle.prgd_step(T, pr.idx, y, pr.n, pr.r, 1.0)
+    got = ctx.get_cores()
+    err = oracle.tt_diff_norm(got, T)
+    assert err <= 1e-8, err
+    res = ctx.residual_norm()
+    ref = float(np.linalg.norm(oracle.residual(T, pr.idx, y)))
+    assert abs(res - ref) <= 1e-8 * max(ref, 1e-300) + 1e-14 * np.linalg.norm(y)
+    ctx.close()
+
+
+def test_rules_rgd_fixed_raw(pkg):
+    pr, y, init = problem(2, 50_000)
+    for kw in [dict(eps_rule="none"), dict(eps_rule="fixed", eps_value=0.37),
+               dict(eps_rule="vee", step_rule="raw")]:
+        ctx = context(pkg, pr, y, init)
+        ctx.set_metric(kw.get("eps_rule", "vee"), kw.get("eps_value", 0.0), kw.get("step_rule", "theory"))
+        step = 0.5 if kw.get("step_rule") == "raw" else 1.0
+        ctx.step(step)
+        ref = oracle.prgd_step(init, pr.idx, y, pr.n, pr.r, step, **kw)
+        assert oracle.tt_diff_norm(ctx.get_cores(), ref) <= 1e-11, kw
+        ctx.close()
+
+
+def test_exact_fit_is_noop_and_edge_cases(pkg):
+    pr, _, init = problem(1)
+    y = oracle.eval_at(init, pr.idx)          # G = 0 at the init -> eps = 0 -> no-op (R4)
+    ctx = context(pkg, pr, y, init)
+    ctx.step(1.0)
+    for k in range(pr.d):
+        np.testing.assert_array_equal(ctx.get_core(k), init[k])
+    ctx.close()
+    # out-of-range observation index
+    ctx = pkg.TTContext(pr.n, pr.r)
+    bad = pr.idx.copy()
+    bad[5, 1] = pr.n[1]
+    with pytest.raises(pkg.PRGDError) as ei:
+        ctx.set_observations(bad, y)
+    assert ei.value.code == pkg.TT_ERR_INDEX
+    # empty Omega: residual 0, step refused
+    ctx.set_observations(np.zeros((0, pr.d), np.int32), np.zeros(0))
+    ctx.set_cores(init)
+    assert ctx.residual_norm() == 0.0
+    with pytest.raises(pkg.PRGDError) as ei:
+        ctx.step(1.0)
+    assert ei.value.code == pkg.TT_ERR_STATE
+    assert ctx.eval_at(np.zeros((0, pr.d), np.int32)).shape == (0,)
+    with pytest.raises(pkg.PRGDError) as ei:
+        ctx.eval_at(bad[:10])
+    assert ei.value.code == pkg.TT_ERR_INDEX
+    ctx.close()
+    # stepping before cores are set
+    ctx = pkg.TTContext(pr.n, pr.r)
+    ctx.set_observations(pr.idx, y)
+    with pytest.raises(pkg.PRGDError) as ei:
+        ctx.step(1.0)
+    assert ei.value.code == pkg.TT_ERR_STATE
+    ctx.close()
+
+
+def test_single_sample_and_matrix_case(pkg):
+    # degenerate sizes: d = 2 (matrix completion), one observed entry
+    rng = np.random.default_rng(3)
+    n, r = (7, 5), (1, 2, 1)
+    cores = [rng.standard_normal((r[k], n[k], r[k + 1])) for k in range(2)]
+    idx = np.array([[3, 4]], dtype=np.int32)
+    y = np.array([0.25])
+    ctx = pkg.TTContext(n, r)
+    ctx.set_observations(idx, y)
+    ctx.set_cores(cores)
+    ctx.step(1.0)
+    ref = oracle.prgd_step(cores, idx, y, n, r, 1.0)
+    assert oracle.tt_diff_norm(ctx.get_cores(), ref) <= 1e-11
+    ctx.close()
