@@ -140,11 +140,22 @@ def test_rules_rgd_fixed_raw(pkg):
 
 def test_exact_fit_is_noop_and_edge_cases(pkg):
     pr, _, init = problem(1)
-    y = oracle.eval_at(init, pr.idx)          # G = 0 at the init -> eps = 0 -> no-op (R4)
-    ctx = context(pkg, pr, y, init)
+    # Integer cores: every chain product is exact in fp64 in any order, so G = 0
+    # exactly on both sides -> eps = 0 -> the step is a no-op (reading R4).
+    rng = np.random.default_rng(5)
+    icores = [rng.integers(-2, 3, size=c.shape).astype(np.float64) for c in init]
+    yi = oracle.eval_at(icores, pr.idx)
+    ctx = context(pkg, pr, yi, icores)
+    assert ctx.residual_norm() == 0.0
     ctx.step(1.0)
     for k in range(pr.d):
-        np.testing.assert_array_equal(ctx.get_core(k), init[k])
+        np.testing.assert_array_equal(ctx.get_core(k), icores[k])
+    ctx.close()
+    # y = T_l(Omega) up to rounding: eps is tiny but nonzero; the tensor moves <= 1e-13
+    y = oracle.eval_at(init, pr.idx)
+    ctx = context(pkg, pr, y, init)
+    ctx.step(1.0)
+    assert oracle.tt_diff_norm(ctx.get_cores(), init) <= 1e-13
     ctx.close()
     # out-of-range observation index
     ctx = pkg.TTContext(pr.n, pr.r)
