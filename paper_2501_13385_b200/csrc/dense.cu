@@ -1,130 +1,234 @@
-// dense.cu — the small, sequential dense work of one PRGD iteration, each sweep in a
-// single persistent CTA (no host round trips, graph-capturable):
+// dense.cu — the small dense work of one PRGD iteration.
 //
-//   k_dense_orth   A4 That = W^{1/2} T (Prop. 3.1),
+//   k_dense_orth   (1 CTA)  A4 That = W^{1/2} T (Prop. 3.1),
 //                  A5 left-orthogonal U by a Householder QR sweep,
-//                  A6 right Grams P_k = That^{>=k+1} That^{>=k+1 T} + Cholesky.
-//   k_dense_round  A10 closed-form projection, A11 unweighting
-//                  (PAPER.md:293, 360), A13 rank-2r TT of W_l,
-//                  A14 TT-rounding = Alg. 1 on W_l: right-to-left
-//                  Householder QR, then left-to-right QR + one-sided Jacobi SVD.
+//                  A6 right Grams P_k = That^{>=k+1} That^{>=k+1 T} and their Cholesky
+//                  factors.
+//   k_project      (d CTAs, one per core, independent) A10 closed-form projection
+//                  (PAPER.md:356-360), A11 unweighting and A13 the
+//                  rank-2r cores B_k of W_l = T_l - alpha grad.
+//   k_dense_round  (1 CTA)  A14 TT-rounding = Alg. 1 on W_l:
+//                  right-to-left Householder QR, then left-to-right QR + one-sided
+//                  Jacobi SVD keeping the top r_k left singular vectors.
 //
-// Householder reflectors follow LAPACK dgeqr2/dorg2r conventions (beta = -sign(alpha)
-// ||x||, tau = (beta - alpha)/beta, v_j = 1; tau = 0 when the sub-column is zero).
-// Matrices are staged in shared memory when they fit, else processed in the global
-// scratch area (same code through MatView).
+// Householder QR (LAPACK dgeqr2 / dorg2r conventions: beta = -sign(alpha)||x||,
+// tau = (beta - alpha)/beta, v_j = 1, tau = 0 for a zero sub-column) with rows owned
+// by threads (row i by thread i mod blockDim) and two block barriers per column:
+// per-thread column partials are reduced across the warp by a transpose-reduction
+// (31 shuffles for 32 columns) and across warps through shared memory.  Matrices are
+// staged in shared memory (odd row stride: conflict-free column access) when they
+// fit, else processed in a global scratch area by the same code.
 #include "prgd_internal.cuh"
 
 namespace prgd {
 namespace {
 
-struct MatView {
-  double* p;
-  int64_t rs, cs;
-  __device__ __forceinline__ double& at(int i, int j) const { return p[i * rs + j * cs]; }
+constexpr int kNW = kDenseThreads / 32;
+constexpr int kMaxCols = 2 * kMaxRank;   // 64
+
+__device__ __forceinline__ double shx(double v, int o) { return __shfl_xor_sync(0xffffffffu, v, o); }
+
+// Warp transpose-reduction of NM per-lane values: afterwards lane l holds the warp
+// total of index (l & (NM-1)) in o0 (NM <= 32), or of indices l and l+32 (NM = 64).
+template <int NM>
+__device__ __forceinline__ void warp_treduce(double (&v)[NM], int lane, double& o0, double& o1) {
+  if constexpr (NM == 64) {
+    double a[32], b[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      a[i] = v[i];
+      b[i] = v[i + 32];
+    }
+    double t;
+    warp_treduce<32>(a, lane, o0, t);
+    warp_treduce<32>(b, lane, o1, t);
+  } else {
+#pragma unroll
+    for (int off = 16; off >= NM; off >>= 1) {
+#pragma unroll
+      for (int i = 0; i < NM; ++i) v[i] += shx(v[i], off);
+    }
+#pragma unroll
+    for (int off = NM / 2; off >= 1; off >>= 1) {
+      const bool up = (lane & off) != 0;
+#pragma unroll
+      for (int i = 0; i < off; ++i) {
+        const double send = up ? v[i] : v[i + off];
+        const double keep = up ? v[i + off] : v[i];
+        v[i] = keep + shx(send, off);
+      }
+    }
+    o0 = v[0];
+    o1 = 0.0;
+  }
+}
+
+struct Work {
+  double* red;   // [kNW][kMaxCols] warp partials
+  double* vec;   // [kMaxCols] per-column coefficients
+  double* sc3;   // [4] tau, denom, beta
+  double* tau;   // [kMaxCols]
+  double* S1;    // S x S
+  double* S2;
+  double* S3;
+  int* perm;     // [S]
+  double* mat;   // staging area
+  int64_t mat_cap;
 };
 
-// Householder QR in place; tau[kmin].  red: >= blockDim.x doubles; colv: >= 2*n doubles.
-__device__ void blk_geqr2(MatView A, int m, int n, double* tau, double* red, double* colv) {
-  const int T = blockDim.x, tid = threadIdx.x;
+__device__ Work carve(double* sm, int smem_doubles, int S) {
+  Work w;
+  double* p = sm;
+  w.red = p; p += kNW * kMaxCols;
+  w.vec = p; p += kMaxCols;
+  w.sc3 = p; p += 4;
+  w.tau = p; p += kMaxCols;
+  w.S1 = p; p += S * S;
+  w.S2 = p; p += S * S;
+  w.S3 = p; p += S * S;
+  w.perm = reinterpret_cast<int*>(p); p += (S + 1) / 2 + 1;
+  w.mat = p;
+  w.mat_cap = smem_doubles - (int64_t)(p - sm);
+  return w;
+}
+
+// Householder QR in place of the m x n row-major matrix A (row stride ld).
+template <int NM>
+__device__ void qr_rows(double* A, int ld, int m, int n, const Work& w) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int T = blockDim.x;
   const int kmin = m < n ? m : n;
-  double* colsum = colv;        // [n]
-  double* wv = colv + n;        // [n]
-  __shared__ double s_tau, s_denom, s_beta;
   for (int j = 0; j < kmin; ++j) {
-    const int nc = n - j;
-    const int G = T / nc;
-    const int q = tid % nc, g = tid / nc;
-    double s = 0.0;
-    if (g < G)
-      for (int i = j + 1 + g; i < m; i += G) s = fma(A.at(i, j), A.at(i, j + q), s);
-    red[tid] = (g < G) ? s : 0.0;
+    double p[NM];
+#pragma unroll
+    for (int c = 0; c < NM; ++c) p[c] = 0.0;
+    for (int i = tid; i < m; i += T) {
+      if (i <= j) continue;
+      const double* row = A + (int64_t)i * ld;
+      const double aij = row[j];
+#pragma unroll
+      for (int c = 0; c < NM; ++c)
+        if (c >= j && c < n) p[c] = fma(aij, row[c], p[c]);
+    }
+    double o0, o1;
+    warp_treduce<NM>(p, lane, o0, o1);
+    if (lane < NM) w.red[warp * kMaxCols + lane] = o0;
+    if (NM == 64) w.red[warp * kMaxCols + 32 + lane] = o1;
     __syncthreads();
-    if (tid < nc) {
-      double acc = 0.0;
-      for (int gg = 0; gg < G; ++gg) acc += red[gg * nc + tid];
-      colsum[tid] = acc;
+    if (warp == 0) {
+      double cs0 = 0.0, cs1 = 0.0;
+      for (int ww = 0; ww < kNW; ++ww) {
+        if (lane < NM) cs0 += w.red[ww * kMaxCols + lane];
+        if (NM == 64) cs1 += w.red[ww * kMaxCols + 32 + lane];
+      }
+      const double xb2 = (j < 32) ? __shfl_sync(0xffffffffu, cs0, j & 31)
+                                  : __shfl_sync(0xffffffffu, cs1, j & 31);
+      const double alpha = A[(int64_t)j * ld + j];
+      double tau = 0.0, denom = 0.0, beta = alpha;
+      if (xb2 != 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + xb2), alpha);
+        tau = (beta - alpha) / beta;
+        denom = 1.0 / (alpha - beta);
+      }
+      const double* rj = A + (int64_t)j * ld;
+      if (lane > j && lane < n) w.vec[lane] = tau * (rj[lane] + cs0 * denom);
+      if (NM == 64 && lane + 32 > j && lane + 32 < n) w.vec[lane + 32] = tau * (rj[lane + 32] + cs1 * denom);
+      if (lane == 0) {
+        w.sc3[0] = tau;
+        w.sc3[1] = denom;
+        w.sc3[2] = beta;
+        w.tau[j] = tau;
+      }
     }
     __syncthreads();
-    if (tid == 0) {
-      const double alpha = A.at(j, j);
-      const double xb2 = colsum[0];
-      if (xb2 == 0.0) {
-        s_tau = 0.0;
-        s_denom = 0.0;
-        s_beta = alpha;
-      } else {
-        const double beta = -copysign(sqrt(alpha * alpha + xb2), alpha);
-        s_tau = (beta - alpha) / beta;
-        s_denom = 1.0 / (alpha - beta);
-        s_beta = beta;
+    const double tau = w.sc3[0];
+    if (tau != 0.0) {
+      const double denom = w.sc3[1], beta = w.sc3[2];
+      for (int i = tid; i < m; i += T) {
+        if (i < j) continue;
+        double* row = A + (int64_t)i * ld;
+        const double v = (i == j) ? 1.0 : row[j] * denom;
+        for (int c = j + 1; c < n; ++c) row[c] = fma(-v, w.vec[c], row[c]);
+        row[j] = (i == j) ? beta : v;
       }
-      tau[j] = s_tau;
-    }
-    __syncthreads();
-    const double tj = s_tau, dn = s_denom;
-    if (tj != 0.0) {
-      if (tid < nc - 1) {
-        const int c = j + 1 + tid;
-        wv[c] = A.at(j, c) + colsum[1 + tid] * dn;
-      }
-      __syncthreads();
-      const int ncr = nc - 1;
-      if (ncr > 0) {
-        const int64_t tot = (int64_t)(m - j) * ncr;
-        for (int64_t e = tid; e < tot; e += T) {
-          const int i = j + (int)(e / ncr);
-          const int c = j + 1 + (int)(e % ncr);
-          const double vi = (i == j) ? 1.0 : A.at(i, j) * dn;
-          A.at(i, c) -= tj * vi * wv[c];
-        }
-      }
-      __syncthreads();
-      for (int i = j + 1 + tid; i < m; i += T) A.at(i, j) *= dn;
-      if (tid == 0) A.at(j, j) = s_beta;
-      __syncthreads();
     }
   }
+  __syncthreads();
 }
 
-// Form the m x k Q (k = #reflectors) in place over the first k columns (dorg2r).
-__device__ void blk_org2r(MatView A, int m, int k, const double* tau, double* red, double* colv) {
-  const int T = blockDim.x, tid = threadIdx.x;
-  double* colsum = colv;
+// Form Q (m x k, k = min(m, n) reflectors) in place over the first k columns (dorg2r).
+template <int NM>
+__device__ void orgqr_rows(double* A, int ld, int m, int k, const Work& w) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int T = blockDim.x;
   for (int j = k - 1; j >= 0; --j) {
-    const double tj = tau[j];
-    const int nc = k - 1 - j;  // columns j+1..k-1
-    if (nc > 0 && tj != 0.0) {
-      const int G = T / nc;
-      const int q = tid % nc, g = tid / nc;
-      double s = 0.0;
-      if (g < G)
-        for (int i = j + 1 + g; i < m; i += G) s = fma(A.at(i, j), A.at(i, j + 1 + q), s);
-      red[tid] = (g < G) ? s : 0.0;
+    const double tj = w.tau[j];
+    if (j < k - 1 && tj != 0.0) {
+      double p[NM];
+#pragma unroll
+      for (int c = 0; c < NM; ++c) p[c] = 0.0;
+      for (int i = tid; i < m; i += T) {
+        if (i <= j) continue;
+        const double* row = A + (int64_t)i * ld;
+        const double aij = row[j];
+#pragma unroll
+        for (int c = 0; c < NM; ++c)
+          if (c > j && c < k) p[c] = fma(aij, row[c], p[c]);
+      }
+      double o0, o1;
+      warp_treduce<NM>(p, lane, o0, o1);
+      if (lane < NM) w.red[warp * kMaxCols + lane] = o0;
+      if (NM == 64) w.red[warp * kMaxCols + 32 + lane] = o1;
       __syncthreads();
-      if (tid < nc) {
-        double acc = 0.0;
-        for (int gg = 0; gg < G; ++gg) acc += red[gg * nc + tid];
-        colsum[tid] = (A.at(j, j + 1 + tid) + acc) * tj;   // tau * w_c
+      if (warp == 0) {
+        double cs0 = 0.0, cs1 = 0.0;
+        for (int ww = 0; ww < kNW; ++ww) {
+          if (lane < NM) cs0 += w.red[ww * kMaxCols + lane];
+          if (NM == 64) cs1 += w.red[ww * kMaxCols + 32 + lane];
+        }
+        const double* rj = A + (int64_t)j * ld;
+        if (lane > j && lane < k) w.vec[lane] = (rj[lane] + cs0) * tj;
+        if (NM == 64 && lane + 32 > j && lane + 32 < k) w.vec[lane + 32] = (rj[lane + 32] + cs1) * tj;
       }
       __syncthreads();
-      const int64_t tot = (int64_t)(m - j) * nc;
-      for (int64_t e = tid; e < tot; e += T) {
-        const int i = j + (int)(e / nc);
-        const int c = j + 1 + (int)(e % nc);
-        const double vi = (i == j) ? 1.0 : A.at(i, j);
-        A.at(i, c) -= vi * colsum[c - j - 1];
+      for (int i = tid; i < m; i += T) {
+        if (i < j) continue;
+        double* row = A + (int64_t)i * ld;
+        const double v = (i == j) ? 1.0 : row[j];
+        for (int c = j + 1; c < k; ++c) row[c] = fma(-v, w.vec[c], row[c]);
       }
-      __syncthreads();
     }
-    for (int i = j + 1 + tid; i < m; i += T) A.at(i, j) *= -tj;
-    for (int i = tid; i < j; i += T) A.at(i, j) = 0.0;
-    if (tid == 0) A.at(j, j) = 1.0 - tj;
-    __syncthreads();
+    for (int i = tid; i < m; i += T) {
+      double* row = A + (int64_t)i * ld;
+      if (i > j) row[j] *= -tj;
+      else if (i == j) row[j] = 1.0 - tj;
+      else row[j] = 0.0;
+    }
   }
+  __syncthreads();
 }
 
-// In-place Cholesky of the R x R SPD matrix P (row-major), lower factor; returns false on
+// QR of the m x n matrix staged at A (stride ld): R (kmin x n, row-major, zeros below
+// the diagonal) into Rout, Q in place over the first kmin columns.  Returns kmin.
+__device__ int qr_explicit(double* A, int ld, int m, int n, double* Rout, const Work& w) {
+  const int kmin = m < n ? m : n;
+  if (n <= 8) qr_rows<8>(A, ld, m, n, w);
+  else if (n <= 16) qr_rows<16>(A, ld, m, n, w);
+  else if (n <= 32) qr_rows<32>(A, ld, m, n, w);
+  else qr_rows<64>(A, ld, m, n, w);
+  for (int e = threadIdx.x; e < kmin * n; e += blockDim.x) {
+    const int a = e / n, b = e - a * n;
+    Rout[e] = b >= a ? A[(int64_t)a * ld + b] : 0.0;
+  }
+  __syncthreads();
+  if (kmin <= 8) orgqr_rows<8>(A, ld, m, kmin, w);
+  else if (kmin <= 16) orgqr_rows<16>(A, ld, m, kmin, w);
+  else if (kmin <= 32) orgqr_rows<32>(A, ld, m, kmin, w);
+  else orgqr_rows<64>(A, ld, m, kmin, w);
+  return kmin;
+}
+
+// In-place Cholesky of the R x R SPD matrix P (row-major), lower factor; false on
 // breakdown (block-uniform).
 __device__ bool blk_chol(double* P, int R) {
   __shared__ int s_ok;
@@ -149,16 +253,15 @@ __device__ bool blk_chol(double* P, int R) {
     __syncthreads();
   }
   for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    int i = e / R, c = e % R;
+    const int i = e / R, c = e - i * R;
     if (c > i) P[e] = 0.0;
   }
   __syncthreads();
   return s_ok != 0;
 }
 
-// One-sided Jacobi on the columns of X (rows x kc, column-major: X[c*rows + i]),
-// accumulating V (kc x kc, column-major).  Round-robin parallel ordering, one warp
-// per pair.  Returns false if not converged.
+// One-sided Jacobi on the columns of X (rows x kc, column-major X[c*rows + i]),
+// accumulating V (kc x kc, column-major); round-robin ordering, one warp per pair.
 __device__ bool blk_jacobi(double* X, int rows, int kc, double* V) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   __shared__ int s_rot;
@@ -173,40 +276,41 @@ __device__ bool blk_jacobi(double* X, int rows, int kc, double* V) {
     __syncthreads();
     for (int round = 0; round < kp - 1; ++round) {
       for (int pr = warp; pr < npairs; pr += nw) {
-        auto pos = [&](int i) { return i == 0 ? 0 : ((i - 1 + round) % (kp - 1)) + 1; };
-        int a = pos(pr), b = pos(kp - 1 - pr);
-        if (a > b) { int t = a; a = b; b = t; }
+        int a = pr == 0 ? 0 : ((pr - 1 + round) % (kp - 1)) + 1;
+        const int q = kp - 1 - pr;
+        int b = q == 0 ? 0 : ((q - 1 + round) % (kp - 1)) + 1;
+        if (a > b) { const int t = a; a = b; b = t; }
         if (b >= kc) continue;
         double* xa = X + (int64_t)a * rows;
         double* xb = X + (int64_t)b * rows;
         double al = 0.0, be = 0.0, ga = 0.0;
         for (int i = lane; i < rows; i += 32) {
-          const double u = xa[i], w = xb[i];
+          const double u = xa[i], v = xb[i];
           al = fma(u, u, al);
-          be = fma(w, w, be);
-          ga = fma(u, w, ga);
+          be = fma(v, v, be);
+          ga = fma(u, v, ga);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-          al += __shfl_xor_sync(0xffffffffu, al, o);
-          be += __shfl_xor_sync(0xffffffffu, be, o);
-          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+          al += shx(al, o);
+          be += shx(be, o);
+          ga += shx(ga, o);
         }
         if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
           const double zeta = (be - al) / (2.0 * ga);
           const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
           for (int i = lane; i < rows; i += 32) {
-            const double u = xa[i], w = xb[i];
-            xa[i] = c * u - s * w;
-            xb[i] = s * u + c * w;
+            const double u = xa[i], v = xb[i];
+            xa[i] = c * u - s * v;
+            xb[i] = s * u + c * v;
           }
           double* va = V + (int64_t)a * kc;
           double* vb = V + (int64_t)b * kc;
           for (int i = lane; i < kc; i += 32) {
-            const double u = va[i], w = vb[i];
-            va[i] = c * u - s * w;
-            vb[i] = s * u + c * w;
+            const double u = va[i], v = vb[i];
+            va[i] = c * u - s * v;
+            vb[i] = s * u + c * v;
           }
           if (lane == 0) s_rot = 1;
         }
@@ -220,116 +324,34 @@ __device__ bool blk_jacobi(double* X, int rows, int kc, double* V) {
   return false;
 }
 
-struct Smem {
-  double* red;    // blockDim
-  double* colv;   // 2*kMaxCols
-  double* tau;    // kMaxCols
-  double* small1; // S x S
-  double* small2; // S x S
-  double* small3; // S x S
-  int* perm;      // S
-  double* mat;    // staging area
-  int64_t mat_cap;
-};
-
-constexpr int kMaxCols = 2 * kMaxRank;
-
-__device__ Smem carve(double* sm, int smem_doubles, int S) {
-  Smem s;
-  double* p = sm;
-  s.red = p; p += kDenseThreads;
-  s.colv = p; p += 2 * kMaxCols;
-  s.tau = p; p += kMaxCols;
-  s.small1 = p; p += S * S;
-  s.small2 = p; p += S * S;
-  s.small3 = p; p += S * S;
-  s.perm = reinterpret_cast<int*>(p); p += (S + 1) / 2 + 1;
-  s.mat = p;
-  s.mat_cap = smem_doubles - (int64_t)(p - sm);
-  return s;
-}
-
-// Copy a (rows x cols) strided view into a compact row-major destination.
-__device__ void blk_copy_in(double* dst, const double* src, int rows, int cols, int64_t rs,
-                            int64_t cs) {
-  const int64_t tot = (int64_t)rows * cols;
-  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
-    int i = (int)(e / cols), j = (int)(e % cols);
-    dst[e] = src[i * rs + j * cs];
-  }
-}
-
 __device__ void blk_copy(double* dst, const double* src, int64_t n) {
   for (int64_t e = threadIdx.x; e < n; e += blockDim.x) dst[e] = src[e];
 }
 
-// Mode-1 product: out[a', rest] = sum_b M[a', b] in[b, rest]; M (ra x rb) row-major.
+// out[a', x] = sum_b M[a', b] in[b, x]  (M: ra x rb row-major; in: rb x rest)
 __device__ void blk_mode1(double* out, const double* M, int ra, int rb, const double* in,
-                          int64_t rest) {
-  const int64_t tot = (int64_t)ra * rest;
-  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
-    const int a = (int)(e / rest);
-    const int64_t x = e - (int64_t)a * rest;
+                          int rest) {
+  const int tot = ra * rest;
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int a = e / rest, x = e - a * rest;
     double acc = 0.0;
     for (int b = 0; b < rb; ++b) acc = fma(M[a * rb + b], in[(int64_t)b * rest + x], acc);
     out[e] = acc;
   }
 }
 
-// Mode-3 product with M^T: out[row, c'] = sum_b in[row, b] M[c', b]; M (rc x rb) row-major.
-__device__ void blk_mode3t(double* out, const double* in, int64_t rows, int rb, const double* M,
-                           int rc) {
-  const int64_t tot = rows * rc;
-  for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
-    const int64_t row = e / rc;
-    const int c = (int)(e - row * rc);
+// out[row, c'] = sum_b in[row, b] M[c', b]  (M: rc x rb row-major)
+__device__ void blk_mode3t(double* out, const double* in, int rows, int rb, const double* M, int rc) {
+  const int tot = rows * rc;
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int row = e / rc, c = e - row * rc;
     double acc = 0.0;
-    for (int b = 0; b < rb; ++b) acc = fma(in[row * rb + b], M[c * rb + b], acc);
+    for (int b = 0; b < rb; ++b) acc = fma(in[(int64_t)row * rb + b], M[c * rb + b], acc);
     out[e] = acc;
   }
 }
 
-// QR of a compact row-major (m x n) matrix at `g` (global).  Stages into smem when it
-// fits.  On return: R (kmin x n, row-major, zero below diag) in Rout, Q (m x kmin,
-// row-major compact) at Qout (may alias g).  Returns kmin.
-__device__ int blk_qr_explicit(const Smem& sm, double* g, int m, int n, double* Rout,
-                               double* Qout, double* gwork) {
-  const int kmin = m < n ? m : n;
-  const int64_t sz = (int64_t)m * n;
-  double* A = (sz <= sm.mat_cap) ? sm.mat : gwork;
-  if (A != g) {
-    blk_copy(A, g, sz);
-    __syncthreads();
-  }
-  MatView V{A, n, 1};
-  blk_geqr2(V, m, n, sm.tau, sm.red, sm.colv);
-  for (int64_t e = threadIdx.x; e < (int64_t)kmin * n; e += blockDim.x) {
-    int a = (int)(e / n), b = (int)(e % n);
-    Rout[e] = b >= a ? V.at(a, b) : 0.0;
-  }
-  __syncthreads();
-  blk_org2r(V, m, kmin, sm.tau, sm.red, sm.colv);
-  // compact Q (m x kmin) from the leading columns
-  if (Qout != A || kmin != n) {
-    // write row-major m x kmin; when Qout aliases A and kmin < n, rows shrink: do it in
-    // increasing order after a barrier-separated copy through the red buffer per row.
-    if (Qout == A) {
-      for (int i = 0; i < m; ++i) {
-        double v = threadIdx.x < kmin ? A[(int64_t)i * n + threadIdx.x] : 0.0;
-        __syncthreads();
-        if (threadIdx.x < kmin) Qout[(int64_t)i * kmin + threadIdx.x] = v;
-        __syncthreads();
-      }
-    } else {
-      for (int64_t e = threadIdx.x; e < (int64_t)m * kmin; e += blockDim.x) {
-        int i = (int)(e / kmin), c = (int)(e % kmin);
-        Qout[e] = A[(int64_t)i * n + c];
-      }
-    }
-  }
-  __syncthreads();
-  return kmin;
-}
+__device__ __forceinline__ int odd_ld(int n) { return n | 1; }
 
 __global__ void __launch_bounds__(kDenseThreads) k_dense_orth(DenseArgs a) {
   extern __shared__ double smraw[];
@@ -338,79 +360,84 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_orth(DenseArgs a) {
   const int d = a.d;
   int S = 2;
   for (int k = 0; k <= d; ++k) S = a.r[k] > S ? a.r[k] : S;
-  Smem sm = carve(smraw, a.smem_doubles, S);
+  Work w = carve(smraw, a.smem_doubles, S);
   // A4: U_k = phi_k (.)_2 C_k
   for (int k = 0; k < d; ++k) {
     const int r0 = a.r[k], nk = a.n[k], r1 = a.r[k + 1];
-    const int64_t tot = (int64_t)r0 * nk * r1;
+    const int tot = r0 * nk * r1;
     const double* C = a.C + a.core_off[k];
     double* U = a.U + a.core_off[k];
     const double* ph = a.phi + a.phi_off[k];
-    for (int64_t e = threadIdx.x; e < tot; e += blockDim.x) {
-      const int j = (int)((e / r1) % nk);
-      U[e] = C[e] * ph[j];
-    }
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) U[e] = C[e] * ph[(e / r1) % nk];
   }
   __syncthreads();
-  // A5: Householder QR sweep, U_k <- Q, U_{k+1} <- R U_{k+1}
+  // A5: U_k <- Q, U_{k+1} <- R U_{k+1}
   double* gw = a.work;
   for (int k = 0; k + 1 < d; ++k) {
     const int r0 = a.r[k], nk = a.n[k], r1 = a.r[k + 1];
     const int m = r0 * nk;
     double* U = a.U + a.core_off[k];
-    double* R = sm.small1;
-    blk_qr_explicit(sm, U, m, r1, R, U, gw);   // kmin = r1 (feasible ranks); Q -> U
-    double* Un = a.U + a.core_off[k + 1];
-    const int64_t rest = (int64_t)a.n[k + 1] * a.r[k + 2];
-    blk_mode1(gw, R, r1, r1, Un, rest);
-    __syncthreads();
-    blk_copy(Un, gw, (int64_t)r1 * rest);
-    __syncthreads();
-  }
-  // A6: P_{d-1} = [1]; P_k = sum_j U_{k+1}(:,j,:) P_{k+1} U_{k+1}(:,j,:)^T, Cholesky.
-  {
-    double* P = a.P + a.p_off[d - 1];
-    double* L = a.L + a.p_off[d - 1];
-    if (threadIdx.x == 0) {
-      P[0] = 1.0;
-      L[0] = 1.0;
+    int ld = odd_ld(r1);
+    double* A = w.mat;
+    if ((int64_t)m * ld > w.mat_cap) {
+      A = gw;
+      ld = r1;
+    }
+    for (int e = threadIdx.x; e < m * r1; e += blockDim.x) {
+      const int i = e / r1, c = e - i * r1;
+      A[(int64_t)i * ld + c] = U[e];
     }
     __syncthreads();
+    qr_explicit(A, ld, m, r1, w.S1, w);   // kmin = r1 (feasible ranks)
+    for (int e = threadIdx.x; e < m * r1; e += blockDim.x) {
+      const int i = e / r1, c = e - i * r1;
+      U[e] = A[(int64_t)i * ld + c];
+    }
+    double* Un = a.U + a.core_off[k + 1];
+    const int rest = a.n[k + 1] * a.r[k + 2];
+    double* tmp = (A == gw) ? gw + (int64_t)m * ld : gw;
+    blk_mode1(tmp, w.S1, r1, r1, Un, rest);
+    __syncthreads();
+    blk_copy(Un, tmp, (int64_t)r1 * rest);
+    __syncthreads();
   }
+  // A6: P_{d-1} = [1]; P_k = sum_j U_{k+1}(:,j,:) P_{k+1} U_{k+1}(:,j,:)^T; Cholesky.
+  if (threadIdx.x == 0) {
+    a.P[a.p_off[d - 1]] = 1.0;
+    a.L[a.p_off[d - 1]] = 1.0;
+  }
+  __syncthreads();
   bool ok = true;
   for (int k = d - 2; k >= 0; --k) {
     const int R1 = a.r[k + 1], nk = a.n[k + 1], R2 = a.r[k + 2];
     const double* Un = a.U + a.core_off[k + 1];
     const double* Pn = a.P + a.p_off[k + 1];
-    // T1[a, j, e] = sum_c U[a, j, c] Pn[c, e]  (into gw)
-    const int64_t t1 = (int64_t)R1 * nk * R2;
-    for (int64_t e = threadIdx.x; e < t1; e += blockDim.x) {
-      const int ee = (int)(e % R2);
-      const int64_t aj = e / R2;
+    const int t1 = R1 * nk * R2;
+    double* T1 = gw;
+    for (int e = threadIdx.x; e < t1; e += blockDim.x) {
+      const int aj = e / R2, ee = e - aj * R2;
       double acc = 0.0;
       for (int c = 0; c < R2; ++c) acc = fma(Un[aj * R2 + c], Pn[c * R2 + ee], acc);
-      gw[e] = acc;
+      T1[e] = acc;
     }
     __syncthreads();
     double* P = a.P + a.p_off[k];
+    const int len = nk * R2;
     for (int e = threadIdx.x; e < R1 * R1; e += blockDim.x) {
-      const int aa = e / R1, bb = e % R1;
+      const int aa = e / R1, bb = e - aa * R1;
       double acc = 0.0;
-      const int64_t len = (int64_t)nk * R2;
-      for (int64_t q = 0; q < len; ++q) acc = fma(gw[aa * len + q], Un[bb * len + q], acc);
+      for (int q = 0; q < len; ++q) acc = fma(T1[aa * len + q], Un[bb * len + q], acc);
       P[e] = acc;
     }
     __syncthreads();
-    // symmetrise (exact symmetry for the Cholesky input)
-    double* Ls = sm.small1;
+    double* Ls = w.S1;
     for (int e = threadIdx.x; e < R1 * R1; e += blockDim.x) {
-      const int aa = e / R1, bb = e % R1;
+      const int aa = e / R1, bb = e - aa * R1;
       Ls[e] = 0.5 * (P[aa * R1 + bb] + P[bb * R1 + aa]);
     }
     __syncthreads();
     ok = blk_chol(Ls, R1) && ok;
-    double* L = a.L + a.p_off[k];
-    blk_copy(L, Ls, (int64_t)R1 * R1);
+    blk_copy(a.L + a.p_off[k], Ls, (int64_t)R1 * R1);
     __syncthreads();
   }
   if (!ok && threadIdx.x == 0) {
@@ -419,99 +446,116 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_orth(DenseArgs a) {
   }
 }
 
+// One CTA per core k: projection (A10), unweighting (A11), assembly of B_k (A13).
+__global__ void __launch_bounds__(kDenseThreads) k_project(DenseArgs a) {
+  extern __shared__ double smraw[];
+  Scalars* sc = a.sc;
+  if (sc->noop) return;
+  const int d = a.d, k = blockIdx.x;
+  const double alpha = sc->alpha;
+  const int r0 = a.r[k], nk = a.n[k], r1 = a.r[k + 1];
+  const int m = r0 * nk;
+  const double* Y = a.Y + a.core_off[k];
+  const double* U = a.U + a.core_off[k];
+  double* Ah = a.Ahat + a.core_off[k];
+  if (k == d - 1) {
+    blk_copy(Ah, Y, (int64_t)m * r1);
+    __syncthreads();
+  } else {
+    double* Ls = smraw;                       // r1 x r1
+    double* W = Ls + r1 * r1;                 // r1 x r1
+    double* Z = W + r1 * r1;                  // m x ld (staged) or Ah
+    const int ld = odd_ld(r1);
+    const bool stage = (int64_t)m * ld * 2 + 2 * r1 * r1 <= a.smem_doubles;
+    double* Us = stage ? Z + (int64_t)m * ld : nullptr;
+    const int zld = stage ? ld : r1;
+    if (!stage) Z = Ah;
+    blk_copy(Ls, a.L + a.p_off[k], (int64_t)r1 * r1);
+    if (stage)
+      for (int e = threadIdx.x; e < m * r1; e += blockDim.x) {
+        const int i = e / r1, c = e - i * r1;
+        Us[(int64_t)i * ld + c] = U[e];
+      }
+    __syncthreads();
+    // Z = L(Y_k) P_k^{-1}: per row, forward then back substitution with L L^T
+    for (int row = threadIdx.x; row < m; row += blockDim.x) {
+      const double* y = Y + (int64_t)row * r1;
+      double* z = Z + (int64_t)row * zld;
+      for (int i = 0; i < r1; ++i) {
+        double s = y[i];
+        for (int c = 0; c < i; ++c) s = fma(-Ls[i * r1 + c], z[c], s);
+        z[i] = s / Ls[i * r1 + i];
+      }
+      for (int i = r1 - 1; i >= 0; --i) {
+        double s = z[i];
+        for (int c = i + 1; c < r1; ++c) s = fma(-Ls[c * r1 + i], z[c], s);
+        z[i] = s / Ls[i * r1 + i];
+      }
+    }
+    __syncthreads();
+    // W = L(U_k)^T Z  (r1 x r1)
+    const double* Uv = stage ? Us : U;
+    const int uld = stage ? ld : r1;
+    for (int e = threadIdx.x; e < r1 * r1; e += blockDim.x) {
+      const int aa = e / r1, bb = e - aa * r1;
+      double acc = 0.0;
+      for (int row = 0; row < m; ++row)
+        acc = fma(Uv[(int64_t)row * uld + aa], Z[(int64_t)row * zld + bb], acc);
+      W[e] = acc;
+    }
+    __syncthreads();
+    // Ahat = Z - L(U_k) W   (when Z aliases Ah each thread reads/writes only its slot)
+    for (int e = threadIdx.x; e < m * r1; e += blockDim.x) {
+      const int row = e / r1, bb = e - row * r1;
+      double acc = 0.0;
+      for (int aa = 0; aa < r1; ++aa) acc = fma(Uv[(int64_t)row * uld + aa], W[aa * r1 + bb], acc);
+      Ah[e] = Z[(int64_t)row * zld + bb] - acc;
+    }
+    __syncthreads();
+  }
+  // A11 + A13: B_k from Ttil = U/phi and X = -alpha Ahat/phi
+  const double* ph = a.phi + a.phi_off[k];
+  double* B = a.B + a.b_off[k];
+  if (k == 0) {
+    const int Rb1 = 2 * r1;
+    for (int e = threadIdx.x; e < nk * Rb1; e += blockDim.x) {
+      const int x = e / Rb1, c = e - x * Rb1;
+      const double inv = 1.0 / ph[x];
+      B[e] = c < r1 ? -alpha * Ah[x * r1 + c] * inv : U[x * r1 + (c - r1)] * inv;
+    }
+  } else if (k == d - 1) {
+    for (int e = threadIdx.x; e < 2 * r0 * nk; e += blockDim.x) {
+      const int aa = e / nk, x = e - aa * nk;
+      const double inv = 1.0 / ph[x];
+      B[e] = aa < r0 ? U[aa * nk + x] * inv
+                     : (U[(aa - r0) * nk + x] - alpha * Ah[(aa - r0) * nk + x]) * inv;
+    }
+  } else {
+    const int Rb1 = 2 * r1;
+    const int tot = 2 * r0 * nk * Rb1;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+      const int c = e % Rb1;
+      const int x = (e / Rb1) % nk;
+      const int aa = e / (Rb1 * nk);
+      const double inv = 1.0 / ph[x];
+      double v;
+      if (aa < r0) v = c < r1 ? U[(aa * nk + x) * r1 + c] * inv : 0.0;
+      else if (c < r1) v = -alpha * Ah[((aa - r0) * nk + x) * r1 + c] * inv;
+      else v = U[((aa - r0) * nk + x) * r1 + (c - r1)] * inv;
+      B[e] = v;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
   extern __shared__ double smraw[];
   Scalars* sc = a.sc;
   if (sc->noop) return;
   const int d = a.d;
-  const double alpha = sc->alpha;
   int S = 2;
   for (int k = 0; k <= d; ++k) S = 2 * a.r[k] > S ? 2 * a.r[k] : S;
-  Smem sm = carve(smraw, a.smem_doubles, S);
+  Work w = carve(smraw, a.smem_doubles, S);
   double* gw = a.work;
-  // ---- A10: projection, A11 + A13 assembly into B
-  for (int k = 0; k < d; ++k) {
-    const int r0 = a.r[k], nk = a.n[k], r1 = a.r[k + 1];
-    const int m = r0 * nk;
-    const double* Y = a.Y + a.core_off[k];
-    double* Ah = a.Ahat + a.core_off[k];
-    const double* U = a.U + a.core_off[k];
-    if (k == d - 1) {
-      blk_copy(Ah, Y, (int64_t)m * r1);
-      __syncthreads();
-    } else {
-      const double* L = a.L + a.p_off[k];
-      double* Ls = sm.small1;
-      blk_copy(Ls, L, (int64_t)r1 * r1);
-      __syncthreads();
-      for (int row = threadIdx.x; row < m; row += blockDim.x) {
-        const double* y = Y + (int64_t)row * r1;
-        double* z = Ah + (int64_t)row * r1;
-        for (int i = 0; i < r1; ++i) {
-          double s = y[i];
-          for (int c = 0; c < i; ++c) s -= Ls[i * r1 + c] * z[c];
-          z[i] = s / Ls[i * r1 + i];
-        }
-        for (int i = r1 - 1; i >= 0; --i) {
-          double s = z[i];
-          for (int c = i + 1; c < r1; ++c) s -= Ls[c * r1 + i] * z[c];
-          z[i] = s / Ls[i * r1 + i];
-        }
-      }
-      __syncthreads();
-      double* W = sm.small2;
-      for (int e = threadIdx.x; e < r1 * r1; e += blockDim.x) {
-        const int aa = e / r1, bb = e % r1;
-        double acc = 0.0;
-        for (int row = 0; row < m; ++row) acc = fma(U[(int64_t)row * r1 + aa], Ah[(int64_t)row * r1 + bb], acc);
-        W[e] = acc;
-      }
-      __syncthreads();
-      for (int64_t e = threadIdx.x; e < (int64_t)m * r1; e += blockDim.x) {
-        const int64_t row = e / r1;
-        const int bb = (int)(e - row * r1);
-        double acc = 0.0;
-        for (int aa = 0; aa < r1; ++aa) acc = fma(U[row * r1 + aa], W[aa * r1 + bb], acc);
-        Ah[e] -= acc;
-      }
-      __syncthreads();
-    }
-    // assembly of B_k (ranks Rb[k] x n x Rb[k+1])
-    const double* ph = a.phi + a.phi_off[k];
-    double* B = a.B + a.b_off[k];
-    if (d == 1) {
-      // not reachable (d >= 2)
-    } else if (k == 0) {
-      const int Rb1 = 2 * r1;
-      for (int64_t e = threadIdx.x; e < (int64_t)nk * Rb1; e += blockDim.x) {
-        const int x = (int)(e / Rb1), c = (int)(e % Rb1);
-        const double inv = 1.0 / ph[x];
-        B[e] = c < r1 ? -alpha * Ah[x * r1 + c] * inv : U[x * r1 + (c - r1)] * inv;
-      }
-    } else if (k == d - 1) {
-      for (int64_t e = threadIdx.x; e < (int64_t)2 * r0 * nk; e += blockDim.x) {
-        const int aa = (int)(e / nk), x = (int)(e % nk);
-        const double inv = 1.0 / ph[x];
-        if (aa < r0) B[e] = U[aa * nk + x] * inv;
-        else B[e] = (U[(aa - r0) * nk + x] - alpha * Ah[(aa - r0) * nk + x]) * inv;
-      }
-    } else {
-      const int Rb0 = 2 * r0, Rb1 = 2 * r1;
-      for (int64_t e = threadIdx.x; e < (int64_t)Rb0 * nk * Rb1; e += blockDim.x) {
-        const int c = (int)(e % Rb1);
-        const int x = (int)((e / Rb1) % nk);
-        const int aa = (int)(e / ((int64_t)Rb1 * nk));
-        const double inv = 1.0 / ph[x];
-        double v;
-        if (aa < r0) v = c < r1 ? U[((int64_t)aa * nk + x) * r1 + c] * inv : 0.0;
-        else if (c < r1) v = -alpha * Ah[((int64_t)(aa - r0) * nk + x) * r1 + c] * inv;
-        else v = U[((int64_t)(aa - r0) * nk + x) * r1 + (c - r1)] * inv;
-        B[e] = v;
-      }
-    }
-    __syncthreads();
-  }
-  // ---- A14 (i): right-to-left orthogonalisation
   __shared__ int curR[kMaxD + 1];
   if (threadIdx.x == 0) {
     curR[0] = 1;
@@ -519,59 +563,60 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
     curR[d] = 1;
   }
   __syncthreads();
+  // ---- (i) right-to-left: R(B_k)^T = Q R, B_k <- Q^T, B_{k-1} <- B_{k-1} x_3 R^T
   for (int k = d - 1; k >= 1; --k) {
     const int R0 = curR[k], nk = a.n[k], R1 = curR[k + 1];
     const int rows = nk * R1, cols = R0;
     double* B = a.B + a.b_off[k];
-    // stage M^T (rows x cols) compact: Mt[i, a] = B[a*rows + i]
-    const int64_t sz = (int64_t)rows * cols;
-    double* A = sz <= sm.mat_cap ? sm.mat : gw;
-    for (int64_t e = threadIdx.x; e < sz; e += blockDim.x) {
-      const int i = (int)(e / cols), aa = (int)(e % cols);
-      A[e] = B[(int64_t)aa * rows + i];
+    int ld = odd_ld(cols);
+    double* A = w.mat;
+    if ((int64_t)rows * ld > w.mat_cap) {
+      A = gw;
+      ld = cols;
+    }
+    for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+      const int aa = e / rows, i = e - aa * rows;      // B[aa][i], coalesced read
+      A[(int64_t)i * ld + aa] = B[e];
     }
     __syncthreads();
-    double* R = sm.small1;
-    const int kmin = blk_qr_explicit(sm, A, rows, cols, R, A, A);
-    double* tmp = (A == gw) ? gw + sz : gw;
-    // new B_k = Q^T (kmin x rows)
-    for (int64_t e = threadIdx.x; e < (int64_t)kmin * rows; e += blockDim.x) {
-      const int aa = (int)(e / rows), i = (int)(e % rows);
-      B[e] = A[(int64_t)i * kmin + aa];
+    const int kmin = qr_explicit(A, ld, rows, cols, w.S1, w);
+    for (int e = threadIdx.x; e < kmin * rows; e += blockDim.x) {
+      const int aa = e / rows, i = e - aa * rows;
+      B[e] = A[(int64_t)i * ld + aa];
     }
-    __syncthreads();
-    // B_{k-1} <- B_{k-1} x_3 R^T  (R: kmin x R0)
     double* Bp = a.B + a.b_off[k - 1];
-    const int64_t prow = (int64_t)curR[k - 1] * a.n[k - 1];
-    blk_mode3t(tmp, Bp, prow, R0, R, kmin);
+    const int prow = curR[k - 1] * a.n[k - 1];
+    double* tmp = (A == gw) ? gw + (int64_t)rows * ld : gw;
+    blk_mode3t(tmp, Bp, prow, R0, w.S1, kmin);
     __syncthreads();
-    blk_copy(Bp, tmp, prow * kmin);
-    __syncthreads();
+    blk_copy(Bp, tmp, (int64_t)prow * kmin);
     if (threadIdx.x == 0) curR[k] = kmin;
     __syncthreads();
   }
-  // ---- A14 (ii): left-to-right truncated SVD sweep
+  // ---- (ii) left-to-right truncated SVD sweep
   bool ok = true;
   for (int k = 0; k + 1 < d; ++k) {
     const int R0 = curR[k], nk = a.n[k], R1 = curR[k + 1];
     const int m = R0 * nk;
     const int rk = a.r[k + 1];
     double* B = a.B + a.b_off[k];
-    const int64_t sz = (int64_t)m * R1;
-    double* A = sz <= sm.mat_cap ? sm.mat : gw;
-    blk_copy(A, B, sz);
+    int ld = odd_ld(R1);
+    double* A = w.mat;
+    if ((int64_t)m * ld > w.mat_cap) {
+      A = gw;
+      ld = R1;
+    }
+    for (int e = threadIdx.x; e < m * R1; e += blockDim.x) {
+      const int i = e / R1, c = e - i * R1;
+      A[(int64_t)i * ld + c] = B[e];
+    }
     __syncthreads();
-    double* R = sm.small1;
-    const int kmin = blk_qr_explicit(sm, A, m, R1, R, A, A);
-    double* tmp = (A == gw) ? gw + sz : gw;
-    // X = R^T (R1 x kmin), column-major: X[c*R1 + i] = R[c, i]
-    double* X = sm.small2;
-    double* V = sm.small3;
-    for (int e = threadIdx.x; e < kmin * R1; e += blockDim.x) X[e] = R[e];
-    __syncthreads();
+    double* X = w.S2;
+    const int kmin = qr_explicit(A, ld, m, R1, X, w);   // X <- R (kmin x R1) row-major
+    // the same storage read column-major (R1 x kmin) is X = R^T
+    double* V = w.S3;
     ok = blk_jacobi(X, R1, kmin, V) && ok;
-    // sort columns by norm, descending (ties by index)
-    double* nrm = sm.red;
+    double* nrm = w.red;
     if (threadIdx.x < kmin) {
       double s = 0.0;
       for (int i = 0; i < R1; ++i) s = fma(X[threadIdx.x * R1 + i], X[threadIdx.x * R1 + i], s);
@@ -581,48 +626,38 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
     if (threadIdx.x < kmin) {
       const int c = threadIdx.x;
       int rank = 0;
-      for (int c2 = 0; c2 < kmin; ++c2)
-        rank += (nrm[c2] > nrm[c]) || (nrm[c2] == nrm[c] && c2 < c);
-      sm.perm[rank] = c;
+      for (int c2 = 0; c2 < kmin; ++c2) rank += (nrm[c2] > nrm[c]) || (nrm[c2] == nrm[c] && c2 < c);
+      w.perm[rank] = c;
     }
     __syncthreads();
-    // C'_k = Q V[:, perm[:rk]]  (m x rk), written to the output core k
     double* Cout = a.C + a.core_off[k];
-    for (int64_t e = threadIdx.x; e < (int64_t)m * rk; e += blockDim.x) {
-      const int64_t row = e / rk;
-      const int c = (int)(e - row * rk);
+    for (int e = threadIdx.x; e < m * rk; e += blockDim.x) {
+      const int row = e / rk, c = e - row * rk;
       double acc = 0.0;
       if (c < kmin) {
-        const int pc = sm.perm[c];
-        for (int q = 0; q < kmin; ++q) acc = fma(A[row * kmin + q], V[pc * kmin + q], acc);
+        const double* vcol = V + w.perm[c] * kmin;
+        const double* q = A + (int64_t)row * ld;
+        for (int t = 0; t < kmin; ++t) acc = fma(q[t], vcol[t], acc);
       }
-      tmp[e] = acc;
+      Cout[e] = acc;
     }
-    __syncthreads();
-    blk_copy(Cout, tmp, (int64_t)m * rk);
-    // SVt (rk x R1): row a' = X[:, perm[a']]^T
-    double* SV = sm.small1;
+    double* SV = w.S1;
     for (int e = threadIdx.x; e < rk * R1; e += blockDim.x) {
-      const int ap = e / R1, i = e % R1;
-      SV[e] = ap < kmin ? X[sm.perm[ap] * R1 + i] : 0.0;
+      const int ap = e / R1, i = e - ap * R1;
+      SV[e] = ap < kmin ? X[w.perm[ap] * R1 + i] : 0.0;
     }
     __syncthreads();
     double* Bn = a.B + a.b_off[k + 1];
-    const int64_t rest = (int64_t)a.n[k + 1] * curR[k + 2];
+    const int rest = a.n[k + 1] * curR[k + 2];
+    double* tmp = (A == gw) ? gw + (int64_t)m * ld : gw;
     blk_mode1(tmp, SV, rk, R1, Bn, rest);
     __syncthreads();
     blk_copy(Bn, tmp, (int64_t)rk * rest);
-    __syncthreads();
     if (threadIdx.x == 0) curR[k + 1] = rk;
     __syncthreads();
   }
-  {
-    const int k = d - 1;
-    const int64_t sz = (int64_t)curR[k] * a.n[k];
-    blk_copy(a.C + a.core_off[k], a.B + a.b_off[k], sz);
-  }
+  blk_copy(a.C + a.core_off[d - 1], a.B + a.b_off[d - 1], (int64_t)curR[d - 1] * a.n[d - 1]);
   __syncthreads();
-  // finite check of the new iterate
   __shared__ int s_bad;
   if (threadIdx.x == 0) s_bad = 0;
   __syncthreads();
@@ -643,6 +678,7 @@ void dense_init() {
   const int bytes = dense_smem_doubles() * (int)sizeof(double);
   cudaFuncSetAttribute(k_dense_orth, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_dense_round, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 void launch_dense_orth(cudaStream_t s, const DenseArgs& a, int64_t* launches) {
@@ -653,8 +689,9 @@ void launch_dense_orth(cudaStream_t s, const DenseArgs& a, int64_t* launches) {
 
 void launch_dense_round(cudaStream_t s, const DenseArgs& a, int64_t* launches) {
   const size_t bytes = (size_t)a.smem_doubles * sizeof(double);
+  k_project<<<a.d, kDenseThreads, bytes, s>>>(a);
   k_dense_round<<<1, kDenseThreads, bytes, s>>>(a);
-  ++*launches;
+  *launches += 2;
 }
 
 }  // namespace prgd
