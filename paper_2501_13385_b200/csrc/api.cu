@@ -269,6 +269,7 @@ int ensure_base(tt_ctx* ctx) {
   CK(cudaMemsetAsync(ctx->sc, 0, sizeof(Scalars), ctx->stream));
   CK(cudaMemsetAsync(ctx->h, 0, ctx->phi_off[d] * sizeof(double), ctx->stream));
   dense_init();
+  tables_init();
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->base_ready = true;
   return TT_OK;

@@ -395,10 +395,11 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_orth(DenseArgs a) {
     }
     double* Un = a.U + a.core_off[k + 1];
     const int rest = a.n[k + 1] * a.r[k + 2];
-    double* tmp = (A == gw) ? gw + (int64_t)m * ld : gw;
-    blk_mode1(tmp, w.S1, r1, r1, Un, rest);
     __syncthreads();
-    blk_copy(Un, tmp, (int64_t)r1 * rest);
+    double* st = ((int64_t)r1 * rest <= w.mat_cap) ? w.mat : gw + (int64_t)m * ld;
+    blk_copy(st, Un, (int64_t)r1 * rest);        // stage U_{k+1} (coalesced)
+    __syncthreads();
+    blk_mode1(Un, w.S1, r1, r1, st, rest);       // U_{k+1} <- R U_{k+1}
     __syncthreads();
   }
   // A6: P_{d-1} = [1]; P_k = sum_j U_{k+1}(:,j,:) P_{k+1} U_{k+1}(:,j,:)^T; Cholesky.
@@ -410,10 +411,16 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_orth(DenseArgs a) {
   bool ok = true;
   for (int k = d - 2; k >= 0; --k) {
     const int R1 = a.r[k + 1], nk = a.n[k + 1], R2 = a.r[k + 2];
-    const double* Un = a.U + a.core_off[k + 1];
-    const double* Pn = a.P + a.p_off[k + 1];
     const int t1 = R1 * nk * R2;
-    double* T1 = gw;
+    const bool fits = 2 * (int64_t)t1 + R2 * R2 <= w.mat_cap;
+    double* Un = fits ? w.mat : a.U + a.core_off[k + 1];
+    double* T1 = fits ? w.mat + t1 : gw;
+    double* Pn = fits ? w.mat + 2 * t1 : a.P + a.p_off[k + 1];
+    if (fits) {
+      blk_copy(Un, a.U + a.core_off[k + 1], t1);
+      blk_copy(Pn, a.P + a.p_off[k + 1], R2 * R2);
+      __syncthreads();
+    }
     for (int e = threadIdx.x; e < t1; e += blockDim.x) {
       const int aj = e / R2, ee = e - aj * R2;
       double acc = 0.0;
@@ -478,8 +485,15 @@ __global__ void __launch_bounds__(kDenseThreads) k_project(DenseArgs a) {
       }
     __syncthreads();
     // Z = L(Y_k) P_k^{-1}: per row, forward then back substitution with L L^T
+    if (stage) {
+      for (int e = threadIdx.x; e < m * r1; e += blockDim.x) {
+        const int i = e / r1, c = e - i * r1;
+        Z[(int64_t)i * ld + c] = Y[e];          // stage Y (coalesced); solve in place
+      }
+      __syncthreads();
+    }
     for (int row = threadIdx.x; row < m; row += blockDim.x) {
-      const double* y = Y + (int64_t)row * r1;
+      const double* y = stage ? Z + (int64_t)row * zld : Y + (int64_t)row * r1;
       double* z = Z + (int64_t)row * zld;
       for (int i = 0; i < r1; ++i) {
         double s = y[i];
@@ -586,10 +600,11 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
     }
     double* Bp = a.B + a.b_off[k - 1];
     const int prow = curR[k - 1] * a.n[k - 1];
-    double* tmp = (A == gw) ? gw + (int64_t)rows * ld : gw;
-    blk_mode3t(tmp, Bp, prow, R0, w.S1, kmin);
     __syncthreads();
-    blk_copy(Bp, tmp, (int64_t)prow * kmin);
+    double* st = ((int64_t)prow * R0 <= w.mat_cap) ? w.mat : gw + (int64_t)rows * ld;
+    blk_copy(st, Bp, (int64_t)prow * R0);           // stage B_{k-1} (coalesced)
+    __syncthreads();
+    blk_mode3t(Bp, st, prow, R0, w.S1, kmin);       // B_{k-1} <- B_{k-1} x_3 R^T
     if (threadIdx.x == 0) curR[k] = kmin;
     __syncthreads();
   }
@@ -649,10 +664,10 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
     __syncthreads();
     double* Bn = a.B + a.b_off[k + 1];
     const int rest = a.n[k + 1] * curR[k + 2];
-    double* tmp = (A == gw) ? gw + (int64_t)m * ld : gw;
-    blk_mode1(tmp, SV, rk, R1, Bn, rest);
+    double* st = ((int64_t)R1 * rest <= w.mat_cap) ? w.mat : gw + (int64_t)m * ld;
+    blk_copy(st, Bn, (int64_t)R1 * rest);           // stage B_{k+1} (coalesced)
     __syncthreads();
-    blk_copy(Bn, tmp, (int64_t)rk * rest);
+    blk_mode1(Bn, SV, rk, R1, st, rest);            // B_{k+1} <- (S V^T)_r x_1 B_{k+1}
     if (threadIdx.x == 0) curR[k + 1] = rk;
     __syncthreads();
   }

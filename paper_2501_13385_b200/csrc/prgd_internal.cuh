@@ -112,6 +112,7 @@ void launch_Y(cudaStream_t s, bool left, const double* A, int ldA, const double*
               int64_t nsum, int r0, int nk, int r1, double* Y, double* partial,
               int64_t partial_cap, const Scalars* sc, int64_t* launches);
 int64_t Y_partial_need(int64_t nsum, int r0, int nk, int r1);
+void tables_init();  // shared-memory attributes (call once, outside capture)
 
 // passes.cu
 enum SegMode { kSDDMM = 0, kGSQ = 1, kSPMM = 2 };

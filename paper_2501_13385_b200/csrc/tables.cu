@@ -44,48 +44,83 @@ __global__ void k_table_left(const double* __restrict__ in, int ld_in,
   out[row * ld_out + c] = acc;
 }
 
+// Right table level: block = R rows x ld_out lanes; the R core slices C_k(:, j, :) the
+// block needs are staged transposed ([c][i], i fastest) so lanes i read consecutive
+// shared-memory words; the R input rows B_{k+1}[q, :] are staged too.
 __global__ void k_table_right(const double* __restrict__ in, int ld_in,
                               const double* __restrict__ core, int r0, int nk, int r1,
                               double* __restrict__ out, int ld_out, int64_t rows,
                               const double* __restrict__ rowscale, const Scalars* sc) {
   if (sc && sc->noop) return;
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t row = e / ld_out;
-  int i = (int)(e - row * ld_out);
-  if (row >= rows) return;
+  extern __shared__ double sm[];
+  const int R = blockDim.x / ld_out;
+  const int64_t row0 = (int64_t)blockIdx.x * R;
+  double* slices = sm;                       // [R][r1][r0]
+  double* vin = sm + (int64_t)R * r1 * r0;   // [R][r1]
+  const int per = r1 * r0;
+  for (int t = threadIdx.x; t < R * per; t += blockDim.x) {
+    const int lr = t / per, rem = t - lr * per;
+    const int i = rem / r1, c = rem - i * r1;  // c fastest: coalesced global reads
+    const int64_t row = row0 + lr;
+    double v = 0.0;
+    if (row < rows) {
+      const int j = (int)(row % nk);
+      v = core[((int64_t)i * nk + j) * r1 + c];
+    }
+    slices[(lr * r1 + c) * r0 + i] = v;
+  }
+  for (int t = threadIdx.x; t < R * r1; t += blockDim.x) {
+    const int lr = t / r1, c = t - lr * r1;
+    const int64_t row = row0 + lr;
+    double v = 0.0;
+    if (row < rows) v = in == nullptr ? 1.0 : in[(row / nk) * ld_in + c];
+    vin[t] = v;
+  }
+  __syncthreads();
+  const int lr = threadIdx.x / ld_out, i = threadIdx.x - lr * ld_out;
+  const int64_t row = row0 + lr;
+  if (lr >= R || row >= rows) return;
   double acc = 0.0;
   if (i < r0) {
-    int64_t q = row / nk;
-    int j = (int)(row - q * nk);
-    const double* cp = core + ((int64_t)i * nk + j) * r1;
-    if (in == nullptr) {
-      acc = cp[0];
-    } else {
-      const double* b = in + q * ld_in;
-      for (int c = 0; c < r1; ++c) acc = fma(cp[c], b[c], acc);
-    }
+    const double* sl = slices + (int64_t)lr * r1 * r0 + i;
+    const double* vv = vin + lr * r1;
+    for (int c = 0; c < r1; ++c) acc = fma(sl[c * r0], vv[c], acc);
     if (rowscale) acc *= rowscale[row];
   }
   out[row * ld_out + i] = acc;
 }
 
+// E_k[p, i] = sum_{j,c} U_k[i, j, c] E_{k+1}[p n_k + j, c]: block = R rows p x ld_out
+// lanes i; the core is staged transposed ([j][c][i]) in chunks of slices.
 __global__ void k_E_down(const double* __restrict__ Ein, int ld_in, const double* __restrict__ core,
                          int r0, int nk, int r1, double* __restrict__ Eout, int ld_out,
-                         int64_t rows, const Scalars* sc) {
+                         int64_t rows, int jchunk, const Scalars* sc) {
   if (sc && sc->noop) return;
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t p = e / ld_out;
-  int i = (int)(e - p * ld_out);
-  if (p >= rows) return;
+  extern __shared__ double sm[];
+  const int R = blockDim.x / ld_out;
+  const int lr = threadIdx.x / ld_out, i = threadIdx.x - lr * ld_out;
+  const int64_t p = (int64_t)blockIdx.x * R + lr;
+  const bool active = lr < R && p < rows && i < r0;
   double acc = 0.0;
-  if (i < r0) {
-    for (int j = 0; j < nk; ++j) {
-      const double* ein = Ein + (p * nk + j) * ld_in;
-      const double* cp = core + ((int64_t)i * nk + j) * r1;
-      for (int c = 0; c < r1; ++c) acc = fma(cp[c], ein[c], acc);
+  const int per = r1 * r0;
+  for (int j0 = 0; j0 < nk; j0 += jchunk) {
+    const int jn = nk - j0 < jchunk ? nk - j0 : jchunk;
+    __syncthreads();
+    for (int t = threadIdx.x; t < jn * per; t += blockDim.x) {
+      const int jj = t / per, rem = t - jj * per;
+      const int ii = rem / r1, c = rem - ii * r1;
+      sm[(jj * r1 + c) * r0 + ii] = core[((int64_t)ii * nk + j0 + jj) * r1 + c];
+    }
+    __syncthreads();
+    if (active) {
+      for (int jj = 0; jj < jn; ++jj) {
+        const double* ein = Ein + (p * nk + j0 + jj) * ld_in;
+        const double* sl = sm + jj * per + i;
+        for (int c = 0; c < r1; ++c) acc = fma(sl[c * r0], ein[c], acc);
+      }
     }
   }
-  Eout[p * ld_out + i] = acc;
+  if (lr < R && p < rows) Eout[p * ld_out + i] = acc;
 }
 
 __global__ void k_F_up(const double* __restrict__ Fin, int ld_in, const double* __restrict__ core,
@@ -109,6 +144,7 @@ __global__ void k_F_up(const double* __restrict__ Fin, int ld_in, const double* 
 }
 
 constexpr int kYThreads = 128;
+constexpr int64_t kTableSmemDoubles = 12288;   // 96 KB of staged slices
 
 // One thread per (j, c) of Y_k and a chunk of the summation index; all r0 values of
 // i live in registers.  partial[chunk][i][j][c].
@@ -165,6 +201,15 @@ __global__ void k_Y_reduce(const double* __restrict__ partial, int64_t nchunks, 
   Y[o] = acc;
 }
 
+}  // namespace
+
+void tables_init() {
+  cudaFuncSetAttribute(k_table_right, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(k_E_down, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+}
+
+namespace {
+
 int64_t y_chunks(int64_t nsum, int nk, int r1) {
   int64_t njc = (int64_t)nk * r1;
   int64_t want = (160000 + njc - 1) / njc;     // enough threads to fill 148 SMs
@@ -189,18 +234,26 @@ void launch_table_left(cudaStream_t s, const double* in, int ld_in, const double
 void launch_table_right(cudaStream_t s, const double* in, int ld_in, const double* core, int r0,
                         int nk, int r1, double* out, int ld_out, int64_t rows_out,
                         const double* rowscale, const Scalars* sc, int64_t* launches) {
-  int64_t n = rows_out * ld_out;
-  k_table_right<<<blocks_for(n, 256), 256, 0, s>>>(in, ld_in, core, r0, nk, r1, out, ld_out,
-                                                   rows_out, rowscale, sc);
+  const int threads = 256;
+  const int R = threads / ld_out;
+  const size_t smem = ((size_t)R * r1 * r0 + (size_t)R * r1) * sizeof(double);
+  k_table_right<<<blocks_for(rows_out, R), threads, smem, s>>>(in, ld_in, core, r0, nk, r1, out,
+                                                              ld_out, rows_out, rowscale, sc);
   ++*launches;
 }
 
 void launch_E_down(cudaStream_t s, const double* Ein, int ld_in, const double* core, int r0,
                    int nk, int r1, double* Eout, int ld_out, int64_t rows_out,
                    const Scalars* sc, int64_t* launches) {
-  int64_t n = rows_out * ld_out;
-  k_E_down<<<blocks_for(n, 256), 256, 0, s>>>(Ein, ld_in, core, r0, nk, r1, Eout, ld_out,
-                                              rows_out, sc);
+  const int threads = 256;
+  const int R = threads / ld_out;
+  const int per = r0 * r1;
+  int jchunk = (int)(kTableSmemDoubles / per);
+  if (jchunk > nk) jchunk = nk;
+  if (jchunk < 1) jchunk = 1;
+  const size_t smem = (size_t)jchunk * per * sizeof(double);
+  k_E_down<<<blocks_for(rows_out, R), threads, smem, s>>>(Ein, ld_in, core, r0, nk, r1, Eout,
+                                                         ld_out, rows_out, jchunk, sc);
   ++*launches;
 }
 
