@@ -971,13 +971,14 @@ int tt_debug_get(tt_ctx* ctx, int what, int k, void* h_out, int64_t cap, int64_t
       break;
     case TT_DBG_EPS: {
       if ((rc = read_scalars(ctx))) return rc;
-      if (cap < 4) return fail(ctx, TT_ERR_ARG, "capacity too small");
+      if (cap < 5) return fail(ctx, TT_ERR_ARG, "capacity too small");
       double* o = static_cast<double*>(h_out);
       o[0] = ctx->sc_host->eps;
       o[1] = ctx->sc_host->sumsq;
       o[2] = ctx->sc_host->alpha;
       o[3] = ctx->sc_host->p;
-      *count = 4;
+      o[4] = (double)ctx->sc_host->pad;   // cumulative Jacobi sweeps (diagnostic)
+      *count = 5;
       return TT_OK;
     }
     case TT_DBG_RESID: {

@@ -262,7 +262,7 @@ __device__ bool blk_chol(double* P, int R) {
 
 // One-sided Jacobi on the columns of X (rows x kc, column-major X[c*rows + i]),
 // accumulating V (kc x kc, column-major); round-robin ordering, one warp per pair.
-__device__ bool blk_jacobi(double* X, int rows, int kc, double* V) {
+__device__ bool blk_jacobi(double* X, int rows, int kc, double* V, int* sweeps) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   __shared__ int s_rot;
   for (int e = tid; e < kc * kc; e += blockDim.x) V[e] = (e / kc == e % kc) ? 1.0 : 0.0;
@@ -271,7 +271,9 @@ __device__ bool blk_jacobi(double* X, int rows, int kc, double* V) {
   const int kp = kc + (kc & 1);
   const int npairs = kp / 2;
   const double tol = 2.3e-16 * sqrt((double)(rows > 1 ? rows : 1));
+  const double tol2 = tol * tol;
   for (int sweep = 0; sweep < 60; ++sweep) {
+    if (tid == 0 && sweeps) atomicAdd(sweeps, 1);
     if (tid == 0) s_rot = 0;
     __syncthreads();
     for (int round = 0; round < kp - 1; ++round) {
@@ -296,10 +298,13 @@ __device__ bool blk_jacobi(double* X, int rows, int kc, double* V) {
           be += shx(be, o);
           ga += shx(ga, o);
         }
-        if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+        if (ga != 0.0 && ga * ga > tol2 * (al * be)) {
+          // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga),
+          // written with one sqrt and one division; c = 1/sqrt(1 + t^2), s = c t.
+          const double dlt = be - al;
+          const double sg = (dlt > 0.0 || (dlt == 0.0 && !signbit(dlt))) ? 1.0 : -1.0;
+          const double t = (2.0 * ga * sg) / (fabs(dlt) + sqrt(fma(dlt, dlt, 4.0 * ga * ga)));
+          const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
           for (int i = lane; i < rows; i += 32) {
             const double u = xa[i], v = xb[i];
             xa[i] = c * u - s * v;
@@ -340,13 +345,14 @@ __device__ void blk_mode1(double* out, const double* M, int ra, int rb, const do
   }
 }
 
-// out[row, c'] = sum_b in[row, b] M[c', b]  (M: rc x rb row-major)
-__device__ void blk_mode3t(double* out, const double* in, int rows, int rb, const double* M, int rc) {
+// out[row, c'] = sum_b in[row, b] Mt[b, c']  (Mt: rb x rc row-major, i.e. M^T): lanes
+// vary c' over consecutive words of Mt (conflict-free), in[row, :] is a broadcast.
+__device__ void blk_mode3t(double* out, const double* in, int rows, int rb, const double* Mt, int rc) {
   const int tot = rows * rc;
   for (int e = threadIdx.x; e < tot; e += blockDim.x) {
     const int row = e / rc, c = e - row * rc;
     double acc = 0.0;
-    for (int b = 0; b < rb; ++b) acc = fma(in[(int64_t)row * rb + b], M[c * rb + b], acc);
+    for (int b = 0; b < rb; ++b) acc = fma(in[(int64_t)row * rb + b], Mt[b * rc + c], acc);
     out[e] = acc;
   }
 }
@@ -430,11 +436,22 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_orth(DenseArgs a) {
     __syncthreads();
     double* P = a.P + a.p_off[k];
     const int len = nk * R2;
-    for (int e = threadIdx.x; e < R1 * R1; e += blockDim.x) {
-      const int aa = e / R1, bb = e - aa * R1;
-      double acc = 0.0;
-      for (int q = 0; q < len; ++q) acc = fma(T1[aa * len + q], Un[bb * len + q], acc);
-      P[e] = acc;
+    {
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      for (int aa = warp; aa < R1; aa += kNW) {
+        double pv[32];
+#pragma unroll
+        for (int bb = 0; bb < 32; ++bb) pv[bb] = 0.0;
+        for (int q = lane; q < len; q += 32) {
+          const double t = T1[aa * len + q];
+#pragma unroll
+          for (int bb = 0; bb < 32; ++bb)
+            if (bb < R1) pv[bb] = fma(t, Un[bb * len + q], pv[bb]);
+        }
+        double o0, o1;
+        warp_treduce<32>(pv, lane, o0, o1);
+        if (lane < R1) P[aa * R1 + lane] = o0;
+      }
     }
     __syncthreads();
     double* Ls = w.S1;
@@ -604,7 +621,12 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
     double* st = ((int64_t)prow * R0 <= w.mat_cap) ? w.mat : gw + (int64_t)rows * ld;
     blk_copy(st, Bp, (int64_t)prow * R0);           // stage B_{k-1} (coalesced)
     __syncthreads();
-    blk_mode3t(Bp, st, prow, R0, w.S1, kmin);       // B_{k-1} <- B_{k-1} x_3 R^T
+    for (int e = threadIdx.x; e < kmin * R0; e += blockDim.x) {   // S2 <- R^T (R0 x kmin)
+      const int c = e / R0, b = e - c * R0;
+      w.S2[b * kmin + c] = w.S1[e];
+    }
+    __syncthreads();
+    blk_mode3t(Bp, st, prow, R0, w.S2, kmin);       // B_{k-1} <- B_{k-1} x_3 R^T
     if (threadIdx.x == 0) curR[k] = kmin;
     __syncthreads();
   }
@@ -630,7 +652,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
     const int kmin = qr_explicit(A, ld, m, R1, X, w);   // X <- R (kmin x R1) row-major
     // the same storage read column-major (R1 x kmin) is X = R^T
     double* V = w.S3;
-    ok = blk_jacobi(X, R1, kmin, V) && ok;
+    ok = blk_jacobi(X, R1, kmin, V, &sc->pad) && ok;
     double* nrm = w.red;
     if (threadIdx.x < kmin) {
       double s = 0.0;
@@ -645,17 +667,21 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
       w.perm[rank] = c;
     }
     __syncthreads();
+    double* Vp = w.S1;                               // Vp[t][c] = V[t, perm[c]]
+    for (int e = threadIdx.x; e < kmin * rk; e += blockDim.x) {
+      const int t = e / rk, c = e - t * rk;
+      Vp[e] = c < kmin ? V[w.perm[c] * kmin + t] : 0.0;
+    }
+    __syncthreads();
     double* Cout = a.C + a.core_off[k];
     for (int e = threadIdx.x; e < m * rk; e += blockDim.x) {
       const int row = e / rk, c = e - row * rk;
+      const double* q = A + (int64_t)row * ld;
       double acc = 0.0;
-      if (c < kmin) {
-        const double* vcol = V + w.perm[c] * kmin;
-        const double* q = A + (int64_t)row * ld;
-        for (int t = 0; t < kmin; ++t) acc = fma(q[t], vcol[t], acc);
-      }
+      for (int t = 0; t < kmin; ++t) acc = fma(q[t], Vp[t * rk + c], acc);
       Cout[e] = acc;
     }
+    __syncthreads();
     double* SV = w.S1;
     for (int e = threadIdx.x; e < rk * R1; e += blockDim.x) {
       const int ap = e / R1, i = e - ap * R1;

@@ -31,7 +31,7 @@ struct Scalars {
   int noop;          // 1: skip the rest of this update (eps = 0 or a fault)
   int err;           // nonzero: numeric fault (sticky until read by the host)
   int index_err;     // set by index validation kernels
-  int pad;
+  int pad;          // cumulative one-sided Jacobi sweeps (diagnostic)
 };
 
 enum ErrBits { kErrNaN = 1, kErrChol = 2, kErrSVD = 4 };

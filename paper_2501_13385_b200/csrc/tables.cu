@@ -18,129 +18,165 @@ namespace {
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
-__global__ void k_table_left(const double* __restrict__ in, int ld_in,
-                             const double* __restrict__ core, int r0, int nk, int r1,
-                             double* __restrict__ out, int ld_out, int64_t rows,
-                             const double* __restrict__ rowscale, const Scalars* sc) {
-  if (sc && sc->noop) return;
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t row = e / ld_out;
-  int c = (int)(e - row * ld_out);
-  if (row >= rows) return;
-  double acc = 0.0;
-  if (c < r1) {
-    int64_t p = row / nk;
-    int j = (int)(row - p * nk);
-    const double* cp = core + (int64_t)j * r1 + c;
-    if (in == nullptr) {
-      acc = cp[0];
-    } else {
-      const double* a = in + p * ld_in;
-      const int64_t cs = (int64_t)nk * r1;
-      for (int i = 0; i < r0; ++i) acc = fma(a[i], cp[i * cs], acc);
-    }
-    if (rowscale) acc *= rowscale[row];
-  }
-  out[row * ld_out + c] = acc;
-}
+constexpr int kTabThreads = 256;
+constexpr int kRowsPerBlock = 64;      // parent rows per (slice, block) of a table level
+constexpr int kRecRows = 128;          // output rows per block of the E/F recursions
 
-// Right table level: block = R rows x ld_out lanes; the R core slices C_k(:, j, :) the
-// block needs are staged transposed ([c][i], i fastest) so lanes i read consecutive
-// shared-memory words; the R input rows B_{k+1}[q, :] are staged too.
-__global__ void k_table_right(const double* __restrict__ in, int ld_in,
-                              const double* __restrict__ core, int r0, int nk, int r1,
-                              double* __restrict__ out, int ld_out, int64_t rows,
-                              const double* __restrict__ rowscale, const Scalars* sc) {
+// Left table level: block (j, parent-row range).  out[(p n_k + j), c] =
+// scale * sum_i in[p, i] C(i, j, c); slice C(:, j, :) staged in shared memory.
+__global__ void __launch_bounds__(kTabThreads) k_table_left(
+    const double* __restrict__ in, int ld_in, const double* __restrict__ core, int r0, int nk,
+    int r1, double* __restrict__ out, int ld_out, int64_t nparent,
+    const double* __restrict__ rowscale, const Scalars* sc) {
   if (sc && sc->noop) return;
-  extern __shared__ double sm[];
-  const int R = blockDim.x / ld_out;
-  const int64_t row0 = (int64_t)blockIdx.x * R;
-  double* slices = sm;                       // [R][r1][r0]
-  double* vin = sm + (int64_t)R * r1 * r0;   // [R][r1]
-  const int per = r1 * r0;
-  for (int t = threadIdx.x; t < R * per; t += blockDim.x) {
-    const int lr = t / per, rem = t - lr * per;
-    const int i = rem / r1, c = rem - i * r1;  // c fastest: coalesced global reads
-    const int64_t row = row0 + lr;
-    double v = 0.0;
-    if (row < rows) {
-      const int j = (int)(row % nk);
-      v = core[((int64_t)i * nk + j) * r1 + c];
-    }
-    slices[(lr * r1 + c) * r0 + i] = v;
-  }
-  for (int t = threadIdx.x; t < R * r1; t += blockDim.x) {
-    const int lr = t / r1, c = t - lr * r1;
-    const int64_t row = row0 + lr;
-    double v = 0.0;
-    if (row < rows) v = in == nullptr ? 1.0 : in[(row / nk) * ld_in + c];
-    vin[t] = v;
+  __shared__ double cs[kMaxRank * kMaxRank];
+  const int j = blockIdx.x;
+  for (int t = threadIdx.x; t < r0 * r1; t += blockDim.x) {
+    const int i = t / r1, c = t - i * r1;
+    cs[t] = core[((int64_t)i * nk + j) * r1 + c];
   }
   __syncthreads();
-  const int lr = threadIdx.x / ld_out, i = threadIdx.x - lr * ld_out;
-  const int64_t row = row0 + lr;
-  if (lr >= R || row >= rows) return;
-  double acc = 0.0;
-  if (i < r0) {
-    const double* sl = slices + (int64_t)lr * r1 * r0 + i;
-    const double* vv = vin + lr * r1;
-    for (int c = 0; c < r1; ++c) acc = fma(sl[c * r0], vv[c], acc);
-    if (rowscale) acc *= rowscale[row];
+  const int lanes = ld_out, per = blockDim.x / lanes;
+  const int pl = threadIdx.x / lanes, c = threadIdx.x - pl * lanes;
+  if (pl >= per) return;
+  const int64_t p0 = (int64_t)blockIdx.y * kRowsPerBlock;
+  for (int64_t p = p0 + pl; p < p0 + kRowsPerBlock && p < nparent; p += per) {
+    const int64_t row = p * nk + j;
+    double acc = 0.0;
+    if (c < r1) {
+      if (in == nullptr) {
+        acc = cs[c];
+      } else {
+        const double* a = in + p * ld_in;
+        for (int i = 0; i < r0; ++i) acc = fma(a[i], cs[i * r1 + c], acc);
+      }
+      if (rowscale) acc *= rowscale[row];
+    }
+    out[row * ld_out + c] = acc;
   }
-  out[row * ld_out + i] = acc;
 }
 
-// E_k[p, i] = sum_{j,c} U_k[i, j, c] E_{k+1}[p n_k + j, c]: block = R rows p x ld_out
-// lanes i; the core is staged transposed ([j][c][i]) in chunks of slices.
-__global__ void k_E_down(const double* __restrict__ Ein, int ld_in, const double* __restrict__ core,
-                         int r0, int nk, int r1, double* __restrict__ Eout, int ld_out,
-                         int64_t rows, int jchunk, const Scalars* sc) {
+// Right table level: block (j, parent-row range).  out[(j + n_k q), i] =
+// scale * sum_c C(i, j, c) in[q, c]; slice staged transposed ([c][i]).
+__global__ void __launch_bounds__(kTabThreads) k_table_right(
+    const double* __restrict__ in, int ld_in, const double* __restrict__ core, int r0, int nk,
+    int r1, double* __restrict__ out, int ld_out, int64_t nparent,
+    const double* __restrict__ rowscale, const Scalars* sc) {
+  if (sc && sc->noop) return;
+  __shared__ double ct[kMaxRank * kMaxRank];
+  const int j = blockIdx.x;
+  for (int t = threadIdx.x; t < r0 * r1; t += blockDim.x) {
+    const int i = t / r1, c = t - i * r1;
+    ct[c * r0 + i] = core[((int64_t)i * nk + j) * r1 + c];
+  }
+  __syncthreads();
+  const int lanes = ld_out, per = blockDim.x / lanes;
+  const int ql = threadIdx.x / lanes, i = threadIdx.x - ql * lanes;
+  if (ql >= per) return;
+  const int64_t q0 = (int64_t)blockIdx.y * kRowsPerBlock;
+  for (int64_t q = q0 + ql; q < q0 + kRowsPerBlock && q < nparent; q += per) {
+    const int64_t row = (int64_t)j + (int64_t)nk * q;
+    double acc = 0.0;
+    if (i < r0) {
+      if (in == nullptr) {
+        acc = ct[i];
+      } else {
+        const double* b = in + q * ld_in;
+        for (int c = 0; c < r1; ++c) acc = fma(ct[c * r0 + i], b[c], acc);
+      }
+      if (rowscale) acc *= rowscale[row];
+    }
+    out[row * ld_out + i] = acc;
+  }
+}
+
+// E_k[p, i] = sum_{j,c} U_k(i, j, c) E_{k+1}[p n_k + j, c]; the core is staged
+// transposed ([j][c][i]) once per block (in chunks of slices) for kRecRows rows.
+__global__ void __launch_bounds__(kTabThreads) k_E_down(
+    const double* __restrict__ Ein, int ld_in, const double* __restrict__ core, int r0, int nk,
+    int r1, double* __restrict__ Eout, int ld_out, int64_t rows, int jchunk, const Scalars* sc) {
   if (sc && sc->noop) return;
   extern __shared__ double sm[];
-  const int R = blockDim.x / ld_out;
-  const int lr = threadIdx.x / ld_out, i = threadIdx.x - lr * ld_out;
-  const int64_t p = (int64_t)blockIdx.x * R + lr;
-  const bool active = lr < R && p < rows && i < r0;
-  double acc = 0.0;
-  const int per = r1 * r0;
+  const int lanes = ld_out, per = blockDim.x / lanes;
+  const int pl = threadIdx.x / lanes, i = threadIdx.x - pl * lanes;
+  const int64_t p0 = (int64_t)blockIdx.x * kRecRows;
+  double acc[kRecRows / (kTabThreads / kMaxRank) + 1];
+  const int nloc = (kRecRows + per - 1) / per;
+  for (int t = 0; t < nloc; ++t) acc[t] = 0.0;
+  const int psz = r1 * r0;
   for (int j0 = 0; j0 < nk; j0 += jchunk) {
     const int jn = nk - j0 < jchunk ? nk - j0 : jchunk;
     __syncthreads();
-    for (int t = threadIdx.x; t < jn * per; t += blockDim.x) {
-      const int jj = t / per, rem = t - jj * per;
+    for (int t = threadIdx.x; t < jn * psz; t += blockDim.x) {
+      const int jj = t / psz, rem = t - jj * psz;
       const int ii = rem / r1, c = rem - ii * r1;
       sm[(jj * r1 + c) * r0 + ii] = core[((int64_t)ii * nk + j0 + jj) * r1 + c];
     }
     __syncthreads();
-    if (active) {
-      for (int jj = 0; jj < jn; ++jj) {
-        const double* ein = Ein + (p * nk + j0 + jj) * ld_in;
-        const double* sl = sm + jj * per + i;
-        for (int c = 0; c < r1; ++c) acc = fma(sl[c * r0], ein[c], acc);
+    if (pl < per && i < r0) {
+      for (int t = 0; t < nloc; ++t) {
+        const int64_t p = p0 + pl + (int64_t)t * per;
+        if (p >= rows || p >= p0 + kRecRows) break;
+        double a = acc[t];
+        for (int jj = 0; jj < jn; ++jj) {
+          const double* ein = Ein + (p * nk + j0 + jj) * ld_in;
+          const double* sl = sm + jj * psz + i;
+          for (int c = 0; c < r1; ++c) a = fma(sl[c * r0], ein[c], a);
+        }
+        acc[t] = a;
       }
     }
   }
-  if (lr < R && p < rows) Eout[p * ld_out + i] = acc;
+  if (pl < per)
+    for (int t = 0; t < nloc; ++t) {
+      const int64_t p = p0 + pl + (int64_t)t * per;
+      if (p >= rows || p >= p0 + kRecRows) break;
+      Eout[p * ld_out + i] = i < r0 ? acc[t] : 0.0;
+    }
 }
 
-__global__ void k_F_up(const double* __restrict__ Fin, int ld_in, const double* __restrict__ core,
-                       int r0, int nk, int r1, double* __restrict__ Fout, int ld_out, int64_t rows,
-                       const Scalars* sc) {
+// F_{k+1}[q, c] = sum_{j,i} F_k[j + n_k q, i] U_k(i, j, c); core staged as [j][i][c].
+__global__ void __launch_bounds__(kTabThreads) k_F_up(
+    const double* __restrict__ Fin, int ld_in, const double* __restrict__ core, int r0, int nk,
+    int r1, double* __restrict__ Fout, int ld_out, int64_t rows, int jchunk, const Scalars* sc) {
   if (sc && sc->noop) return;
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t q = e / ld_out;
-  int c = (int)(e - q * ld_out);
-  if (q >= rows) return;
-  double acc = 0.0;
-  if (c < r1) {
-    const int64_t cs = (int64_t)nk * r1;
-    for (int j = 0; j < nk; ++j) {
-      const double* f = Fin + ((int64_t)j + (int64_t)nk * q) * ld_in;
-      const double* cp = core + (int64_t)j * r1 + c;
-      for (int i = 0; i < r0; ++i) acc = fma(f[i], cp[i * cs], acc);
+  extern __shared__ double sm[];
+  const int lanes = ld_out, per = blockDim.x / lanes;
+  const int ql = threadIdx.x / lanes, c = threadIdx.x - ql * lanes;
+  const int64_t q0 = (int64_t)blockIdx.x * kRecRows;
+  double acc[kRecRows / (kTabThreads / kMaxRank) + 1];
+  const int nloc = (kRecRows + per - 1) / per;
+  for (int t = 0; t < nloc; ++t) acc[t] = 0.0;
+  const int psz = r0 * r1;
+  for (int j0 = 0; j0 < nk; j0 += jchunk) {
+    const int jn = nk - j0 < jchunk ? nk - j0 : jchunk;
+    __syncthreads();
+    for (int t = threadIdx.x; t < jn * psz; t += blockDim.x) {
+      const int jj = t / psz, rem = t - jj * psz;
+      const int ii = rem / r1, cc = rem - ii * r1;
+      sm[t] = core[((int64_t)ii * nk + j0 + jj) * r1 + cc];   // [jj][ii][cc]
+    }
+    __syncthreads();
+    if (ql < per && c < r1) {
+      for (int t = 0; t < nloc; ++t) {
+        const int64_t q = q0 + ql + (int64_t)t * per;
+        if (q >= rows || q >= q0 + kRecRows) break;
+        double a = acc[t];
+        for (int jj = 0; jj < jn; ++jj) {
+          const double* f = Fin + ((int64_t)(j0 + jj) + (int64_t)nk * q) * ld_in;
+          const double* sl = sm + jj * psz + c;
+          for (int ii = 0; ii < r0; ++ii) a = fma(f[ii], sl[ii * r1], a);
+        }
+        acc[t] = a;
+      }
     }
   }
-  Fout[q * ld_out + c] = acc;
+  if (ql < per)
+    for (int t = 0; t < nloc; ++t) {
+      const int64_t q = q0 + ql + (int64_t)t * per;
+      if (q >= rows || q >= q0 + kRecRows) break;
+      Fout[q * ld_out + c] = c < r1 ? acc[t] : 0.0;
+    }
 }
 
 constexpr int kYThreads = 128;
@@ -204,8 +240,8 @@ __global__ void k_Y_reduce(const double* __restrict__ partial, int64_t nchunks, 
 }  // namespace
 
 void tables_init() {
-  cudaFuncSetAttribute(k_table_right, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   cudaFuncSetAttribute(k_E_down, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(k_F_up, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
 }
 
 namespace {
@@ -225,44 +261,47 @@ int64_t y_chunks(int64_t nsum, int nk, int r1) {
 void launch_table_left(cudaStream_t s, const double* in, int ld_in, const double* core, int r0,
                        int nk, int r1, double* out, int ld_out, int64_t rows_out,
                        const double* rowscale, const Scalars* sc, int64_t* launches) {
-  int64_t n = rows_out * ld_out;
-  k_table_left<<<blocks_for(n, 256), 256, 0, s>>>(in, ld_in, core, r0, nk, r1, out, ld_out,
-                                                  rows_out, rowscale, sc);
+  const int64_t nparent = rows_out / nk;
+  dim3 grid(nk, blocks_for(nparent, kRowsPerBlock));
+  k_table_left<<<grid, kTabThreads, 0, s>>>(in, ld_in, core, r0, nk, r1, out, ld_out, nparent,
+                                             rowscale, sc);
   ++*launches;
 }
 
 void launch_table_right(cudaStream_t s, const double* in, int ld_in, const double* core, int r0,
                         int nk, int r1, double* out, int ld_out, int64_t rows_out,
                         const double* rowscale, const Scalars* sc, int64_t* launches) {
-  const int threads = 256;
-  const int R = threads / ld_out;
-  const size_t smem = ((size_t)R * r1 * r0 + (size_t)R * r1) * sizeof(double);
-  k_table_right<<<blocks_for(rows_out, R), threads, smem, s>>>(in, ld_in, core, r0, nk, r1, out,
-                                                              ld_out, rows_out, rowscale, sc);
+  const int64_t nparent = rows_out / nk;
+  dim3 grid(nk, blocks_for(nparent, kRowsPerBlock));
+  k_table_right<<<grid, kTabThreads, 0, s>>>(in, ld_in, core, r0, nk, r1, out, ld_out, nparent,
+                                              rowscale, sc);
   ++*launches;
+}
+
+static int rec_jchunk(int r0, int nk, int r1) {
+  int jc = (int)(kTableSmemDoubles / ((int64_t)r0 * r1));
+  if (jc > nk) jc = nk;
+  if (jc < 1) jc = 1;
+  return jc;
 }
 
 void launch_E_down(cudaStream_t s, const double* Ein, int ld_in, const double* core, int r0,
                    int nk, int r1, double* Eout, int ld_out, int64_t rows_out,
                    const Scalars* sc, int64_t* launches) {
-  const int threads = 256;
-  const int R = threads / ld_out;
-  const int per = r0 * r1;
-  int jchunk = (int)(kTableSmemDoubles / per);
-  if (jchunk > nk) jchunk = nk;
-  if (jchunk < 1) jchunk = 1;
-  const size_t smem = (size_t)jchunk * per * sizeof(double);
-  k_E_down<<<blocks_for(rows_out, R), threads, smem, s>>>(Ein, ld_in, core, r0, nk, r1, Eout,
-                                                         ld_out, rows_out, jchunk, sc);
+  const int jc = rec_jchunk(r0, nk, r1);
+  const size_t smem = (size_t)jc * r0 * r1 * sizeof(double);
+  k_E_down<<<blocks_for(rows_out, kRecRows), kTabThreads, smem, s>>>(Ein, ld_in, core, r0, nk, r1,
+                                                                     Eout, ld_out, rows_out, jc, sc);
   ++*launches;
 }
 
 void launch_F_up(cudaStream_t s, const double* Fin, int ld_in, const double* core, int r0, int nk,
                  int r1, double* Fout, int ld_out, int64_t rows_out, const Scalars* sc,
                  int64_t* launches) {
-  int64_t n = rows_out * ld_out;
-  k_F_up<<<blocks_for(n, 256), 256, 0, s>>>(Fin, ld_in, core, r0, nk, r1, Fout, ld_out, rows_out,
-                                            sc);
+  const int jc = rec_jchunk(r0, nk, r1);
+  const size_t smem = (size_t)jc * r0 * r1 * sizeof(double);
+  k_F_up<<<blocks_for(rows_out, kRecRows), kTabThreads, smem, s>>>(Fin, ld_in, core, r0, nk, r1,
+                                                                   Fout, ld_out, rows_out, jc, sc);
   ++*launches;
 }
 
