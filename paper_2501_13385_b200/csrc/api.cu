@@ -254,11 +254,12 @@ int ensure_base(tt_ctx* ctx) {
       !A(ctx, &ctx->psiL, ctx->plan.NL, L) || !A(ctx, &ctx->psiR, ctx->plan.NR, L))
     return fail(ctx, TT_ERR_OOM, "device allocation failed (H / psi)");
   int64_t ycap = 1;
-  for (int k = 0; k < KL; ++k)
-    ycap = std::max(ycap, Y_partial_need(ctx->NLk[k], (int)ctx->r[k], (int)ctx->n[k], (int)ctx->r[k + 1]));
-  for (int k = KL; k < d; ++k)
-    ycap = std::max(ycap, Y_partial_need(k + 1 < d ? ctx->NRk[k + 1] : 1, (int)ctx->r[k],
-                                         (int)ctx->n[k], (int)ctx->r[k + 1]));
+  for (int k = 0; k < d; ++k) {
+    const int64_t ng = k < KL ? ctx->NLk[k] : (k + 1 < d ? ctx->NRk[k + 1] : 1);
+    const int r0 = (int)ctx->r[k], nk = (int)ctx->n[k], r1 = (int)ctx->r[k + 1];
+    ycap = std::max(ycap, Y_partial_need(ng, r0, nk, r1));
+    ycap = std::max(ycap, back_partial_need(ng, r0, nk, r1));
+  }
   ctx->Ypart_cap = ycap;
   if (!A(ctx, &ctx->Ypart, ycap, L)) return fail(ctx, TT_ERR_OOM, "device allocation failed (Y)");
   if (cudaMallocHost(&ctx->sc_host, sizeof(Scalars)) != cudaSuccess)
@@ -416,24 +417,36 @@ void enqueue_update(tt_ctx* ctx, int64_t* lc) {
   grp(ctx, 9, true);
   for (int k = KL - 1; k >= 0; --k) {
     const double* Atab = k >= 1 ? ctx->LT[k] : nullptr;
-    launch_Y(s, true, Atab, ctx->ldr[k], ctx->EL[k + 1], ctx->ldr[k + 1], ctx->NLk[k],
-             (int)ctx->r[k], (int)ctx->n[k], (int)ctx->r[k + 1], ctx->Y + ctx->core_off[k],
-             ctx->Ypart, ctx->Ypart_cap, ctx->sc, lc);
+    const int r0 = (int)ctx->r[k], nk = (int)ctx->n[k], r1 = (int)ctx->r[k + 1];
+    if (back_fused_ok(r0, nk, r1)) {
+      launch_back_level(s, true, ctx->EL[k + 1], ctx->ldr[k + 1], Atab, ctx->ldr[k],
+                        ctx->U + ctx->core_off[k], r0, nk, r1, k >= 1 ? ctx->EL[k] : nullptr,
+                        ctx->ldr[k], ctx->NLk[k], ctx->Y + ctx->core_off[k], ctx->Ypart,
+                        ctx->Ypart_cap, ctx->sc, lc);
+      continue;
+    }
+    launch_Y(s, true, Atab, ctx->ldr[k], ctx->EL[k + 1], ctx->ldr[k + 1], ctx->NLk[k], r0, nk, r1,
+             ctx->Y + ctx->core_off[k], ctx->Ypart, ctx->Ypart_cap, ctx->sc, lc);
     if (k >= 1)
-      launch_E_down(s, ctx->EL[k + 1], ctx->ldr[k + 1], ctx->U + ctx->core_off[k], (int)ctx->r[k],
-                    (int)ctx->n[k], (int)ctx->r[k + 1], ctx->EL[k], ctx->ldr[k], ctx->NLk[k],
-                    ctx->sc, lc);
+      launch_E_down(s, ctx->EL[k + 1], ctx->ldr[k + 1], ctx->U + ctx->core_off[k], r0, nk, r1,
+                    ctx->EL[k], ctx->ldr[k], ctx->NLk[k], ctx->sc, lc);
   }
   for (int k = KL; k < d; ++k) {
     const double* Btab = k + 1 < d ? ctx->RT[k + 1] : nullptr;
     const int64_t nsum = k + 1 < d ? ctx->NRk[k + 1] : 1;
-    launch_Y(s, false, Btab, ctx->ldr[k + 1], ctx->FR[k], ctx->ldr[k], nsum, (int)ctx->r[k],
-             (int)ctx->n[k], (int)ctx->r[k + 1], ctx->Y + ctx->core_off[k], ctx->Ypart,
-             ctx->Ypart_cap, ctx->sc, lc);
+    const int r0 = (int)ctx->r[k], nk = (int)ctx->n[k], r1 = (int)ctx->r[k + 1];
+    if (back_fused_ok(r0, nk, r1)) {
+      launch_back_level(s, false, ctx->FR[k], ctx->ldr[k], Btab, ctx->ldr[k + 1],
+                        ctx->U + ctx->core_off[k], r0, nk, r1, k + 1 < d ? ctx->FR[k + 1] : nullptr,
+                        ctx->ldr[k + 1], nsum, ctx->Y + ctx->core_off[k], ctx->Ypart,
+                        ctx->Ypart_cap, ctx->sc, lc);
+      continue;
+    }
+    launch_Y(s, false, Btab, ctx->ldr[k + 1], ctx->FR[k], ctx->ldr[k], nsum, r0, nk, r1,
+             ctx->Y + ctx->core_off[k], ctx->Ypart, ctx->Ypart_cap, ctx->sc, lc);
     if (k + 1 < d)
-      launch_F_up(s, ctx->FR[k], ctx->ldr[k], ctx->U + ctx->core_off[k], (int)ctx->r[k],
-                  (int)ctx->n[k], (int)ctx->r[k + 1], ctx->FR[k + 1], ctx->ldr[k + 1],
-                  ctx->NRk[k + 1], ctx->sc, lc);
+      launch_F_up(s, ctx->FR[k], ctx->ldr[k], ctx->U + ctx->core_off[k], r0, nk, r1,
+                  ctx->FR[k + 1], ctx->ldr[k + 1], ctx->NRk[k + 1], ctx->sc, lc);
   }
   grp(ctx, 9, false);
   grp(ctx, 10, true);
@@ -971,14 +984,15 @@ int tt_debug_get(tt_ctx* ctx, int what, int k, void* h_out, int64_t cap, int64_t
       break;
     case TT_DBG_EPS: {
       if ((rc = read_scalars(ctx))) return rc;
-      if (cap < 5) return fail(ctx, TT_ERR_ARG, "capacity too small");
+      if (cap < 13) return fail(ctx, TT_ERR_ARG, "capacity too small");
       double* o = static_cast<double*>(h_out);
       o[0] = ctx->sc_host->eps;
       o[1] = ctx->sc_host->sumsq;
       o[2] = ctx->sc_host->alpha;
       o[3] = ctx->sc_host->p;
       o[4] = (double)ctx->sc_host->pad;   // cumulative Jacobi sweeps (diagnostic)
-      *count = 5;
+      for (int i = 0; i < 8; ++i) o[5 + i] = (double)ctx->sc_host->cyc[i];
+      *count = 13;
       return TT_OK;
     }
     case TT_DBG_RESID: {

@@ -359,6 +359,15 @@ __device__ void blk_mode3t(double* out, const double* in, int rows, int rb, cons
 
 __device__ __forceinline__ int odd_ld(int n) { return n | 1; }
 
+// Phase timer (thread 0): cyc[ph] += clock64() - t0.  Diagnostic only.
+struct PhaseClock {
+  long long t0;
+  __device__ void start() { t0 = clock64(); }
+  __device__ void stop(Scalars* sc, int ph) {
+    if (threadIdx.x == 0) sc->cyc[ph] += clock64() - t0;
+  }
+};
+
 __global__ void __launch_bounds__(kDenseThreads) k_dense_orth(DenseArgs a) {
   extern __shared__ double smraw[];
   Scalars* sc = a.sc;
@@ -379,6 +388,8 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_orth(DenseArgs a) {
   __syncthreads();
   // A5: U_k <- Q, U_{k+1} <- R U_{k+1}
   double* gw = a.work;
+  PhaseClock pc;
+  pc.start();
   for (int k = 0; k + 1 < d; ++k) {
     const int r0 = a.r[k], nk = a.n[k], r1 = a.r[k + 1];
     const int m = r0 * nk;
@@ -408,6 +419,8 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_orth(DenseArgs a) {
     blk_mode1(Un, w.S1, r1, r1, st, rest);       // U_{k+1} <- R U_{k+1}
     __syncthreads();
   }
+  pc.stop(sc, 5);
+  pc.start();
   // A6: P_{d-1} = [1]; P_k = sum_j U_{k+1}(:,j,:) P_{k+1} U_{k+1}(:,j,:)^T; Cholesky.
   if (threadIdx.x == 0) {
     a.P[a.p_off[d - 1]] = 1.0;
@@ -464,6 +477,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_orth(DenseArgs a) {
     blk_copy(a.L + a.p_off[k], Ls, (int64_t)R1 * R1);
     __syncthreads();
   }
+  pc.stop(sc, 6);
   if (!ok && threadIdx.x == 0) {
     atomicOr(&sc->err, (int)kErrChol);
     sc->noop = 1;
@@ -610,7 +624,11 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
       A[(int64_t)i * ld + aa] = B[e];
     }
     __syncthreads();
+    PhaseClock pc;
+    pc.start();
     const int kmin = qr_explicit(A, ld, rows, cols, w.S1, w);
+    pc.stop(sc, 0);
+    pc.start();
     for (int e = threadIdx.x; e < kmin * rows; e += blockDim.x) {
       const int aa = e / rows, i = e - aa * rows;
       B[e] = A[(int64_t)i * ld + aa];
@@ -629,6 +647,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
     blk_mode3t(Bp, st, prow, R0, w.S2, kmin);       // B_{k-1} <- B_{k-1} x_3 R^T
     if (threadIdx.x == 0) curR[k] = kmin;
     __syncthreads();
+    pc.stop(sc, 1);
   }
   // ---- (ii) left-to-right truncated SVD sweep
   bool ok = true;
@@ -649,10 +668,16 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
     }
     __syncthreads();
     double* X = w.S2;
+    PhaseClock pc;
+    pc.start();
     const int kmin = qr_explicit(A, ld, m, R1, X, w);   // X <- R (kmin x R1) row-major
+    pc.stop(sc, 2);
     // the same storage read column-major (R1 x kmin) is X = R^T
     double* V = w.S3;
+    pc.start();
     ok = blk_jacobi(X, R1, kmin, V, &sc->pad) && ok;
+    pc.stop(sc, 3);
+    pc.start();
     double* nrm = w.red;
     if (threadIdx.x < kmin) {
       double s = 0.0;
@@ -696,6 +721,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
     blk_mode1(Bn, SV, rk, R1, st, rest);            // B_{k+1} <- (S V^T)_r x_1 B_{k+1}
     if (threadIdx.x == 0) curR[k + 1] = rk;
     __syncthreads();
+    pc.stop(sc, 4);
   }
   blk_copy(a.C + a.core_off[d - 1], a.B + a.b_off[d - 1], (int64_t)curR[d - 1] * a.n[d - 1]);
   __syncthreads();

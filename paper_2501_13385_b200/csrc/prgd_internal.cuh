@@ -32,6 +32,7 @@ struct Scalars {
   int err;           // nonzero: numeric fault (sticky until read by the host)
   int index_err;     // set by index validation kernels
   int pad;          // cumulative one-sided Jacobi sweeps (diagnostic)
+  long long cyc[8]; // cumulative SM cycles per dense phase (diagnostic)
 };
 
 enum ErrBits { kErrNaN = 1, kErrChol = 2, kErrSVD = 4 };
@@ -112,7 +113,14 @@ void launch_Y(cudaStream_t s, bool left, const double* A, int ldA, const double*
               int64_t nsum, int r0, int nk, int r1, double* Y, double* partial,
               int64_t partial_cap, const Scalars* sc, int64_t* launches);
 int64_t Y_partial_need(int64_t nsum, int r0, int nk, int r1);
-void tables_init();  // shared-memory attributes (call once, outside capture)
+void tables_init();
+// Fused backward level (E_k or F_{k+1} and Y_k in one pass), when r0 nk r1 <= 4096.
+bool back_fused_ok(int r0, int nk, int r1);
+int64_t back_partial_need(int64_t ngroups, int r0, int nk, int r1);
+void launch_back_level(cudaStream_t s, bool left, const double* X, int ldX, const double* V,
+                       int ldV, const double* core, int r0, int nk, int r1, double* O, int ldO,
+                       int64_t ngroups, double* Y, double* partial, int64_t partial_cap,
+                       const Scalars* sc, int64_t* launches);  // shared-memory attributes (call once, outside capture)
 
 // passes.cu
 enum SegMode { kSDDMM = 0, kGSQ = 1, kSPMM = 2 };

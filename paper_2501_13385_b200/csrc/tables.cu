@@ -227,6 +227,89 @@ __global__ void __launch_bounds__(kYThreads) k_Y_partial(
     if (i < r0) out[(int64_t)i * njc + jc] = acc[i];
 }
 
+// Fused backward step of one mode k, for r_k n_k r_{k+1} <= 4096:
+//  left  (k < K_L): group p, X_p[j][c] = E_{k+1}[p n_k + j, c], v = A_k[p, :]
+//        E_k[p, i] = sum_{j,c} U_k(i,j,c) X_p[j][c];   Y_k(i,j,c) += v[i] X_p[j][c]
+//  right (k >= K_L): group q, X_q[j][i] = F_k[j + n_k q, i], v = B_{k+1}[q, :]
+//        F_{k+1}[q, c] = sum_{j,i} X_q[j][i] U_k(i,j,c); Y_k(i,j,c) += X_q[j][i] v[c]
+// G groups are staged per sub-batch; the core is staged once in the order the output
+// rows read it; each block writes one split-K partial of Y_k (reduced in chunk order).
+constexpr int kBackThreads = 256;
+constexpr int kBackNY = 16;
+__global__ void __launch_bounds__(kBackThreads) k_back_level(
+    int left, const double* __restrict__ X, int ldX, const double* __restrict__ V, int ldV,
+    const double* __restrict__ core, int r0, int nk, int r1, double* __restrict__ O, int ldO,
+    int64_t ngroups, int64_t chunk, int G, double* __restrict__ partial, const Scalars* sc) {
+  if (sc && sc->noop) return;
+  extern __shared__ double sm[];
+  const int w = left ? r1 : r0;
+  const int vlen = left ? r0 : r1;
+  const int olen = left ? r0 : r1;
+  const int blk = nk * w;
+  const int count = r0 * nk * r1;
+  const int njc = nk * r1;
+  double* Us = sm;
+  double* Xs = Us + count;
+  double* Vs = Xs + (int64_t)G * blk;
+  for (int t = threadIdx.x; t < count; t += blockDim.x) {
+    const int i = t / njc, rem = t - i * njc;
+    const int j = rem / r1, c = rem - j * r1;
+    const double u = core[t];
+    if (left) Us[(j * r1 + c) * r0 + i] = u;
+    else Us[(j * r0 + i) * r1 + c] = u;
+  }
+  double acc[kBackNY];
+#pragma unroll
+  for (int u = 0; u < kBackNY; ++u) acc[u] = 0.0;
+  const int64_t g0 = (int64_t)blockIdx.x * chunk;
+  const int64_t g1 = g0 + chunk < ngroups ? g0 + chunk : ngroups;
+  for (int64_t gb = g0; gb < g1; gb += G) {
+    const int gn = (int)(g1 - gb < G ? g1 - gb : G);
+    __syncthreads();
+    for (int t = threadIdx.x; t < gn * blk; t += blockDim.x) {
+      const int g = t / blk, rem = t - g * blk;
+      const int j = rem / w, x = rem - j * w;
+      Xs[t] = X[((gb + g) * nk + j) * ldX + x];
+    }
+    for (int t = threadIdx.x; t < gn * vlen; t += blockDim.x) {
+      const int g = t / vlen, x = t - g * vlen;
+      Vs[t] = V ? V[(gb + g) * ldV + x] : 1.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kBackNY; ++u) {
+      const int o = threadIdx.x + u * kBackThreads;
+      if (o < count) {
+        const int i = o / njc, jc = o - i * njc;
+        const int j = jc / r1, c = jc - j * r1;
+        double a = acc[u];
+        if (left) {
+          for (int g = 0; g < gn; ++g) a = fma(Vs[g * vlen + i], Xs[g * blk + jc], a);
+        } else {
+          for (int g = 0; g < gn; ++g) a = fma(Xs[g * blk + j * w + i], Vs[g * vlen + c], a);
+        }
+        acc[u] = a;
+      }
+    }
+    if (O) {
+      const int len = nk * w;
+      for (int pr = threadIdx.x; pr < gn * olen; pr += blockDim.x) {
+        const int g = pr / olen, oo = pr - g * olen;
+        const double* xg = Xs + g * blk;
+        double s = 0.0;
+        for (int q = 0; q < len; ++q) s = fma(Us[q * olen + oo], xg[q], s);
+        O[(gb + g) * ldO + oo] = s;
+      }
+    }
+  }
+  double* out = partial + (int64_t)blockIdx.x * count;
+#pragma unroll
+  for (int u = 0; u < kBackNY; ++u) {
+    const int o = threadIdx.x + u * kBackThreads;
+    if (o < count) out[o] = acc[u];
+  }
+}
+
 __global__ void k_Y_reduce(const double* __restrict__ partial, int64_t nchunks, int64_t count,
                            double* __restrict__ Y, const Scalars* sc) {
   if (sc && sc->noop) return;
@@ -242,6 +325,7 @@ __global__ void k_Y_reduce(const double* __restrict__ partial, int64_t nchunks, 
 void tables_init() {
   cudaFuncSetAttribute(k_E_down, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   cudaFuncSetAttribute(k_F_up, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(k_back_level, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
 }
 
 namespace {
@@ -322,6 +406,42 @@ void launch_Y(cudaStream_t s, bool left, const double* A, int ldA, const double*
   k_Y_partial<<<grid, kYThreads, 0, s>>>(left ? 1 : 0, A, ldA, E, ldE, nsum, chunk, r0, nk, r1,
                                          partial, sc);
   k_Y_reduce<<<blocks_for(count, 256), 256, 0, s>>>(partial, nch, count, Y, sc);
+  *launches += 2;
+}
+
+bool back_fused_ok(int r0, int nk, int r1) {
+  return (int64_t)r0 * nk * r1 <= (int64_t)kBackNY * kBackThreads;
+}
+
+int64_t back_partial_need(int64_t ngroups, int r0, int nk, int r1) {
+  const int64_t count = (int64_t)r0 * nk * r1;
+  int64_t nb = (ngroups + 15) / 16;
+  if (nb > 296) nb = 296;
+  if (nb < 1) nb = 1;
+  return nb * count;
+}
+
+void launch_back_level(cudaStream_t s, bool left, const double* X, int ldX, const double* V,
+                       int ldV, const double* core, int r0, int nk, int r1, double* O, int ldO,
+                       int64_t ngroups, double* Y, double* partial, int64_t partial_cap,
+                       const Scalars* sc, int64_t* launches) {
+  const int w = left ? r1 : r0;
+  const int blk = nk * w;
+  int G = (int)(8192 / blk);
+  if (G > 16) G = 16;
+  if (G < 1) G = 1;
+  const int64_t count = (int64_t)r0 * nk * r1;
+  int64_t nb = (ngroups + G - 1) / G;
+  if (nb > 296) nb = 296;
+  if (nb * count > partial_cap) nb = partial_cap / count;
+  if (nb < 1) nb = 1;
+  int64_t chunk = (ngroups + nb - 1) / nb;
+  chunk = ((chunk + G - 1) / G) * G;
+  nb = (ngroups + chunk - 1) / chunk;
+  const size_t smem = ((size_t)count + (size_t)G * blk + (size_t)G * kMaxRank) * sizeof(double);
+  k_back_level<<<(unsigned)nb, kBackThreads, smem, s>>>(left ? 1 : 0, X, ldX, V, ldV, core, r0, nk,
+                                                       r1, O, ldO, ngroups, chunk, G, partial, sc);
+  k_Y_reduce<<<blocks_for(count, 256), 256, 0, s>>>(partial, nb, count, Y, sc);
   *launches += 2;
 }
 
