@@ -71,7 +71,10 @@ struct Work {
   double* S1;    // S x S
   double* S2;
   double* S3;
+  double* S4;    // S x S (QR scratch: Gram / Cholesky factor)
+  double* S5;    // S x S (QR scratch: accumulated R)
   int* perm;     // [S]
+  int* ptab;     // Jacobi pair table, [S][S/2] x 2 ints
   double* mat;   // staging area
   int64_t mat_cap;
 };
@@ -86,7 +89,10 @@ __device__ Work carve(double* sm, int smem_doubles, int S) {
   w.S1 = p; p += S * S;
   w.S2 = p; p += S * S;
   w.S3 = p; p += S * S;
+  w.S4 = p; p += S * S;
+  w.S5 = p; p += S * S;
   w.perm = reinterpret_cast<int*>(p); p += (S + 1) / 2 + 1;
+  w.ptab = reinterpret_cast<int*>(p); p += (S * S) / 2 + 1;
   w.mat = p;
   w.mat_cap = smem_doubles - (int64_t)(p - sm);
   return w;
@@ -208,9 +214,146 @@ __device__ void orgqr_rows(double* A, int ld, int m, int k, const Work& w) {
   __syncthreads();
 }
 
+// ---------------------------------------------------------------- CholeskyQR2
+// G = A^T A (n x n, full) for the m x n matrix A (stride ld); one thread per (i <= j).
+__device__ void blk_gram(const double* A, int ld, int m, int n, double* G) {
+  const int npairs = n * (n + 1) / 2;
+  for (int pr = threadIdx.x; pr < npairs; pr += blockDim.x) {
+    int i = 0, rem = pr;
+    while (rem >= n - i) {
+      rem -= n - i;
+      ++i;
+    }
+    const int j = i + rem;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int r = 0;
+    for (; r + 3 < m; r += 4) {
+      const double* a0 = A + (int64_t)r * ld;
+      s0 = fma(a0[i], a0[j], s0);
+      s1 = fma(a0[ld + i], a0[ld + j], s1);
+      s2 = fma(a0[2 * ld + i], a0[2 * ld + j], s2);
+      s3 = fma(a0[3 * ld + i], a0[3 * ld + j], s3);
+    }
+    for (; r < m; ++r) s0 = fma(A[(int64_t)r * ld + i], A[(int64_t)r * ld + j], s0);
+    const double sv = (s0 + s1) + (s2 + s3);
+    G[i * n + j] = sv;
+    G[j * n + i] = sv;
+  }
+  __syncthreads();
+}
+
+// In-place Cholesky G = L L^T by warp 0 (lower factor, upper zeroed).  A pivot below
+// 1e-14 of its original diagonal counts as breakdown (the block is too ill-conditioned
+// for CholeskyQR2 and goes to Householder).  Block-uniform result.
+__device__ bool blk_chol_warp(double* G, int n) {
+  __shared__ int s_ok;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    bool ok = true;
+    for (int j = 0; j < n; ++j) {
+      const double djj = G[j * n + j];
+      __syncwarp();
+      double d = 1.0;
+      if (djj > 0.0 && isfinite(djj)) d = sqrt(djj);
+      else ok = false;
+      for (int i = j + 1 + lane; i < n; i += 32) G[i * n + j] /= d;
+      if (lane == 0) G[j * n + j] = d;
+      __syncwarp();
+      for (int i = j + 1 + lane; i < n; i += 32) {
+        const double lij = G[i * n + j];
+        for (int k = j + 1; k <= i; ++k) G[i * n + k] = fma(-lij, G[k * n + j], G[i * n + k]);
+      }
+      __syncwarp();
+    }
+    for (int e = lane; e < n * n; e += 32)
+      if (e % n > e / n) G[e] = 0.0;
+    if (lane == 0) s_ok = ok ? 1 : 0;
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+// A <- A L^{-T} row by row (forward substitution with the lower factor L).
+__device__ void blk_solve_rows(double* A, int ld, int m, int n, const double* L) {
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    double* row = A + (int64_t)r * ld;
+    for (int j = 0; j < n; ++j) {
+      double s = row[j];
+      for (int i = 0; i < j; ++i) s = fma(-row[i], L[j * n + i], s);
+      row[j] = s / L[j * n + j];
+    }
+  }
+  __syncthreads();
+}
+
+// CholeskyQR2 with an orthogonality check: on success Q in A, R (n x n upper) in R.
+// Returns 0 on success, 1 if the first Cholesky failed (A untouched), 2 if it failed
+// later (A holds Q1 = A R1^{-1}, R holds R1): the caller finishes with Householder.
+__device__ int blk_cholqr2(double* A, int ld, int m, int n, double* R, const Work& w) {
+  double* G = w.S4;
+  for (int pass = 0; pass < 2; ++pass) {
+    blk_gram(A, ld, m, n, G);
+    double gmin = 0.0;
+    if (threadIdx.x == 0) {
+      gmin = G[0];
+      for (int j = 1; j < n; ++j) gmin = fmin(gmin, G[j * n + j]);
+      w.sc3[3] = gmin;
+    }
+    // remember the diagonal for the relative pivot test
+    for (int j = threadIdx.x; j < n; j += blockDim.x) w.vec[j] = G[j * n + j];
+    __syncthreads();
+    bool ok = blk_chol_warp(G, n);
+    if (ok) {
+      __shared__ int s_ok2;
+      if (threadIdx.x == 0) {
+        int o = 1;
+        for (int j = 0; j < n; ++j)
+          if (!(G[j * n + j] * G[j * n + j] > 1e-14 * w.vec[j])) o = 0;
+        s_ok2 = o;
+      }
+      __syncthreads();
+      ok = s_ok2 != 0;
+    }
+    if (!ok) return pass == 0 ? 1 : 2;
+    blk_solve_rows(A, ld, m, n, G);
+    // R <- L^T R (pass 1) or L^T (pass 0)
+    if (pass == 0) {
+      for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+        const int i = e / n, j = e - i * n;
+        R[e] = j >= i ? G[j * n + i] : 0.0;
+      }
+    } else {
+      double* T = w.S5;
+      for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+        const int i = e / n, j = e - i * n;
+        double acc = 0.0;
+        for (int q = i; q <= j; ++q) acc = fma(G[q * n + i], R[q * n + j], acc);
+        T[e] = j >= i ? acc : 0.0;
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < n * n; e += blockDim.x) R[e] = T[e];
+    }
+    __syncthreads();
+  }
+  // orthogonality check ||Q^T Q - I||_max <= 1e-13
+  blk_gram(A, ld, m, n, G);
+  __shared__ int s_orth;
+  if (threadIdx.x == 0) s_orth = 1;
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const double v = G[e] - ((e / n == e % n) ? 1.0 : 0.0);
+    if (!(fabs(v) <= 1e-13)) s_orth = 0;
+  }
+  __syncthreads();
+  return s_orth ? 0 : 2;
+}
+
 // QR of the m x n matrix staged at A (stride ld): R (kmin x n, row-major, zeros below
 // the diagonal) into Rout, Q in place over the first kmin columns.  Returns kmin.
-__device__ int qr_explicit(double* A, int ld, int m, int n, double* Rout, const Work& w) {
+// Tall blocks (m >= n) try CholeskyQR2 first (O(1) barriers); ill-conditioned or wide
+// blocks use Householder (LAPACK conventions), continuing from CholeskyQR2's partial
+// result when it failed late (A = Q1, R = R1  =>  A_orig = Q (R_h R1)).
+__device__ void householder_explicit(double* A, int ld, int m, int n, double* Rout, const Work& w) {
   const int kmin = m < n ? m : n;
   if (n <= 8) qr_rows<8>(A, ld, m, n, w);
   else if (n <= 16) qr_rows<16>(A, ld, m, n, w);
@@ -225,6 +368,31 @@ __device__ int qr_explicit(double* A, int ld, int m, int n, double* Rout, const 
   else if (kmin <= 16) orgqr_rows<16>(A, ld, m, kmin, w);
   else if (kmin <= 32) orgqr_rows<32>(A, ld, m, kmin, w);
   else orgqr_rows<64>(A, ld, m, kmin, w);
+}
+
+__device__ int qr_explicit(double* A, int ld, int m, int n, double* Rout, const Work& w) {
+  const int kmin = m < n ? m : n;
+  if (m >= n) {
+    const int st = blk_cholqr2(A, ld, m, n, Rout, w);
+    if (st == 0) return kmin;
+    if (st == 2) {
+      // finish: Q1 = Q_h R_h  =>  A_orig = Q_h (R_h R1)
+      double* R1 = w.S5;
+      for (int e = threadIdx.x; e < n * n; e += blockDim.x) R1[e] = Rout[e];
+      __syncthreads();
+      double* Rh = w.S4;
+      householder_explicit(A, ld, m, n, Rh, w);
+      for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+        const int i = e / n, j = e - i * n;
+        double acc = 0.0;
+        for (int q = i; q <= j; ++q) acc = fma(Rh[i * n + q], R1[q * n + j], acc);
+        Rout[e] = j >= i ? acc : 0.0;
+      }
+      __syncthreads();
+      return kmin;
+    }
+  }
+  householder_explicit(A, ld, m, n, Rout, w);
   return kmin;
 }
 
@@ -261,63 +429,79 @@ __device__ bool blk_chol(double* P, int R) {
 }
 
 // One-sided Jacobi on the columns of X (rows x kc, column-major X[c*rows + i]),
-// accumulating V (kc x kc, column-major); round-robin ordering, one warp per pair.
-__device__ bool blk_jacobi(double* X, int rows, int kc, double* V, int* sweeps) {
+// accumulating V (kc x kc, column-major).  Round-robin ordering from a precomputed
+// pair table, one warp per pair; column norms are kept in shared memory and updated
+// by the exact rotation identities (a' = a - t g, b' = b + t g), recomputed per sweep.
+__device__ bool blk_jacobi(double* X, int rows, int kc, double* V, int* sweeps, double* nrm,
+                           int* ptab) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   __shared__ int s_rot;
   for (int e = tid; e < kc * kc; e += blockDim.x) V[e] = (e / kc == e % kc) ? 1.0 : 0.0;
-  __syncthreads();
-  if (kc < 2) return true;
+  if (kc < 2) {
+    __syncthreads();
+    return true;
+  }
   const int kp = kc + (kc & 1);
   const int npairs = kp / 2;
+  for (int e = tid; e < (kp - 1) * npairs; e += blockDim.x) {
+    const int round = e / npairs, pr = e - round * npairs;
+    int a = pr == 0 ? 0 : ((pr - 1 + round) % (kp - 1)) + 1;
+    const int q = kp - 1 - pr;
+    int b = q == 0 ? 0 : ((q - 1 + round) % (kp - 1)) + 1;
+    if (a > b) { const int t = a; a = b; b = t; }
+    ptab[2 * e] = a;
+    ptab[2 * e + 1] = b;
+  }
   const double tol = 2.3e-16 * sqrt((double)(rows > 1 ? rows : 1));
   const double tol2 = tol * tol;
   for (int sweep = 0; sweep < 60; ++sweep) {
-    if (tid == 0 && sweeps) atomicAdd(sweeps, 1);
-    if (tid == 0) s_rot = 0;
+    if (tid == 0) {
+      s_rot = 0;
+      if (sweeps) atomicAdd(sweeps, 1);
+    }
+    __syncthreads();
+    for (int c = warp; c < kc; c += nw) {
+      double s = 0.0;
+      for (int i = lane; i < rows; i += 32) s = fma(X[c * rows + i], X[c * rows + i], s);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += shx(s, o);
+      if (lane == 0) nrm[c] = s;
+    }
     __syncthreads();
     for (int round = 0; round < kp - 1; ++round) {
+      const int* pt = ptab + 2 * round * npairs;
       for (int pr = warp; pr < npairs; pr += nw) {
-        int a = pr == 0 ? 0 : ((pr - 1 + round) % (kp - 1)) + 1;
-        const int q = kp - 1 - pr;
-        int b = q == 0 ? 0 : ((q - 1 + round) % (kp - 1)) + 1;
-        if (a > b) { const int t = a; a = b; b = t; }
+        const int a = pt[2 * pr], b = pt[2 * pr + 1];
         if (b >= kc) continue;
         double* xa = X + (int64_t)a * rows;
         double* xb = X + (int64_t)b * rows;
-        double al = 0.0, be = 0.0, ga = 0.0;
-        for (int i = lane; i < rows; i += 32) {
-          const double u = xa[i], v = xb[i];
-          al = fma(u, u, al);
-          be = fma(v, v, be);
-          ga = fma(u, v, ga);
-        }
+        double ga = 0.0;
+        for (int i = lane; i < rows; i += 32) ga = fma(xa[i], xb[i], ga);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          al += shx(al, o);
-          be += shx(be, o);
-          ga += shx(ga, o);
-        }
+        for (int o = 16; o > 0; o >>= 1) ga += shx(ga, o);
+        const double al = nrm[a], be = nrm[b];
         if (ga != 0.0 && ga * ga > tol2 * (al * be)) {
-          // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga),
-          // written with one sqrt and one division; c = 1/sqrt(1 + t^2), s = c t.
           const double dlt = be - al;
           const double sg = (dlt > 0.0 || (dlt == 0.0 && !signbit(dlt))) ? 1.0 : -1.0;
           const double t = (2.0 * ga * sg) / (fabs(dlt) + sqrt(fma(dlt, dlt, 4.0 * ga * ga)));
-          const double c = rsqrt(fma(t, t, 1.0)), s = c * t;
+          const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
           for (int i = lane; i < rows; i += 32) {
             const double u = xa[i], v = xb[i];
-            xa[i] = c * u - s * v;
-            xb[i] = s * u + c * v;
+            xa[i] = c * u - sn * v;
+            xb[i] = sn * u + c * v;
           }
           double* va = V + (int64_t)a * kc;
           double* vb = V + (int64_t)b * kc;
           for (int i = lane; i < kc; i += 32) {
             const double u = va[i], v = vb[i];
-            va[i] = c * u - s * v;
-            vb[i] = s * u + c * v;
+            va[i] = c * u - sn * v;
+            vb[i] = sn * u + c * v;
           }
-          if (lane == 0) s_rot = 1;
+          if (lane == 0) {
+            nrm[a] = al - t * ga;
+            nrm[b] = be + t * ga;
+            s_rot = 1;
+          }
         }
       }
       __syncthreads();
@@ -675,7 +859,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
     // the same storage read column-major (R1 x kmin) is X = R^T
     double* V = w.S3;
     pc.start();
-    ok = blk_jacobi(X, R1, kmin, V, &sc->pad) && ok;
+    ok = blk_jacobi(X, R1, kmin, V, &sc->pad, w.red, w.ptab) && ok;
     pc.stop(sc, 3);
     pc.start();
     double* nrm = w.red;

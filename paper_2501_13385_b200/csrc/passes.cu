@@ -49,7 +49,9 @@ __device__ __forceinline__ double2 ld2(const double* p) {
 template <int LPS, int MODE>
 __global__ void __launch_bounds__(256) k_seg(SegDev a, const Scalars* sc) {
   if (sc && sc->noop) return;
-  constexpr int G = 32 / LPS;
+  constexpr int G = 32 / LPS;        // samples per warp step
+  constexpr int STEPS = 32 / G;      // steps per 32-sample chunk (= LPS)
+  constexpr int UNR = STEPS < 4 ? STEPS : 4;
   const int lane = threadIdx.x & 31;
   const int grp = lane / LPS, sub = lane - grp * LPS;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -64,41 +66,66 @@ __global__ void __launch_bounds__(256) k_seg(SegDev a, const Scalars* sc) {
     if (MODE == kSDDMM) rv = ld2(a.rowtab + (int64_t)row * ld + 2 * sub);
     double accs = 0.0;
     double2 accv = make_double2(0.0, 0.0);
-    for (int tb = 0; tb < cnt; tb += G) {
-      const int t = tb + grp;
-      const bool valid = t < cnt;
-      const int64_t s = beg + t;
-      if (MODE == kSDDMM) {
-        double2 b = make_double2(0.0, 0.0);
-        double yv = 0.0;
-        if (valid) {
-          b = ld2(a.coltab + (int64_t)a.col[s] * ld + 2 * sub);
-          yv = a.y[s];
-        }
-        double part = fma(rv.x, b.x, rv.y * b.y);
+    for (int c0 = 0; c0 < cnt; c0 += 32) {
+      const int nc = cnt - c0 < 32 ? cnt - c0 : 32;
+      const int64_t s = beg + c0 + lane;
+      const bool have = lane < nc;
+      // lane-parallel loads of this chunk's per-sample data (coalesced / independent)
+      int colv = 0;
+      double xv = 0.0;    // y (SDDMM) or g (GSQ, SPMM)
+      if (have) {
+        if (MODE != kGSQ) colv = a.col[s];
+        if (MODE == kSDDMM) xv = a.y[s];
+        else xv = a.perm ? a.g[a.perm[s]] : a.g[s];
+      }
+      if (MODE == kGSQ) {
+        accs = fma(xv, xv, accs);
+        continue;
+      }
 #pragma unroll
-        for (int o = LPS / 2; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
-        const double gv = part - yv;
-        if (valid && sub == 0) {
-          a.g[s] = gv;
-          accs = fma(gv, gv, accs);
+      for (int st0 = 0; st0 < STEPS; st0 += UNR) {
+        double2 b[UNR];
+        double xs[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const int t = (st0 + u) * G + grp;
+          const int cidx = __shfl_sync(kFull, colv, t & 31);
+          xs[u] = __shfl_sync(kFull, xv, t & 31);
+          b[u] = make_double2(0.0, 0.0);
+          if (t < nc) b[u] = ld2(a.coltab + (int64_t)cidx * ld + 2 * sub);
         }
-      } else if (MODE == kGSQ) {
-        if (valid) {
-          const double gv = a.g[a.perm[s]];
-          accs = fma(gv, gv, accs);
-        }
-      } else {
-        if (valid) {
-          const double gv = a.perm ? a.g[a.perm[s]] : a.g[s];
-          const double2 b = ld2(a.coltab + (int64_t)a.col[s] * ld + 2 * sub);
-          accv.x = fma(gv, b.x, accv.x);
-          accv.y = fma(gv, b.y, accv.y);
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const int t = (st0 + u) * G + grp;
+          if (MODE == kSDDMM) {
+            double part = fma(rv.x, b[u].x, rv.y * b[u].y);
+#pragma unroll
+            for (int o = LPS / 2; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
+            if (t < nc) {
+              const double gv = part - xs[u];
+              if (sub == 0) {
+                a.g[beg + c0 + t] = gv;
+                accs = fma(gv, gv, accs);
+              }
+            }
+          } else {
+            if (t < nc) {
+              accv.x = fma(xs[u], b[u].x, accv.x);
+              accv.y = fma(xs[u], b[u].y, accv.y);
+            }
+          }
         }
       }
     }
     const int32_t pslot = a.vrow_part[v];
-    if (MODE != kSPMM) {
+    if (MODE == kGSQ) {
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) accs += __shfl_xor_sync(kFull, accs, o);
+      if (lane == 0) {
+        if (pslot < 0) a.out[row] = accs;
+        else a.part[pslot] = accs;
+      }
+    } else if (MODE == kSDDMM) {
 #pragma unroll
       for (int o = LPS; o < 32; o <<= 1) accs += __shfl_xor_sync(kFull, accs, o);
       if (lane == 0) {
