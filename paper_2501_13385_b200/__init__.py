@@ -138,11 +138,20 @@ class TTContext:
         self.stream = torch.cuda.Stream(device=dev)
         stream = self.stream
 
+        alloc_fn = torch.cuda.caching_allocator_alloc
+        delete_fn = torch.cuda.caching_allocator_delete
+
         def _alloc(nbytes, _user):
-            return torch.cuda.caching_allocator_alloc(int(nbytes), device=dev, stream=stream)
+            try:
+                return alloc_fn(int(nbytes), device=dev, stream=stream)
+            except Exception:
+                return None   # the library reports TT_ERR_OOM
 
         def _free(ptr, _user):
-            torch.cuda.caching_allocator_delete(ptr)
+            try:
+                delete_fn(ptr)
+            except Exception:
+                pass          # interpreter teardown: the process is exiting anyway
 
         fa, ff = ALLOC_FN(_alloc), FREE_FN(_free)
         self._keep += [fa, ff]

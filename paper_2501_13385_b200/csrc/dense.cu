@@ -75,6 +75,7 @@ struct Work {
   double* S5;    // S x S (QR scratch: accumulated R)
   int* perm;     // [S]
   int* ptab;     // Jacobi pair table, [S][S/2] x 2 ints
+  long long* diag;  // diagnostic counters (Scalars::cyc) or null
   double* mat;   // staging area
   int64_t mat_cap;
 };
@@ -84,17 +85,18 @@ __device__ Work carve(double* sm, int smem_doubles, int S) {
   double* p = sm;
   w.red = p; p += kNW * kMaxCols;
   w.vec = p; p += kMaxCols;
-  w.sc3 = p; p += 4;
+  w.sc3 = p; p += 4 + kMaxCols;   // [0..3] scalars, [4..] per-column scratch (dinv)
   w.tau = p; p += kMaxCols;
   w.S1 = p; p += S * S;
   w.S2 = p; p += S * S;
   w.S3 = p; p += S * S;
-  w.S4 = p; p += S * S;
+  w.S4 = p; p += S * (S + 1);
   w.S5 = p; p += S * S;
   w.perm = reinterpret_cast<int*>(p); p += (S + 1) / 2 + 1;
   w.ptab = reinterpret_cast<int*>(p); p += (S * S) / 2 + 1;
   w.mat = p;
   w.mat_cap = smem_doubles - (int64_t)(p - sm);
+  w.diag = nullptr;
   return w;
 }
 
@@ -215,29 +217,28 @@ __device__ void orgqr_rows(double* A, int ld, int m, int k, const Work& w) {
 }
 
 // ---------------------------------------------------------------- CholeskyQR2
-// G = A^T A (n x n, full) for the m x n matrix A (stride ld); one thread per (i <= j).
-__device__ void blk_gram(const double* A, int ld, int m, int n, double* G) {
-  const int npairs = n * (n + 1) / 2;
-  for (int pr = threadIdx.x; pr < npairs; pr += blockDim.x) {
-    int i = 0, rem = pr;
-    while (rem >= n - i) {
-      rem -= n - i;
-      ++i;
+// G = A^T A (n x n, full, row stride gl) for the m x n matrix A (stride ld).  Warp w
+// owns the G rows {w, n-1-w, w+nw, n-1-w-nw, ...} (balanced triangle); lane l owns the
+// columns j = i + l, i + l + 32 (j >= i); 4-way unrolled over the rows of A.
+__device__ void blk_gram(const double* A, int ld, int m, int n, double* G, int gl) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int t = warp; t < n; t += nw) {
+    const int i = (t & 1) ? n - 1 - (t >> 1) : (t >> 1);
+    for (int j = i + lane; j < n; j += 32) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int r = 0;
+      for (; r + 3 < m; r += 4) {
+        const double* a0 = A + (int64_t)r * ld;
+        s0 = fma(a0[i], a0[j], s0);
+        s1 = fma(a0[ld + i], a0[ld + j], s1);
+        s2 = fma(a0[2 * ld + i], a0[2 * ld + j], s2);
+        s3 = fma(a0[3 * ld + i], a0[3 * ld + j], s3);
+      }
+      for (; r < m; ++r) s0 = fma(A[(int64_t)r * ld + i], A[(int64_t)r * ld + j], s0);
+      const double sv = (s0 + s1) + (s2 + s3);
+      G[i * gl + j] = sv;
+      G[j * gl + i] = sv;
     }
-    const int j = i + rem;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int r = 0;
-    for (; r + 3 < m; r += 4) {
-      const double* a0 = A + (int64_t)r * ld;
-      s0 = fma(a0[i], a0[j], s0);
-      s1 = fma(a0[ld + i], a0[ld + j], s1);
-      s2 = fma(a0[2 * ld + i], a0[2 * ld + j], s2);
-      s3 = fma(a0[3 * ld + i], a0[3 * ld + j], s3);
-    }
-    for (; r < m; ++r) s0 = fma(A[(int64_t)r * ld + i], A[(int64_t)r * ld + j], s0);
-    const double sv = (s0 + s1) + (s2 + s3);
-    G[i * n + j] = sv;
-    G[j * n + i] = sv;
   }
   __syncthreads();
 }
@@ -245,42 +246,48 @@ __device__ void blk_gram(const double* A, int ld, int m, int n, double* G) {
 // In-place Cholesky G = L L^T by warp 0 (lower factor, upper zeroed).  A pivot below
 // 1e-14 of its original diagonal counts as breakdown (the block is too ill-conditioned
 // for CholeskyQR2 and goes to Householder).  Block-uniform result.
-__device__ bool blk_chol_warp(double* G, int n) {
+__device__ bool blk_chol_warp(double* G, int n, int gl) {
   __shared__ int s_ok;
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     bool ok = true;
     for (int j = 0; j < n; ++j) {
-      const double djj = G[j * n + j];
+      const double djj = G[j * gl + j];
       __syncwarp();
       double d = 1.0;
       if (djj > 0.0 && isfinite(djj)) d = sqrt(djj);
       else ok = false;
-      for (int i = j + 1 + lane; i < n; i += 32) G[i * n + j] /= d;
-      if (lane == 0) G[j * n + j] = d;
+      const double dinv = 1.0 / d;
+      for (int i = j + 1 + lane; i < n; i += 32) G[i * gl + j] *= dinv;
+      if (lane == 0) G[j * gl + j] = d;
       __syncwarp();
       for (int i = j + 1 + lane; i < n; i += 32) {
-        const double lij = G[i * n + j];
-        for (int k = j + 1; k <= i; ++k) G[i * n + k] = fma(-lij, G[k * n + j], G[i * n + k]);
+        const double lij = G[i * gl + j];
+        for (int k = j + 1; k <= i; ++k) G[i * gl + k] = fma(-lij, G[k * gl + j], G[i * gl + k]);
       }
       __syncwarp();
     }
-    for (int e = lane; e < n * n; e += 32)
-      if (e % n > e / n) G[e] = 0.0;
+    for (int e = lane; e < n * n; e += 32) {
+      const int i = e / n, c = e - i * n;
+      if (c > i) G[i * gl + c] = 0.0;
+    }
     if (lane == 0) s_ok = ok ? 1 : 0;
   }
   __syncthreads();
   return s_ok != 0;
 }
 
-// A <- A L^{-T} row by row (forward substitution with the lower factor L).
-__device__ void blk_solve_rows(double* A, int ld, int m, int n, const double* L) {
+// A <- A L^{-T} row by row (forward substitution with the lower factor L, stride gl).
+__device__ void blk_solve_rows(double* A, int ld, int m, int n, const double* L, int gl,
+                               double* dinv) {
+  for (int j = threadIdx.x; j < n; j += blockDim.x) dinv[j] = 1.0 / L[j * gl + j];
+  __syncthreads();
   for (int r = threadIdx.x; r < m; r += blockDim.x) {
     double* row = A + (int64_t)r * ld;
     for (int j = 0; j < n; ++j) {
       double s = row[j];
-      for (int i = 0; i < j; ++i) s = fma(-row[i], L[j * n + i], s);
-      row[j] = s / L[j * n + j];
+      for (int i = 0; i < j; ++i) s = fma(-row[i], L[j * gl + i], s);
+      row[j] = s * dinv[j];
     }
   }
   __syncthreads();
@@ -290,44 +297,39 @@ __device__ void blk_solve_rows(double* A, int ld, int m, int n, const double* L)
 // Returns 0 on success, 1 if the first Cholesky failed (A untouched), 2 if it failed
 // later (A holds Q1 = A R1^{-1}, R holds R1): the caller finishes with Householder.
 __device__ int blk_cholqr2(double* A, int ld, int m, int n, double* R, const Work& w) {
-  double* G = w.S4;
+  double* G = w.S4;            // n x gl, gl odd (conflict-free column walks)
+  const int gl = n | 1;
+  double* dinv = w.sc3 + 4;    // reuses the tail of vec (see carve): n doubles
+  double* diag0 = w.vec;
   for (int pass = 0; pass < 2; ++pass) {
-    blk_gram(A, ld, m, n, G);
-    double gmin = 0.0;
-    if (threadIdx.x == 0) {
-      gmin = G[0];
-      for (int j = 1; j < n; ++j) gmin = fmin(gmin, G[j * n + j]);
-      w.sc3[3] = gmin;
-    }
-    // remember the diagonal for the relative pivot test
-    for (int j = threadIdx.x; j < n; j += blockDim.x) w.vec[j] = G[j * n + j];
+    blk_gram(A, ld, m, n, G, gl);
+    for (int j = threadIdx.x; j < n; j += blockDim.x) diag0[j] = G[j * gl + j];
     __syncthreads();
-    bool ok = blk_chol_warp(G, n);
+    bool ok = blk_chol_warp(G, n, gl);
     if (ok) {
       __shared__ int s_ok2;
       if (threadIdx.x == 0) {
         int o = 1;
         for (int j = 0; j < n; ++j)
-          if (!(G[j * n + j] * G[j * n + j] > 1e-14 * w.vec[j])) o = 0;
+          if (!(G[j * gl + j] * G[j * gl + j] > 1e-14 * diag0[j])) o = 0;
         s_ok2 = o;
       }
       __syncthreads();
       ok = s_ok2 != 0;
     }
     if (!ok) return pass == 0 ? 1 : 2;
-    blk_solve_rows(A, ld, m, n, G);
-    // R <- L^T R (pass 1) or L^T (pass 0)
+    blk_solve_rows(A, ld, m, n, G, gl, dinv);
     if (pass == 0) {
       for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
         const int i = e / n, j = e - i * n;
-        R[e] = j >= i ? G[j * n + i] : 0.0;
+        R[e] = j >= i ? G[j * gl + i] : 0.0;
       }
     } else {
       double* T = w.S5;
       for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
         const int i = e / n, j = e - i * n;
         double acc = 0.0;
-        for (int q = i; q <= j; ++q) acc = fma(G[q * n + i], R[q * n + j], acc);
+        for (int q = i; q <= j; ++q) acc = fma(G[q * gl + i], R[q * n + j], acc);
         T[e] = j >= i ? acc : 0.0;
       }
       __syncthreads();
@@ -336,12 +338,13 @@ __device__ int blk_cholqr2(double* A, int ld, int m, int n, double* R, const Wor
     __syncthreads();
   }
   // orthogonality check ||Q^T Q - I||_max <= 1e-13
-  blk_gram(A, ld, m, n, G);
+  blk_gram(A, ld, m, n, G, gl);
   __shared__ int s_orth;
   if (threadIdx.x == 0) s_orth = 1;
   __syncthreads();
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    const double v = G[e] - ((e / n == e % n) ? 1.0 : 0.0);
+    const int i = e / n, j = e - i * n;
+    const double v = G[i * gl + j] - (i == j ? 1.0 : 0.0);
     if (!(fabs(v) <= 1e-13)) s_orth = 0;
   }
   __syncthreads();
@@ -374,6 +377,7 @@ __device__ int qr_explicit(double* A, int ld, int m, int n, double* Rout, const 
   const int kmin = m < n ? m : n;
   if (m >= n) {
     const int st = blk_cholqr2(A, ld, m, n, Rout, w);
+    if (threadIdx.x == 0 && w.diag) w.diag[st == 0 ? 6 : (st == 1 ? 7 : 5)] += 1;   // diagnostic
     if (st == 0) return kmin;
     if (st == 2) {
       // finish: Q1 = Q_h R_h  =>  A_orig = Q_h (R_h R1)
@@ -560,6 +564,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_orth(DenseArgs a) {
   int S = 2;
   for (int k = 0; k <= d; ++k) S = a.r[k] > S ? a.r[k] : S;
   Work w = carve(smraw, a.smem_doubles, S);
+  w.diag = sc->cyc;
   // A4: U_k = phi_k (.)_2 C_k
   for (int k = 0; k < d; ++k) {
     const int r0 = a.r[k], nk = a.n[k], r1 = a.r[k + 1];
@@ -661,7 +666,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_orth(DenseArgs a) {
     blk_copy(a.L + a.p_off[k], Ls, (int64_t)R1 * R1);
     __syncthreads();
   }
-  pc.stop(sc, 6);
+  pc.stop(sc, 4);
   if (!ok && threadIdx.x == 0) {
     atomicOr(&sc->err, (int)kErrChol);
     sc->noop = 1;
@@ -784,6 +789,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
   int S = 2;
   for (int k = 0; k <= d; ++k) S = 2 * a.r[k] > S ? 2 * a.r[k] : S;
   Work w = carve(smraw, a.smem_doubles, S);
+  w.diag = sc->cyc;
   double* gw = a.work;
   __shared__ int curR[kMaxD + 1];
   if (threadIdx.x == 0) {
