@@ -46,47 +46,6 @@ __device__ __forceinline__ double2 ld2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
 
-// L2 eviction-priority hints: the gathered table rows are re-read by many samples
-// (evict_last keeps them resident), the per-sample streams are touched once
-// (evict_first, no L1 allocation).
-__device__ __forceinline__ unsigned long long policy_last() {
-  unsigned long long p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ unsigned long long policy_first() {
-  unsigned long long p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ double2 ld2_keep(const double* p, unsigned long long pol) {
-  double2 v;
-  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-               : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ int ld_stream_i(const int* p, unsigned long long pol) {
-  int v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
-               : "=r"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ double ld_stream_d(const double* p, unsigned long long pol) {
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
-               : "=d"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ double ld_once_d(const double* p, unsigned long long pol) {
-  double v;   // g may have been written by this grid's earlier kernels: plain (coherent) load
-  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
-               : "=d"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ void st_stream_d(double* p, double v, unsigned long long pol) {
-  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" :: "l"(p), "d"(v), "l"(pol));
-}
-
 template <int LPS, int MODE>
 __global__ void __launch_bounds__(256) k_seg(SegDev a, const Scalars* sc) {
   if (sc && sc->noop) return;
@@ -98,7 +57,6 @@ __global__ void __launch_bounds__(256) k_seg(SegDev a, const Scalars* sc) {
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (warp >= a.nwarps) return;
   const int ld = a.ld;
-  const unsigned long long keep = policy_last(), once = policy_first();
   const int64_t v0 = a.warp_vbegin[warp], v1 = a.warp_vbegin[warp + 1];
   for (int64_t v = v0; v < v1; ++v) {
     const int32_t row = a.vrow_row[v];
@@ -116,9 +74,9 @@ __global__ void __launch_bounds__(256) k_seg(SegDev a, const Scalars* sc) {
       int colv = 0;
       double xv = 0.0;    // y (SDDMM) or g (GSQ, SPMM)
       if (have) {
-        if (MODE != kGSQ) colv = ld_stream_i(a.col + s, once);
-        if (MODE == kSDDMM) xv = ld_stream_d(a.y + s, once);
-        else xv = a.perm ? ld_once_d(a.g + ld_stream_i(a.perm + s, once), once) : ld_once_d(a.g + s, once);
+        if (MODE != kGSQ) colv = a.col[s];
+        if (MODE == kSDDMM) xv = a.y[s];
+        else xv = a.perm ? a.g[a.perm[s]] : a.g[s];
       }
       if (MODE == kGSQ) {
         accs = fma(xv, xv, accs);
@@ -134,7 +92,7 @@ __global__ void __launch_bounds__(256) k_seg(SegDev a, const Scalars* sc) {
           const int cidx = __shfl_sync(kFull, colv, t & 31);
           xs[u] = __shfl_sync(kFull, xv, t & 31);
           b[u] = make_double2(0.0, 0.0);
-          if (t < nc) b[u] = ld2_keep(a.coltab + (int64_t)cidx * ld + 2 * sub, keep);
+          if (t < nc) b[u] = ld2(a.coltab + (int64_t)cidx * ld + 2 * sub);
         }
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
@@ -146,7 +104,7 @@ __global__ void __launch_bounds__(256) k_seg(SegDev a, const Scalars* sc) {
             if (t < nc) {
               const double gv = part - xs[u];
               if (sub == 0) {
-                st_stream_d(a.g + beg + c0 + t, gv, once);
+                a.g[beg + c0 + t] = gv;
                 accs = fma(gv, gv, accs);
               }
             }

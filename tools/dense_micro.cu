@@ -8,7 +8,7 @@ namespace prgd {
 namespace {
 __global__ void __launch_bounds__(kDenseThreads) k_micro(int which, int m, int n, int reps, long long* out) {
   extern __shared__ double smraw[];
-  Work w = carve(smraw, (200 * 1024) / 8, 64);
+  Work w = carve(smraw, (200 * 1024) / 8, 32);
   const int ld = n | 1;
   double* A = w.mat;
   for (int e = threadIdx.x; e < m * ld; e += blockDim.x) {
