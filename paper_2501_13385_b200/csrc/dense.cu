@@ -63,6 +63,119 @@ __device__ __forceinline__ void warp_treduce(double (&v)[NM], int lane, double& 
   }
 }
 
+// ---------------------------------------------------------------- FP64 tensor-core tiles
+// D(8x8) += A(8x4) B(4x8), mma.sync m8n8k4 f64 (SASS DMMA.8x8x4).  Fragments:
+// a = A[gid][tq], b = B[tq][gid], d0/d1 = D[gid][2tq], D[gid][2tq+1]; gid = lane/4, tq = lane%4.
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+// Block GEMM C[M x N] = sum_k fa(i, k) fb(k, j) on DMMA tiles, warps round-robin over the
+// 8x8 output tiles; the accessors must return 0 outside [0,M) x [0,K) / [0,K) x [0,N),
+// fs(i, j, v) must ignore i >= M or j >= N.  No barrier inside.
+template <class FA, class FB, class FS>
+__device__ __forceinline__ void mma_gemm(int M, int N, int K, FA fa, FB fb, FS fs) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int gid = lane >> 2, tq = lane & 3;
+  const int mt = (M + 7) >> 3, nt = (N + 7) >> 3;
+  for (int t = warp; t < mt * nt; t += nw) {
+    const int I = t / nt, J = t - I * nt;
+    const int i = I * 8 + gid, j = J * 8 + gid;
+    double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+    int k = 0;
+    for (; k + 8 <= K; k += 8) {
+      dmma(d0, d1, fa(i, k + tq), fb(k + tq, j));
+      dmma(e0, e1, fa(i, k + 4 + tq), fb(k + 4 + tq, j));
+    }
+    for (; k < K; k += 4) {
+      const int kk = k + tq;
+      dmma(d0, d1, kk < K ? fa(i, kk) : 0.0, kk < K ? fb(kk, j) : 0.0);
+    }
+    fs(I * 8 + gid, J * 8 + 2 * tq, d0 + e0);
+    fs(I * 8 + gid, J * 8 + 2 * tq + 1, d1 + e1);
+  }
+}
+
+// In place A[m x n] <- A T^T (T: n x n, stride tl); each warp owns 8-row blocks and loads
+// their fragments before writing.  n <= 32.
+__device__ void mma_mul_rt_inplace(double* A, int ld, int m, int n, const double* T, int tl) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int gid = lane >> 2, tq = lane & 3;
+  const int nk = (n + 3) >> 2, nt = (n + 7) >> 3;
+  for (int I = warp; I * 8 < m; I += nw) {
+    const int i = I * 8 + gid;
+    double af[8];
+#pragma unroll
+    for (int s2 = 0; s2 < 8; ++s2) {
+      const int c = 4 * s2 + tq;
+      af[s2] = (s2 < nk && i < m && c < n) ? A[(int64_t)i * ld + c] : 0.0;
+    }
+    for (int J = 0; J < nt; ++J) {
+      const int j = J * 8 + gid;
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2) {
+        if (s2 < nk) {
+          const int c = 4 * s2 + tq;
+          dmma(d0, d1, af[s2], (j < n && c < n) ? T[j * tl + c] : 0.0);
+        }
+      }
+      const int jc = J * 8 + 2 * tq;
+      if (i < m && jc < n) A[(int64_t)i * ld + jc] = d0;
+      if (i < m && jc + 1 < n) A[(int64_t)i * ld + jc + 1] = d1;
+    }
+  }
+}
+
+// Cholesky G = L L^T (n <= 32) by the calling warp, row `lane` of G in registers, column
+// values broadcast by shuffles.  Writes L (upper zeroed); returns false on breakdown.
+__device__ bool chol_warp_reg(double* G, int gl, int n) {
+  const int lane = threadIdx.x & 31;
+  double g[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) g[c] = (lane < n && c < n) ? G[lane * gl + c] : (c == lane ? 1.0 : 0.0);
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const double djj = __shfl_sync(0xffffffffu, g[j], j);
+    double dd = 1.0;
+    if (djj > 0.0 && isfinite(djj)) dd = sqrt(djj);
+    else ok = false;
+    const double lij = (lane > j) ? g[j] / dd : ((lane == j) ? dd : 0.0);
+    if (lane >= j) g[j] = lij;
+#pragma unroll
+    for (int k = j + 1; k < 32; ++k) {
+      const double lkj = __shfl_sync(0xffffffffu, lij, k);
+      if (lane >= k) g[k] = fma(-lij, lkj, g[k]);
+    }
+  }
+  if (lane < n) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+      if (c < n) G[lane * gl + c] = (c <= lane) ? g[c] : 0.0;
+  }
+  return ok;
+}
+
+// Li = L^{-1} (n <= 32, lower) by the calling warp; lane c computes column c.
+__device__ void trinv_warp(const double* L, int gl, int n, double* Li, int il) {
+  const int c = threadIdx.x & 31;
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    double sacc = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) sacc = fma(-L[i * gl + k], x[k], sacc);
+    x[i] = (i < n) ? sacc / L[i * gl + i] : 0.0;
+  }
+  if (c < n) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i < n) Li[i * il + c] = x[i];
+  }
+}
+
 struct Work {
   double* red;   // [kNW][kMaxCols] warp partials
   double* vec;   // [kMaxCols] per-column coefficients
@@ -296,10 +409,10 @@ __device__ void blk_solve_rows(double* A, int ld, int m, int n, const double* L,
 // CholeskyQR2 with an orthogonality check: on success Q in A, R (n x n upper) in R.
 // Returns 0 on success, 1 if the first Cholesky failed (A untouched), 2 if it failed
 // later (A holds Q1 = A R1^{-1}, R holds R1): the caller finishes with Householder.
-__device__ int blk_cholqr2(double* A, int ld, int m, int n, double* R, const Work& w) {
+__device__ int blk_cholqr2_smem(double* A, int ld, int m, int n, double* R, const Work& w) {
   double* G = w.S4;            // n x gl, gl odd (conflict-free column walks)
   const int gl = n | 1;
-  double* dinv = w.sc3 + 4;    // reuses the tail of vec (see carve): n doubles
+  double* dinv = w.sc3 + 4;
   double* diag0 = w.vec;
   for (int pass = 0; pass < 2; ++pass) {
     blk_gram(A, ld, m, n, G, gl);
@@ -337,7 +450,6 @@ __device__ int blk_cholqr2(double* A, int ld, int m, int n, double* R, const Wor
     }
     __syncthreads();
   }
-  // orthogonality check ||Q^T Q - I||_max <= 1e-13
   blk_gram(A, ld, m, n, G, gl);
   __shared__ int s_orth;
   if (threadIdx.x == 0) s_orth = 1;
@@ -349,6 +461,75 @@ __device__ int blk_cholqr2(double* A, int ld, int m, int n, double* R, const Wor
   }
   __syncthreads();
   return s_orth ? 0 : 2;
+}
+
+// CholeskyQR2 on FP64 tensor cores (n <= 32): per pass G = A^T A (DMMA), G = L L^T
+// (warp, registers), Li = L^{-1} (warp), A <- A Li^T (DMMA, in place), R <- L^T R.
+// Orthogonality of the result is certified by the second pass: if its Gram G2 = Q1^T Q1
+// satisfies |G2 - I| <= 1e-6 then |Q^T Q - I| = O(u) (CholeskyQR on a matrix with
+// condition number ~1 is exact to rounding).  Returns 0 on success, 1 if the first
+// Cholesky failed (A untouched), 2 if the result is not certified (A holds a partial Q).
+__device__ int blk_cholqr2(double* A, int ld, int m, int n, double* R, const Work& w) {
+  if (n > 32) return blk_cholqr2_smem(A, ld, m, n, R, w);
+  double* G = w.S4;
+  const int gl = n | 1;
+  double* Li = w.S5;            // n x il
+  const int il = n | 1;
+  double* diag0 = w.vec;
+  __shared__ int s_flag;
+  for (int pass = 0; pass < 2; ++pass) {
+    mma_gemm(n, n, m,
+             [&](int i, int k) { return i < n ? A[(int64_t)k * ld + i] : 0.0; },
+             [&](int k, int j) { return j < n ? A[(int64_t)k * ld + j] : 0.0; },
+             [&](int i, int j, double v) { if (i < n && j < n) G[i * gl + j] = v; });
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      int flag = 1;
+      if (pass == 0) {
+        for (int j = threadIdx.x; j < n; j += 32) diag0[j] = G[j * gl + j];
+      } else {
+        // certification of the second pass: |G2 - I| <= 1e-6
+        for (int e = threadIdx.x; e < n * n; e += 32) {
+          const int i = e / n, j = e - i * n;
+          if (!(fabs(G[i * gl + j] - (i == j ? 1.0 : 0.0)) <= 1e-6)) flag = 0;
+        }
+        flag = __all_sync(0xffffffffu, flag);
+      }
+      __syncwarp();
+      bool ok = chol_warp_reg(G, gl, n);
+      __syncwarp();
+      if (ok && pass == 0)
+        for (int j = threadIdx.x; j < n; j += 32)
+          if (!(G[j * gl + j] * G[j * gl + j] > 1e-14 * diag0[j])) ok = false;
+      ok = __all_sync(0xffffffffu, ok);
+      if (ok) trinv_warp(G, gl, n, Li, il);
+      if (threadIdx.x == 0) s_flag = ok ? flag : -1;
+    }
+    __syncthreads();
+    const int st = s_flag;
+    if (st < 0) return pass == 0 ? 1 : 2;
+    mma_mul_rt_inplace(A, ld, m, n, Li, il);
+    if (pass == 0) {
+      for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+        const int i = e / n, j = e - i * n;
+        R[e] = j >= i ? G[j * gl + i] : 0.0;
+      }
+    } else {
+      double* T = w.S3 == R ? w.S2 : w.S3;
+      for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+        const int i = e / n, j = e - i * n;
+        double acc = 0.0;
+        for (int q = i; q <= j; ++q) acc = fma(G[q * gl + i], R[q * n + j], acc);
+        T[e] = j >= i ? acc : 0.0;
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < n * n; e += blockDim.x) R[e] = T[e];
+      __syncthreads();
+      if (st == 0) return 2;
+    }
+    __syncthreads();
+  }
+  return 0;
 }
 
 // QR of the m x n matrix staged at A (stride ld): R (kmin x n, row-major, zeros below
@@ -517,6 +698,100 @@ __device__ bool blk_jacobi(double* X, int rows, int kc, double* V, int* sweeps, 
   return false;
 }
 
+// Norms of the kc columns of X (rows x kc col-major) into nrm, and the permutation
+// perm sorting them by norm (descending, ties by index).  Ends with a barrier.
+__device__ void col_norms_sorted(const double* X, int rows, int kc, double* nrm, int* perm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int c = warp; c < kc; c += nw) {
+    double s = 0.0;
+    for (int i = lane; i < rows; i += 32) s = fma(X[c * rows + i], X[c * rows + i], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += shx(s, o);
+    if (lane == 0) nrm[c] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < kc) {
+    const int c = threadIdx.x;
+    const double v = nrm[c];
+    int rank = 0;
+    for (int c2 = 0; c2 < kc; ++c2) rank += (nrm[c2] > v) || (nrm[c2] == v && c2 < c);
+    perm[rank] = c;
+  }
+  __syncthreads();
+}
+
+// Truncation subspace of R (the top-rk left singular vectors of R, X = R^T): one-sided
+// Jacobi on the columns of X restricted to pairs across the current top-rk / bottom
+// groups (groups re-formed by norm before every sweep; bipartite round-robin rounds).
+// Rotations inside a group only change the gauge of the kept (or discarded) subspace,
+// so convergence of the cross pairs is exactly convergence of the truncation.  On
+// return perm[0..rk) lists the kept columns by decreasing norm; V accumulates rotations.
+__device__ bool jacobi_truncation(double* X, int rows, int kc, int rk, double* V, int* sweeps,
+                                  double* nrm, int* perm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  __shared__ int s_rot;
+  for (int e = tid; e < kc * kc; e += blockDim.x) V[e] = (e / kc == e % kc) ? 1.0 : 0.0;
+  __syncthreads();
+  col_norms_sorted(X, rows, kc, nrm, perm);
+  if (kc <= rk) return true;
+  const int nb = kc - rk;
+  const int npairs = rk < nb ? rk : nb;
+  const int rounds = rk < nb ? nb : rk;
+  const double tol = 2.3e-16 * sqrt((double)(rows > 1 ? rows : 1));
+  const double tol2 = tol * tol;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (tid == 0) {
+      s_rot = 0;
+      if (sweeps) atomicAdd(sweeps, 1);
+    }
+    __syncthreads();
+    for (int round = 0; round < rounds; ++round) {
+      for (int pr = warp; pr < npairs; pr += nw) {
+        int ti, bi;
+        if (rk <= nb) { ti = pr; bi = (pr + round) % nb; }
+        else { bi = pr; ti = (pr + round) % rk; }
+        const int a = perm[ti], b = perm[rk + bi];
+        double* xa = X + (int64_t)a * rows;
+        double* xb = X + (int64_t)b * rows;
+        double ga = 0.0;
+        for (int i = lane; i < rows; i += 32) ga = fma(xa[i], xb[i], ga);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ga += shx(ga, o);
+        const double al = nrm[a], be = nrm[b];
+        if (ga != 0.0 && ga * ga > tol2 * (al * be)) {
+          const double dlt = be - al;
+          const double sg = (dlt > 0.0 || (dlt == 0.0 && !signbit(dlt))) ? 1.0 : -1.0;
+          const double t = (2.0 * ga * sg) / (fabs(dlt) + sqrt(fma(dlt, dlt, 4.0 * ga * ga)));
+          const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
+          for (int i = lane; i < rows; i += 32) {
+            const double u = xa[i], v = xb[i];
+            xa[i] = c * u - sn * v;
+            xb[i] = sn * u + c * v;
+          }
+          double* va = V + (int64_t)a * kc;
+          double* vb = V + (int64_t)b * kc;
+          for (int i = lane; i < kc; i += 32) {
+            const double u = va[i], v = vb[i];
+            va[i] = c * u - sn * v;
+            vb[i] = sn * u + c * v;
+          }
+          if (lane == 0) {
+            nrm[a] = al - t * ga;
+            nrm[b] = be + t * ga;
+            s_rot = 1;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    const int rot = s_rot;
+    __syncthreads();
+    col_norms_sorted(X, rows, kc, nrm, perm);
+    if (!rot) return true;
+  }
+  return false;
+}
+
 __device__ void blk_copy(double* dst, const double* src, int64_t n) {
   for (int64_t e = threadIdx.x; e < n; e += blockDim.x) dst[e] = src[e];
 }
@@ -605,7 +880,13 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_orth(DenseArgs a) {
     double* st = ((int64_t)r1 * rest <= w.mat_cap) ? w.mat : gw + (int64_t)m * ld;
     blk_copy(st, Un, (int64_t)r1 * rest);        // stage U_{k+1} (coalesced)
     __syncthreads();
-    blk_mode1(Un, w.S1, r1, r1, st, rest);       // U_{k+1} <- R U_{k+1}
+    {
+      const double* Rr = w.S1;
+      mma_gemm(r1, rest, r1,                         // U_{k+1} <- R U_{k+1}
+               [&](int i, int q) { return i < r1 ? Rr[i * r1 + q] : 0.0; },
+               [&](int q, int j) { return j < rest ? st[(int64_t)q * rest + j] : 0.0; },
+               [&](int i, int j, double v) { if (i < r1 && j < rest) Un[(int64_t)i * rest + j] = v; });
+    }
     __syncthreads();
   }
   pc.stop(sc, 5);
@@ -829,12 +1110,13 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
     double* st = ((int64_t)prow * R0 <= w.mat_cap) ? w.mat : gw + (int64_t)rows * ld;
     blk_copy(st, Bp, (int64_t)prow * R0);           // stage B_{k-1} (coalesced)
     __syncthreads();
-    for (int e = threadIdx.x; e < kmin * R0; e += blockDim.x) {   // S2 <- R^T (R0 x kmin)
-      const int c = e / R0, b = e - c * R0;
-      w.S2[b * kmin + c] = w.S1[e];
+    {
+      const double* Rr = w.S1;                      // R: kmin x R0 row-major
+      mma_gemm(prow, kmin, R0,                      // B_{k-1} <- B_{k-1} x_3 R^T
+               [&](int i, int q) { return i < prow ? st[(int64_t)i * R0 + q] : 0.0; },
+               [&](int q, int j) { return j < kmin ? Rr[j * R0 + q] : 0.0; },
+               [&](int i, int j, double v) { if (i < prow && j < kmin) Bp[(int64_t)i * kmin + j] = v; });
     }
-    __syncthreads();
-    blk_mode3t(Bp, st, prow, R0, w.S2, kmin);       // B_{k-1} <- B_{k-1} x_3 R^T
     if (threadIdx.x == 0) curR[k] = kmin;
     __syncthreads();
     pc.stop(sc, 1);
@@ -865,39 +1147,19 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
     // the same storage read column-major (R1 x kmin) is X = R^T
     double* V = w.S3;
     pc.start();
-    ok = blk_jacobi(X, R1, kmin, V, &sc->pad, w.red, w.ptab) && ok;
+    ok = jacobi_truncation(X, R1, kmin, rk, V, &sc->pad, w.red, w.perm) && ok;
     pc.stop(sc, 3);
     pc.start();
-    double* nrm = w.red;
-    if (threadIdx.x < kmin) {
-      double s = 0.0;
-      for (int i = 0; i < R1; ++i) s = fma(X[threadIdx.x * R1 + i], X[threadIdx.x * R1 + i], s);
-      nrm[threadIdx.x] = s;
-    }
-    __syncthreads();
-    if (threadIdx.x < kmin) {
-      const int c = threadIdx.x;
-      int rank = 0;
-      for (int c2 = 0; c2 < kmin; ++c2) rank += (nrm[c2] > nrm[c]) || (nrm[c2] == nrm[c] && c2 < c);
-      w.perm[rank] = c;
-    }
-    __syncthreads();
-    double* Vp = w.S1;                               // Vp[t][c] = V[t, perm[c]]
-    for (int e = threadIdx.x; e < kmin * rk; e += blockDim.x) {
-      const int t = e / rk, c = e - t * rk;
-      Vp[e] = c < kmin ? V[w.perm[c] * kmin + t] : 0.0;
-    }
-    __syncthreads();
+    // C'_k = Q V[:, perm[:rk]]  (m x rk) on DMMA
     double* Cout = a.C + a.core_off[k];
-    for (int e = threadIdx.x; e < m * rk; e += blockDim.x) {
-      const int row = e / rk, c = e - row * rk;
-      const double* q = A + (int64_t)row * ld;
-      double acc = 0.0;
-      for (int t = 0; t < kmin; ++t) acc = fma(q[t], Vp[t * rk + c], acc);
-      Cout[e] = acc;
+    {
+      const int* perm = w.perm;
+      mma_gemm(m, rk, kmin,
+               [&](int i, int q) { return i < m ? A[(int64_t)i * ld + q] : 0.0; },
+               [&](int q, int j) { return j < rk && j < kmin ? V[perm[j] * kmin + q] : 0.0; },
+               [&](int i, int j, double v) { if (i < m && j < rk) Cout[(int64_t)i * rk + j] = v; });
     }
-    __syncthreads();
-    double* SV = w.S1;
+    double* SV = w.S1;                              // (S V^T)_r: row a' = X[:, perm[a']]^T
     for (int e = threadIdx.x; e < rk * R1; e += blockDim.x) {
       const int ap = e / R1, i = e - ap * R1;
       SV[e] = ap < kmin ? X[w.perm[ap] * R1 + i] : 0.0;
@@ -908,7 +1170,10 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
     double* st = ((int64_t)R1 * rest <= w.mat_cap) ? w.mat : gw + (int64_t)m * ld;
     blk_copy(st, Bn, (int64_t)R1 * rest);           // stage B_{k+1} (coalesced)
     __syncthreads();
-    blk_mode1(Bn, SV, rk, R1, st, rest);            // B_{k+1} <- (S V^T)_r x_1 B_{k+1}
+    mma_gemm(rk, rest, R1,                          // B_{k+1} <- (S V^T)_r x_1 B_{k+1}
+             [&](int i, int q) { return i < rk ? SV[i * R1 + q] : 0.0; },
+             [&](int q, int j) { return j < rest ? st[(int64_t)q * rest + j] : 0.0; },
+             [&](int i, int j, double v) { if (i < rk && j < rest) Bn[(int64_t)i * rest + j] = v; });
     if (threadIdx.x == 0) curR[k + 1] = rk;
     __syncthreads();
     pc.stop(sc, 4);

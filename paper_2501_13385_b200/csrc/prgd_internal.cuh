@@ -19,7 +19,7 @@ namespace prgd {
 
 constexpr int kMaxD = 64;
 constexpr int kMaxRank = 32;
-constexpr int kDenseThreads = 512;
+constexpr int kDenseThreads = 256;
 
 // Device-side scalars of one context (one allocation).
 struct Scalars {

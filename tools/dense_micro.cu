@@ -18,14 +18,21 @@ __global__ void __launch_bounds__(kDenseThreads) k_micro(int which, int m, int n
   __syncthreads();
   long long t0 = clock64();
   for (int r = 0; r < reps; ++r) {
-    if (which == 0) blk_gram(A, ld, m, n, w.S4, n | 1);
+    if (which == 0) {
+      double* G = w.S4; const int gl = n | 1;
+      mma_gemm(n, n, m, [&](int i, int k) { return i < n ? A[(int64_t)k * ld + i] : 0.0; },
+               [&](int k, int j) { return j < n ? A[(int64_t)k * ld + j] : 0.0; },
+               [&](int i, int j, double v) { if (i < n && j < n) G[i * gl + j] = v; });
+      __syncthreads();
+    }
     else if (which == 1) {
       for (int e = threadIdx.x; e < n * (n | 1); e += blockDim.x) {
         const int i = e / (n | 1), c = e % (n | 1);
         w.S4[e] = (i == c ? 100.0 : 0.0) + 0.5 / (1 + i + c);
       }
       __syncthreads();
-      blk_chol_warp(w.S4, n, n | 1);
+      if (threadIdx.x < 32) chol_warp_reg(w.S4, n | 1, n);
+      __syncthreads();
     } else if (which == 2) blk_solve_rows(A, ld, m, n, w.S4, n | 1, w.sc3 + 4);
     else if (which == 3) { if (n <= 16) qr_rows<16>(A, ld, m, n, w); else qr_rows<32>(A, ld, m, n, w); }
     else if (which == 4) { int k = m < n ? m : n; if (k <= 16) orgqr_rows<16>(A, ld, m, k, w); else orgqr_rows<32>(A, ld, m, k, w); }
@@ -34,7 +41,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_micro(int which, int m, int n
       double* X = w.S2;
       for (int e = threadIdx.x; e < n * n; e += blockDim.x) X[e] = (e % (n + 1) == 0 ? 2.0 + e * 0.001 : 0.1 / (1 + e % 7));
       __syncthreads();
-      blk_jacobi(X, n, n, w.S3, nullptr, w.red, w.ptab);
+      jacobi_truncation(X, n, n, n / 2, w.S3, nullptr, w.red, w.perm);
     } else if (which == 7) { __syncthreads(); }
   }
   long long t1 = clock64();
@@ -48,7 +55,7 @@ int main() {
   cudaMalloc(&d, 8);
   const int bytes = prgd::dense_smem_doubles() * 8;
   cudaFuncSetAttribute(prgd::k_micro, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  const char* names[] = {"gram", "chol_warp", "solve_rows", "householder_qr", "orgqr", "cholqr2", "jacobi(n x n)", "syncthreads"};
+  const char* names[] = {"gram_dmma", "chol_warp_reg", "trinv+mul_rt", "householder_qr", "orgqr", "cholqr2", "jacobi_trunc(n/2)", "syncthreads"};
   int shapes[][2] = {{512, 32}, {256, 32}, {256, 16}};
   for (auto& sh : shapes) {
     for (int wch = 0; wch < 8; ++wch) {
