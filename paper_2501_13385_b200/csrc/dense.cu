@@ -128,52 +128,63 @@ __device__ void mma_mul_rt_inplace(double* A, int ld, int m, int n, const double
   }
 }
 
-// Cholesky G = L L^T (n <= 32) by the calling warp, row `lane` of G in registers, column
-// values broadcast by shuffles.  Writes L (upper zeroed); returns false on breakdown.
-__device__ bool chol_warp_reg(double* G, int gl, int n) {
-  const int lane = threadIdx.x & 31;
-  double g[32];
-#pragma unroll
-  for (int c = 0; c < 32; ++c) g[c] = (lane < n && c < n) ? G[lane * gl + c] : (c == lane ? 1.0 : 0.0);
+// Cholesky G = L L^T (n <= 64) by the whole CTA, in place (stride gl, upper zeroed).
+// Step j: every thread reads the pivot itself (no broadcast barrier), r_j = rsqrt(pivot);
+// the trailing update G[i][k] -= G[i][j] G[k][j] r_j^2 (j < k <= i) is spread over all
+// threads; column j is scaled at the end from the saved r_j.  One barrier per step.
+// Returns false (CTA-uniform) on a non-positive or non-finite pivot.
+__device__ bool chol_cta(double* G, int gl, int n, double* rinv) {
   bool ok = true;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const double djj = __shfl_sync(0xffffffffu, g[j], j);
-    double dd = 1.0;
-    if (djj > 0.0 && isfinite(djj)) dd = sqrt(djj);
-    else ok = false;
-    const double lij = (lane > j) ? g[j] / dd : ((lane == j) ? dd : 0.0);
-    if (lane >= j) g[j] = lij;
-#pragma unroll
-    for (int k = j + 1; k < 32; ++k) {
-      const double lkj = __shfl_sync(0xffffffffu, lij, k);
-      if (lane >= k) g[k] = fma(-lij, lkj, g[k]);
+  for (int j = 0; j < n; ++j) {
+    const double djj = G[j * gl + j];
+    const bool good = djj > 0.0 && isfinite(djj);
+    ok = ok && good;
+    const double rj = good ? rsqrt(djj) : 1.0;
+    const double rj2 = rj * rj;
+    if (threadIdx.x == 0) rinv[j] = rj;
+    const int nr = n - 1 - j;                       // rows/cols j+1..n-1
+    const int ntri = nr * (nr + 1) / 2;
+    for (int t = threadIdx.x; t < ntri; t += blockDim.x) {
+      // t -> (i, k) with j < k <= i: row-major over the lower triangle
+      int i = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+      while ((i + 1) * (i + 2) / 2 <= t) ++i;
+      while (i * (i + 1) / 2 > t) --i;
+      const int k = t - i * (i + 1) / 2;
+      const int gi = j + 1 + i, gk = j + 1 + k;
+      G[gi * gl + gk] = fma(-G[gi * gl + j] * rj2, G[gk * gl + j], G[gi * gl + gk]);
     }
+    __syncthreads();
   }
-  if (lane < n) {
-#pragma unroll
-    for (int c = 0; c < 32; ++c)
-      if (c < n) G[lane * gl + c] = (c <= lane) ? g[c] : 0.0;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, c = e - i * n;
+    double v;
+    if (c > i) v = 0.0;
+    else if (c == i) v = G[i * gl + i] * rinv[i];   // sqrt(pivot) = pivot * rsqrt(pivot)
+    else v = G[i * gl + c] * rinv[c];
+    G[i * gl + c] = v;
   }
+  __syncthreads();
   return ok;
 }
 
-// Li = L^{-1} (n <= 32, lower) by the calling warp; lane c computes column c.
-__device__ void trinv_warp(const double* L, int gl, int n, double* Li, int il) {
-  const int c = threadIdx.x & 31;
-  double x[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    double sacc = (i == c) ? 1.0 : 0.0;
-#pragma unroll
-    for (int k = 0; k < i; ++k) sacc = fma(-L[i * gl + k], x[k], sacc);
-    x[i] = (i < n) ? sacc / L[i * gl + i] : 0.0;
-  }
+// Li = L^{-1} (lower, n <= 64): thread c < n computes column c by forward substitution
+// directly into Li (shared memory), x_i = (delta_ic - sum_{c<=k<i} L[i][k] x_k) / L[i][i].
+__device__ void trinv_cta(const double* L, int gl, int n, double* Li, int il) {
+  const int c = threadIdx.x;
   if (c < n) {
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (i < n) Li[i * il + c] = x[i];
+    for (int i = 0; i < c; ++i) Li[i * il + c] = 0.0;
+    for (int i = c; i < n; ++i) {
+      double s0 = (i == c) ? 1.0 : 0.0, s1 = 0.0;
+      int k = c;
+      for (; k + 1 < i; k += 2) {
+        s0 = fma(-L[i * gl + k], Li[k * il + c], s0);
+        s1 = fma(-L[i * gl + k + 1], Li[(k + 1) * il + c], s1);
+      }
+      if (k < i) s0 = fma(-L[i * gl + k], Li[k * il + c], s0);
+      Li[i * il + c] = (s0 + s1) / L[i * gl + i];
+    }
   }
+  __syncthreads();
 }
 
 struct Work {
@@ -470,7 +481,7 @@ __device__ int blk_cholqr2_smem(double* A, int ld, int m, int n, double* R, cons
 // condition number ~1 is exact to rounding).  Returns 0 on success, 1 if the first
 // Cholesky failed (A untouched), 2 if the result is not certified (A holds a partial Q).
 __device__ int blk_cholqr2(double* A, int ld, int m, int n, double* R, const Work& w) {
-  if (n > 32) return blk_cholqr2_smem(A, ld, m, n, R, w);
+  if (n > 32) return blk_cholqr2_smem(A, ld, m, n, R, w);   // (mma_mul_rt_inplace: n <= 32)
   double* G = w.S4;
   const int gl = n | 1;
   double* Li = w.S5;            // n x il
@@ -483,30 +494,25 @@ __device__ int blk_cholqr2(double* A, int ld, int m, int n, double* R, const Wor
              [&](int k, int j) { return j < n ? A[(int64_t)k * ld + j] : 0.0; },
              [&](int i, int j, double v) { if (i < n && j < n) G[i * gl + j] = v; });
     __syncthreads();
-    if (threadIdx.x < 32) {
-      int flag = 1;
-      if (pass == 0) {
-        for (int j = threadIdx.x; j < n; j += 32) diag0[j] = G[j * gl + j];
-      } else {
-        // certification of the second pass: |G2 - I| <= 1e-6
-        for (int e = threadIdx.x; e < n * n; e += 32) {
-          const int i = e / n, j = e - i * n;
-          if (!(fabs(G[i * gl + j] - (i == j ? 1.0 : 0.0)) <= 1e-6)) flag = 0;
-        }
-        flag = __all_sync(0xffffffffu, flag);
+    if (threadIdx.x == 0) s_flag = 1;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) diag0[e] = G[e * gl + e];
+    __syncthreads();
+    if (pass == 1) {
+      // certification of the second pass: |G2 - I| <= 1e-6
+      for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+        const int i = e / n, j = e - i * n;
+        if (!(fabs(G[i * gl + j] - (i == j ? 1.0 : 0.0)) <= 1e-6)) s_flag = 0;
       }
-      __syncwarp();
-      bool ok = chol_warp_reg(G, gl, n);
-      __syncwarp();
-      if (ok && pass == 0)
-        for (int j = threadIdx.x; j < n; j += 32)
-          if (!(G[j * gl + j] * G[j * gl + j] > 1e-14 * diag0[j])) ok = false;
-      ok = __all_sync(0xffffffffu, ok);
-      if (ok) trinv_warp(G, gl, n, Li, il);
-      if (threadIdx.x == 0) s_flag = ok ? flag : -1;
     }
+    bool ok = chol_cta(G, gl, n, w.sc3 + 4);
+    if (ok && pass == 0 && threadIdx.x < n)
+      if (!(G[threadIdx.x * gl + threadIdx.x] * G[threadIdx.x * gl + threadIdx.x] > 1e-14 * diag0[threadIdx.x]))
+        s_flag = -1;
+    __syncthreads();
+    if (!ok) s_flag = -1;
     __syncthreads();
     const int st = s_flag;
+    if (st >= 0) trinv_cta(G, gl, n, Li, il);
     if (st < 0) return pass == 0 ? 1 : 2;
     mma_mul_rt_inplace(A, ld, m, n, Li, il);
     if (pass == 0) {
@@ -655,37 +661,47 @@ __device__ bool blk_jacobi(double* X, int rows, int kc, double* V, int* sweeps, 
     __syncthreads();
     for (int round = 0; round < kp - 1; ++round) {
       const int* pt = ptab + 2 * round * npairs;
-      for (int pr = warp; pr < npairs; pr += nw) {
-        const int a = pt[2 * pr], b = pt[2 * pr + 1];
-        if (b >= kc) continue;
+      const int hw = tid >> 4, hl = tid & 15, nhw = blockDim.x >> 4;   // half-warp per pair
+      for (int pr0 = 0; pr0 < npairs; pr0 += nhw) {
+        const int pr = pr0 + hw;
+        const bool act = pr < npairs;
+        int a = 0, b = 0;
+        if (act) {
+          a = pt[2 * pr];
+          b = pt[2 * pr + 1];
+        }
+        const bool live = act && b < kc;
         double* xa = X + (int64_t)a * rows;
         double* xb = X + (int64_t)b * rows;
         double ga = 0.0;
-        for (int i = lane; i < rows; i += 32) ga = fma(xa[i], xb[i], ga);
+        if (live)
+          for (int i = hl; i < rows; i += 16) ga = fma(xa[i], xb[i], ga);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) ga += shx(ga, o);
-        const double al = nrm[a], be = nrm[b];
-        if (ga != 0.0 && ga * ga > tol2 * (al * be)) {
-          const double dlt = be - al;
-          const double sg = (dlt > 0.0 || (dlt == 0.0 && !signbit(dlt))) ? 1.0 : -1.0;
-          const double t = (2.0 * ga * sg) / (fabs(dlt) + sqrt(fma(dlt, dlt, 4.0 * ga * ga)));
-          const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
-          for (int i = lane; i < rows; i += 32) {
-            const double u = xa[i], v = xb[i];
-            xa[i] = c * u - sn * v;
-            xb[i] = sn * u + c * v;
-          }
-          double* va = V + (int64_t)a * kc;
-          double* vb = V + (int64_t)b * kc;
-          for (int i = lane; i < kc; i += 32) {
-            const double u = va[i], v = vb[i];
-            va[i] = c * u - sn * v;
-            vb[i] = sn * u + c * v;
-          }
-          if (lane == 0) {
-            nrm[a] = al - t * ga;
-            nrm[b] = be + t * ga;
-            s_rot = 1;
+        for (int o = 8; o > 0; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        if (live) {
+          const double al = nrm[a], be = nrm[b];
+          if (ga != 0.0 && ga * ga > tol2 * (al * be)) {
+            const double dlt = be - al;
+            const double sg = (dlt > 0.0 || (dlt == 0.0 && !signbit(dlt))) ? 1.0 : -1.0;
+            const double t = (2.0 * ga * sg) / (fabs(dlt) + sqrt(fma(dlt, dlt, 4.0 * ga * ga)));
+            const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
+            for (int i = hl; i < rows; i += 16) {
+              const double u = xa[i], v = xb[i];
+              xa[i] = c * u - sn * v;
+              xb[i] = sn * u + c * v;
+            }
+            double* va = V + (int64_t)a * kc;
+            double* vb = V + (int64_t)b * kc;
+            for (int i = hl; i < kc; i += 16) {
+              const double u = va[i], v = vb[i];
+              va[i] = c * u - sn * v;
+              vb[i] = sn * u + c * v;
+            }
+            if (hl == 0) {
+              nrm[a] = al - t * ga;
+              nrm[b] = be + t * ga;
+              s_rot = 1;
+            }
           }
         }
       }
@@ -1147,7 +1163,8 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
     // the same storage read column-major (R1 x kmin) is X = R^T
     double* V = w.S3;
     pc.start();
-    ok = jacobi_truncation(X, R1, kmin, rk, V, &sc->pad, w.red, w.perm) && ok;
+    ok = blk_jacobi(X, R1, kmin, V, &sc->pad, w.red, w.ptab) && ok;
+    col_norms_sorted(X, R1, kmin, w.red, w.perm);     // kept columns: perm[0..rk)
     pc.stop(sc, 3);
     pc.start();
     // C'_k = Q V[:, perm[:rk]]  (m x rk) on DMMA

@@ -31,8 +31,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_micro(int which, int m, int n
         w.S4[e] = (i == c ? 100.0 : 0.0) + 0.5 / (1 + i + c);
       }
       __syncthreads();
-      if (threadIdx.x < 32) chol_warp_reg(w.S4, n | 1, n);
-      __syncthreads();
+      chol_cta(w.S4, n | 1, n, w.sc3 + 4);
     } else if (which == 2) blk_solve_rows(A, ld, m, n, w.S4, n | 1, w.sc3 + 4);
     else if (which == 3) { if (n <= 16) qr_rows<16>(A, ld, m, n, w); else qr_rows<32>(A, ld, m, n, w); }
     else if (which == 4) { int k = m < n ? m : n; if (k <= 16) orgqr_rows<16>(A, ld, m, k, w); else orgqr_rows<32>(A, ld, m, k, w); }
@@ -41,7 +40,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_micro(int which, int m, int n
       double* X = w.S2;
       for (int e = threadIdx.x; e < n * n; e += blockDim.x) X[e] = (e % (n + 1) == 0 ? 2.0 + e * 0.001 : 0.1 / (1 + e % 7));
       __syncthreads();
-      jacobi_truncation(X, n, n, n / 2, w.S3, nullptr, w.red, w.perm);
+      blk_jacobi(X, n, n, w.S3, nullptr, w.red, w.ptab);
     } else if (which == 7) { __syncthreads(); }
   }
   long long t1 = clock64();
@@ -55,7 +54,7 @@ int main() {
   cudaMalloc(&d, 8);
   const int bytes = prgd::dense_smem_doubles() * 8;
   cudaFuncSetAttribute(prgd::k_micro, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  const char* names[] = {"gram_dmma", "chol_warp_reg", "trinv+mul_rt", "householder_qr", "orgqr", "cholqr2", "jacobi_trunc(n/2)", "syncthreads"};
+  const char* names[] = {"gram_dmma", "chol_cta", "trinv+mul_rt", "householder_qr", "orgqr", "cholqr2", "jacobi(n x n)", "syncthreads"};
   int shapes[][2] = {{512, 32}, {256, 32}, {256, 16}};
   for (auto& sh : shapes) {
     for (int wch = 0; wch < 8; ++wch) {
