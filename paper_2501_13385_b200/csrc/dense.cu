@@ -143,15 +143,12 @@ __device__ bool chol_cta(double* G, int gl, int n, double* rinv) {
     const double rj2 = rj * rj;
     if (threadIdx.x == 0) rinv[j] = rj;
     const int nr = n - 1 - j;                       // rows/cols j+1..n-1
-    const int ntri = nr * (nr + 1) / 2;
-    for (int t = threadIdx.x; t < ntri; t += blockDim.x) {
-      // t -> (i, k) with j < k <= i: row-major over the lower triangle
-      int i = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-      while ((i + 1) * (i + 2) / 2 <= t) ++i;
-      while (i * (i + 1) / 2 > t) --i;
-      const int k = t - i * (i + 1) / 2;
-      const int gi = j + 1 + i, gk = j + 1 + k;
-      G[gi * gl + gk] = fma(-G[gi * gl + j] * rj2, G[gk * gl + j], G[gi * gl + gk]);
+    for (int t = threadIdx.x; t < nr * nr; t += blockDim.x) {
+      const int i = t / nr, k = t - i * nr;         // (i, k) over the square, k <= i kept
+      if (k <= i) {
+        const int gi = j + 1 + i, gk = j + 1 + k;
+        G[gi * gl + gk] = fma(-G[gi * gl + j] * rj2, G[gk * gl + j], G[gi * gl + gk]);
+      }
     }
     __syncthreads();
   }
@@ -498,6 +495,39 @@ __device__ int blk_cholqr2(double* A, int ld, int m, int n, double* R, const Wor
     for (int e = threadIdx.x; e < n; e += blockDim.x) diag0[e] = G[e * gl + e];
     __syncthreads();
     if (pass == 1) {
+      // G2 = Q1^T Q1 = I + E.  For |E| <= 1e-8 its Cholesky factor is L = I + L1 + O(E^2)
+      // with L1 = tril(E, -1) + diag(E)/2, and L^{-1} = I - L1 + O(E^2): exact to rounding.
+      __shared__ int s_small;
+      if (threadIdx.x == 0) s_small = 1;
+      __syncthreads();
+      for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+        const int i = e / n, j = e - i * n;
+        if (!(fabs(G[i * gl + j] - (i == j ? 1.0 : 0.0)) <= 1e-8)) s_small = 0;
+      }
+      __syncthreads();
+      if (s_small) {
+        for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+          const int i = e / n, j = e - i * n;
+          double l1 = 0.0;
+          if (j < i) l1 = G[i * gl + j];
+          else if (j == i) l1 = 0.5 * (G[i * gl + i] - 1.0);
+          Li[i * il + j] = (i == j ? 1.0 : 0.0) - l1;        // L^{-1}
+          w.S3[e] = (i == j ? 1.0 : 0.0) + l1;               // L (row-major, n x n)
+        }
+        __syncthreads();
+        mma_mul_rt_inplace(A, ld, m, n, Li, il);             // Q = Q1 L^{-T}
+        double* T = w.S4;                                    // R <- L^T R
+        for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+          const int i = e / n, j = e - i * n;
+          double acc = 0.0;
+          for (int q = i; q <= j; ++q) acc = fma(w.S3[q * n + i], R[q * n + j], acc);
+          T[e] = j >= i ? acc : 0.0;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < n * n; e += blockDim.x) R[e] = T[e];
+        __syncthreads();
+        return 0;
+      }
       // certification of the second pass: |G2 - I| <= 1e-6
       for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
         const int i = e / n, j = e - i * n;
@@ -836,7 +866,10 @@ __device__ void blk_mode3t(double* out, const double* in, int rows, int rb, cons
   }
 }
 
-__device__ __forceinline__ int odd_ld(int n) { return n | 1; }
+// Row stride of staged matrices: >= n and = 4 (mod 16).  DMMA fragment loads read 4 rows
+// x 8 consecutive columns per half-warp; (4 tq + gid) mod 16 is then distinct for all 16
+// lanes of a half-warp, i.e. bank-conflict free.
+__device__ __forceinline__ int odd_ld(int n) { return n <= 4 ? 4 : ((n + 11) / 16) * 16 + 4; }
 
 // Phase timer (thread 0): cyc[ph] += clock64() - t0.  Diagnostic only.
 struct PhaseClock {
@@ -989,7 +1022,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_project(DenseArgs a) {
     double* Ls = smraw;                       // r1 x r1
     double* W = Ls + r1 * r1;                 // r1 x r1
     double* Z = W + r1 * r1;                  // m x ld (staged) or Ah
-    const int ld = odd_ld(r1);
+    const int ld = r1 | 1;                    // odd: row-per-thread substitutions below
     const bool stage = (int64_t)m * ld * 2 + 2 * r1 * r1 <= a.smem_doubles;
     double* Us = stage ? Z + (int64_t)m * ld : nullptr;
     const int zld = stage ? ld : r1;
