@@ -181,6 +181,12 @@ def run_ours(args, rank, ws, dist):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
 
+    # dense-sweep diagnostics over one extra step: Jacobi sweeps, QR paths
+    e0 = ctx.debug("eps")
+    ctx.step(args.step_size)
+    e1 = ctx.debug("eps")
+    dd = e1 - e0
+    dense_diag = {"jacobi_sweeps": int(dd[4]), "cholqr2_ok": int(dd[11]), "cholqr2_fail_first": int(dd[12])}
     # per-kernel-group durations (CUDA events on the library stream), profile mode
     ctx.set_profiling(True)
     for _ in range(args.profile_steps):
@@ -190,7 +196,8 @@ def run_ours(args, rank, ws, dist):
     ctx.close()
 
     out = dict(pr=pr, y=y, init=init, KL=KL, NL=NL, NR=NR, ms=ms_max, launches=launches,
-               clocks=clocks, prof=prof, t_gen=t_gen, t_setobs=t_setobs, res0=res0, res1=res1)
+               clocks=clocks, prof=prof, t_gen=t_gen, t_setobs=t_setobs, res0=res0, res1=res1,
+               dense_diag=dense_diag)
     if not args.no_e2e:
         out["e2e"] = run_e2e(args, pr, y, init)
     return out
@@ -333,6 +340,7 @@ def main():
         "clocks": r["clocks"],
         "setup_s": {"generate": round(r["t_gen"], 2), "set_observations": round(r["t_setobs"], 3)},
         "residual": {"before": r["res0"], "after": r["res1"]},
+        "dense_diag": r["dense_diag"],
     }
     print(json.dumps(line), flush=True)
 
