@@ -183,7 +183,8 @@ enum {
   TT_DBG_RESID = 5,      /* double[m]  g_s in ORIGINAL sample order          (A2) */
   TT_DBG_H = 6,          /* double[n_k] h_{k,j} of the last pass A           (A3) */
   TT_DBG_PHI = 7,        /* double[n_k] phi_{k,j} of the last step           (A3) */
-  TT_DBG_EPS = 8,        /* double[13] eps, sum g^2, alpha, p, Jacobi sweeps, 8 phase cycle counters */
+  TT_DBG_EPS = 8,        /* double[13] or [29] (cap >= 29): eps, sum g^2, alpha, p, Jacobi sweeps,
+                            then 8 (24) cumulative dense-phase cycle counters / counts */
   TT_DBG_U = 9,          /* double[core k] U_k of the last step              (A5) */
   TT_DBG_P = 10,         /* double[r_k+1 ^2] P_{k+1} (right Gram) of last step (A6) */
   TT_DBG_Y = 11,         /* double[core k] Y_k of the last step              (A9) */

@@ -261,7 +261,7 @@ class TTContext:
         if code in (6, 7):
             return self.n[k]
         if code == 8:
-            return 13
+            return 29
         if code in (9, 11, 12):
             return self.r[k] * self.n[k] * self.r[k + 1]
         if code == 10:

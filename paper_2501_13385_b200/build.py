@@ -16,6 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libprgd.so")
 SOURCES = ["api.cu", "sort.cu", "tables.cu", "passes.cu", "dense.cu"]
+INCLUDES = ["round_cluster.inc"]
 HEADERS = ["prgd_internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
@@ -32,7 +33,7 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS + INCLUDES]
     deps.append(os.path.join(ROOT, "include", "prgd.h"))
     deps.append(os.path.abspath(__file__))
     return any(os.path.getmtime(p) > t for p in deps)
@@ -41,17 +42,37 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp"]
-    cmd += [os.path.join(CSRC, f) for f in SOURCES]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in FLAGS if f != "-shared"]
+    inc = ["-I", os.path.join(ROOT, "include")]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = [NVCC, *cflags, *inc, "-c", os.path.join(CSRC, src), "-o", obj]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, cmd, res
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
     log = os.path.join(HERE, "build.log")
+    failed = False
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
+        for src, obj, cmd, res in results:
+            f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+            failed |= res.returncode != 0
+        if not failed:
+            cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "--cudart", "static",
+                   "-shared", "-o", LIB + ".tmp"] + [r[1] for r in results]
+            res = subprocess.run(cmd, capture_output=True, text=True)
+            f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+            failed = res.returncode != 0
+    if failed:
+        sys.stderr.write(open(log).read()[-20000:])
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write(open(log).read())
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

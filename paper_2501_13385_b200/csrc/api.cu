@@ -119,7 +119,8 @@ struct tt_ctx {
   bool base_ready = false;
   int* n_dev = nullptr;
   double *C = nullptr, *U = nullptr, *Y = nullptr, *Ahat = nullptr, *phi = nullptr, *h = nullptr;
-  double *P = nullptr, *L = nullptr, *B = nullptr, *work = nullptr;
+  double *P = nullptr, *L = nullptr, *B = nullptr, *work = nullptr, *clw = nullptr;
+  int64_t clw_len = 0;
   int64_t work_len = 0;
   std::vector<int64_t> core_off, phi_off, b_off, p_off;
   Scalars* sc = nullptr;
@@ -228,12 +229,21 @@ int ensure_base(tt_ctx* ctx) {
     maxgram = std::max(maxgram, ctx->r[k] * ctx->n[k] * ctx->r[k + 1]);
   }
   ctx->work_len = 2 * std::max(maxb, maxcore) + maxgram + 4096;
+  {
+    int64_t S = 2, nmax = 1;
+    for (int k = 0; k <= d; ++k) S = std::max<int64_t>(S, 2 * ctx->r[k]);
+    for (int k = 0; k < d; ++k) nmax = std::max<int64_t>(nmax, ctx->n[k]);
+    const int64_t nc = round_cluster_size();
+    const int64_t lds = S <= 4 ? 4 : ((S + 11) / 16) * 16 + 4;
+    ctx->clw_len = 8192 + nc * 2 * ((nmax + nc - 1) / nc) * S * lds;
+  }
   bool ok = A(ctx, &ctx->n_dev, d, L) && A(ctx, &ctx->C, ctx->core_off[d], L) &&
             A(ctx, &ctx->U, ctx->core_off[d], L) && A(ctx, &ctx->Y, ctx->core_off[d], L) &&
             A(ctx, &ctx->Ahat, ctx->core_off[d], L) && A(ctx, &ctx->phi, ctx->phi_off[d], L) &&
             A(ctx, &ctx->h, ctx->phi_off[d], L) && A(ctx, &ctx->P, ctx->p_off[d], L) &&
             A(ctx, &ctx->L, ctx->p_off[d], L) && A(ctx, &ctx->B, ctx->b_off[d], L) &&
-            A(ctx, &ctx->work, ctx->work_len, L) && A(ctx, &ctx->sc, 1, L);
+            A(ctx, &ctx->work, ctx->work_len, L) && A(ctx, &ctx->clw, ctx->clw_len, L) &&
+            A(ctx, &ctx->sc, 1, L);
   if (!ok) return fail(ctx, TT_ERR_OOM, "device allocation failed (base buffers)");
   // tables
   ctx->LT.assign(KL + 1, nullptr);
@@ -298,6 +308,8 @@ DenseArgs dense_args(tt_ctx* ctx) {
   a.B = ctx->B;
   a.work = ctx->work;
   a.work_len = ctx->work_len;
+  a.clw = ctx->clw;
+  a.clw_len = ctx->clw_len;
   a.sc = ctx->sc;
   a.smem_doubles = dense_smem_doubles();
   return a;
@@ -991,8 +1003,9 @@ int tt_debug_get(tt_ctx* ctx, int what, int k, void* h_out, int64_t cap, int64_t
       o[2] = ctx->sc_host->alpha;
       o[3] = ctx->sc_host->p;
       o[4] = (double)ctx->sc_host->pad;   // cumulative Jacobi sweeps (diagnostic)
-      for (int i = 0; i < 8; ++i) o[5 + i] = (double)ctx->sc_host->cyc[i];
-      *count = 13;
+      const int nc = cap >= 29 ? 24 : 8;
+      for (int i = 0; i < nc; ++i) o[5 + i] = (double)ctx->sc_host->cyc[i];
+      *count = 5 + nc;
       return TT_OK;
     }
     case TT_DBG_RESID: {

@@ -18,7 +18,11 @@
 // (31 shuffles for 32 columns) and across warps through shared memory.  Matrices are
 // staged in shared memory (odd row stride: conflict-free column access) when they
 // fit, else processed in a global scratch area by the same code.
+#include <cooperative_groups.h>
+
 #include "prgd_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace prgd {
 namespace {
@@ -472,7 +476,7 @@ __device__ int blk_cholqr2_smem(double* A, int ld, int m, int n, double* R, cons
 }
 
 // max_{i,j} |G[i][j] - delta_ij| over the n x n block (stride gl); CTA-uniform result.
-__device__ double blk_max_dev_identity(const double* G, int gl, int n, double* red) {
+__device__ __noinline__ double blk_max_dev_identity(const double* G, int gl, int n, double* red) {
   double mx = 0.0;
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     const int i = e / n, j = e - i * n;
@@ -583,7 +587,7 @@ __device__ int blk_cholqr2(double* A, int ld, int m, int n, double* R, const Wor
 // Tall blocks (m >= n) try CholeskyQR2 first (O(1) barriers); ill-conditioned or wide
 // blocks use Householder (LAPACK conventions), continuing from CholeskyQR2's partial
 // result when it failed late (A = Q1, R = R1  =>  A_orig = Q (R_h R1)).
-__device__ void householder_explicit(double* A, int ld, int m, int n, double* Rout, const Work& w) {
+__device__ __noinline__ void householder_explicit(double* A, int ld, int m, int n, double* Rout, const Work& w) {
   const int kmin = m < n ? m : n;
   if (n <= 8) qr_rows<8>(A, ld, m, n, w);
   else if (n <= 16) qr_rows<16>(A, ld, m, n, w);
@@ -663,7 +667,7 @@ __device__ bool blk_chol(double* P, int R) {
 // accumulating V (kc x kc, column-major).  Round-robin ordering from a precomputed
 // pair table, one warp per pair; column norms are kept in shared memory and updated
 // by the exact rotation identities (a' = a - t g, b' = b + t g), recomputed per sweep.
-__device__ bool blk_jacobi(double* X, int rows, int kc, double* V, int* sweeps, double* nrm,
+__device__ __noinline__ bool blk_jacobi(double* X, int rows, int kc, double* V, int* sweeps, double* nrm,
                            int* ptab) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   __shared__ int s_rot;
@@ -766,7 +770,7 @@ __device__ bool blk_jacobi(double* X, int rows, int kc, double* V, int* sweeps, 
 
 // Norms of the kc columns of X (rows x kc col-major) into nrm, and the permutation
 // perm sorting them by norm (descending, ties by index).  Ends with a barrier.
-__device__ void col_norms_sorted(const double* X, int rows, int kc, double* nrm, int* perm) {
+__device__ __noinline__ void col_norms_sorted(const double* X, int rows, int kc, double* nrm, int* perm) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int c = warp; c < kc; c += nw) {
     double s = 0.0;
@@ -1262,6 +1266,8 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
   }
 }
 
+#include "round_cluster.inc"
+
 }  // namespace
 
 int dense_smem_doubles() { return (200 * 1024) / 8; }
@@ -1271,6 +1277,15 @@ void dense_init() {
   cudaFuncSetAttribute(k_dense_orth, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_dense_round, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaFuncSetAttribute(k_round_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+int round_cluster_size() { return kNC; }
+
+bool round_cluster_ok(int d, const int* r) {
+  int S = 2;
+  for (int k = 0; k <= d; ++k) S = 2 * r[k] > S ? 2 * r[k] : S;
+  return S <= 32;
 }
 
 void launch_dense_orth(cudaStream_t s, const DenseArgs& a, int64_t* launches) {
@@ -1282,7 +1297,8 @@ void launch_dense_orth(cudaStream_t s, const DenseArgs& a, int64_t* launches) {
 void launch_dense_round(cudaStream_t s, const DenseArgs& a, int64_t* launches) {
   const size_t bytes = (size_t)a.smem_doubles * sizeof(double);
   k_project<<<a.d, kDenseThreads, bytes, s>>>(a);
-  k_dense_round<<<1, kDenseThreads, bytes, s>>>(a);
+  if (a.clw && round_cluster_ok(a.d, a.r)) k_round_cl<<<kNC, kDenseThreads, bytes, s>>>(a);
+  else k_dense_round<<<1, kDenseThreads, bytes, s>>>(a);
   *launches += 2;
 }
 

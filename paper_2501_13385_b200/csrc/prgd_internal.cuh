@@ -32,7 +32,7 @@ struct Scalars {
   int err;           // nonzero: numeric fault (sticky until read by the host)
   int index_err;     // set by index validation kernels
   int pad;          // cumulative one-sided Jacobi sweeps (diagnostic)
-  long long cyc[8]; // cumulative SM cycles per dense phase (diagnostic)
+  long long cyc[24]; // cumulative SM cycles / counters per dense phase (diagnostic)
 };
 
 enum ErrBits { kErrNaN = 1, kErrChol = 2, kErrSVD = 4 };
@@ -73,6 +73,8 @@ struct DenseArgs {
   double* B;       // rank-2r cores (rounding workspace)
   double* work;    // global scratch (>= 2 * max B core + extras)
   int64_t work_len;
+  double* clw;     // cluster-rounding scratch: [0, 8192) fallback R, then per-CTA slice buffers
+  int64_t clw_len;
   Scalars* sc;
   int smem_doubles;  // dynamic shared memory available to the kernel, in doubles
 };
@@ -157,6 +159,8 @@ void launch_gather_sq_sum(cudaStream_t s, const double* h0, int n0, Scalars* sc,
 void launch_dense_orth(cudaStream_t s, const DenseArgs& a, int64_t* launches);
 void launch_dense_round(cudaStream_t s, const DenseArgs& a, int64_t* launches);
 int dense_smem_doubles();
+int round_cluster_size();
+bool round_cluster_ok(int d, const int* r);   // cluster rounding applies (2 max r <= 32)
 void dense_init();   // sets the dynamic shared-memory attribute (call once, outside capture)
 
 inline int pad_rank(int r) {

@@ -1,20 +1,39 @@
-"""Diagnostic: Jacobi sweeps and per-phase cycles of the dense sweeps at config 5."""
-import sys, os
+"""Diagnostic: Jacobi sweeps and per-phase cycles of the dense sweeps (cluster rounding).
+
+    python tools/dense_phases.py [cfg] [m] [steps]
+"""
+import os
+import sys
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np
-import synth, paper_2501_13385_b200 as pkg
+import numpy as np  # noqa: E402
+
+import paper_2501_13385_b200 as pkg  # noqa: E402
+import synth  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
-pr = synth.make_problem(cfg, m=200000)
-t = pkg.TTContext(pr.n, pr.r); t.set_cores(pr.truth); clean = t.eval_at(pr.idx); t.close()
+m = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2] else None
+steps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
+pr = synth.make_problem(cfg, m=m)
+t = pkg.TTContext(pr.n, pr.r)
+t.set_cores(pr.truth)
+clean = t.eval_at(pr.idx)
+t.close()
 y = pr.observations(clean)
-ctx = pkg.TTContext(pr.n, pr.r); ctx.set_observations(pr.idx, y); ctx.set_cores(pr.init)
-names = ["r2l_qr", "r2l_prod", "l2r_qr", "jacobi", "l2r_prod+orth_gram", "orth_qr", "n_cholqr_ok", "n_fallback_early"]
-prev = np.zeros(13)
-for i in range(5):
+ctx = pkg.TTContext(pr.n, pr.r)
+ctx.set_observations(pr.idx, y)
+ctx.set_cores(pr.init)
+NAMES = {0: "r2l_qr", 1: "r2l_push", 2: "l2r_qr", 3: "trunc", 4: "l2r_prod", 5: "orth_qr",
+         8: "gram", 9: "reduce", 10: "chol", 11: "apply", 12: "racc", 15: "certify", 16: "fullJacobi"}
+COUNTS = {17: "cert_fail", 18: "qr_fallbacks", 14: "cross_sweeps", 19: "full_sweeps", 6: "orth_cholqr_ok"}
+prev = np.zeros(29)
+for i in range(steps):
+    show = i >= steps - 3
     ctx.step(1.0)
     e = ctx.debug("eps")
-    dl = e - prev; prev = e.copy()
-    print(f"step {i} res {ctx.residual_norm():.4e} sweeps {dl[4]:.0f} " +
-          " ".join(f"{n}={dl[5 + j] / 1.9e3:.0f}us" for j, n in enumerate(names[:5])) +
-          f" fallback_late={dl[10]:.0f} cholqr_ok={dl[11]:.0f} fallback_early={dl[12]:.0f}")
+    dl = e - prev
+    prev = e.copy()
+    cyc = dl[5:]
+    if show: print(f"step {i} res {ctx.residual_norm():.4e} jacobi_sweeps {dl[4]:.0f} " +
+          " ".join(f"{n}={cyc[j] / 1.965e3:.0f}us" for j, n in NAMES.items()) + " " +
+          " ".join(f"{n}={cyc[j]:.0f}" for j, n in COUNTS.items()))
