@@ -269,6 +269,7 @@ int ensure_base(tt_ctx* ctx) {
     const int r0 = (int)ctx->r[k], nk = (int)ctx->n[k], r1 = (int)ctx->r[k + 1];
     ycap = std::max(ycap, Y_partial_need(ng, r0, nk, r1));
     ycap = std::max(ycap, back_partial_need(ng, r0, nk, r1));
+    ycap = std::max(ycap, level_back_partial_need(ng, r0, nk, r1, ctx->ldr[k < KL ? k + 1 : k]));
   }
   ctx->Ypart_cap = ycap;
   if (!A(ctx, &ctx->Ypart, ycap, L)) return fail(ctx, TT_ERR_OOM, "device allocation failed (Y)");
@@ -281,6 +282,7 @@ int ensure_base(tt_ctx* ctx) {
   CK(cudaMemsetAsync(ctx->h, 0, ctx->phi_off[d] * sizeof(double), ctx->stream));
   dense_init();
   tables_init();
+  levels_init();
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->base_ready = true;
   return TT_OK;
@@ -327,23 +329,33 @@ void enqueue_tables(tt_ctx* ctx, bool useU, int64_t* lc) {
   cudaStream_t s = ctx->stream;
   const double* cores = useU ? ctx->U : ctx->C;
   const Scalars* sc = useU ? ctx->sc : nullptr;
-  // left levels 1..KL
+  std::vector<TableLevel> L, R;
+  bool ok = true;
+  // left levels 1..KL (A_{k+1} from A_k and core k), right levels d-1..KL
   for (int k = 0; k < KL; ++k) {
-    const double* in = k == 0 ? nullptr : ctx->LT[k];
-    const int ldin = ctx->ldr[k];
-    const double* rs = (useU && k + 1 == KL) ? ctx->psiL : nullptr;
-    launch_table_left(s, in, ldin, cores + ctx->core_off[k], (int)ctx->r[k], (int)ctx->n[k],
-                      (int)ctx->r[k + 1], ctx->LT[k + 1], ctx->ldr[k + 1], ctx->NLk[k + 1], rs,
-                      sc, lc);
+    TableLevel t{true, k == 0 ? nullptr : ctx->LT[k], ctx->ldr[k], cores + ctx->core_off[k],
+                 (int)ctx->r[k], (int)ctx->n[k], (int)ctx->r[k + 1], ctx->LT[k + 1], ctx->ldr[k + 1],
+                 ctx->NLk[k + 1], (useU && k + 1 == KL) ? ctx->psiL : nullptr};
+    ok = ok && level_tab_ok(t.r0, t.nk, t.r1, t.ld_out);
+    L.push_back(t);
   }
-  // right levels d-1..KL
   for (int k = d - 1; k >= KL; --k) {
-    const double* in = k == d - 1 ? nullptr : ctx->RT[k + 1];
-    const int ldin = ctx->ldr[k + 1];
-    const double* rs = (useU && k == KL) ? ctx->psiR : nullptr;
-    launch_table_right(s, in, ldin, cores + ctx->core_off[k], (int)ctx->r[k], (int)ctx->n[k],
-                       (int)ctx->r[k + 1], ctx->RT[k], ctx->ldr[k], ctx->NRk[k], rs, sc, lc);
+    TableLevel t{false, k == d - 1 ? nullptr : ctx->RT[k + 1], ctx->ldr[k + 1],
+                 cores + ctx->core_off[k], (int)ctx->r[k], (int)ctx->n[k], (int)ctx->r[k + 1],
+                 ctx->RT[k], ctx->ldr[k], ctx->NRk[k], (useU && k == KL) ? ctx->psiR : nullptr};
+    ok = ok && level_tab_ok(t.r0, t.nk, t.r1, t.ld_out);
+    R.push_back(t);
   }
+  if (ok) {
+    launch_table_levels(s, L, R, sc, lc);
+    return;
+  }
+  for (const TableLevel& t : L)
+    launch_table_left(s, t.in, t.ld_in, t.core, t.r0, t.nk, t.r1, t.out, t.ld_out, t.rows_out,
+                      t.rowscale, sc, lc);
+  for (const TableLevel& t : R)
+    launch_table_right(s, t.in, t.ld_in, t.core, t.r0, t.nk, t.r1, t.out, t.ld_out, t.rows_out,
+                       t.rowscale, sc, lc);
 }
 
 void enqueue_evaluate(tt_ctx* ctx, int64_t* lc) {
@@ -427,38 +439,51 @@ void enqueue_update(tt_ctx* ctx, int64_t* lc) {
   launch_seg(s, b, ctx->sc, lc);
   grp(ctx, 8, false);
   grp(ctx, 9, true);
-  for (int k = KL - 1; k >= 0; --k) {
-    const double* Atab = k >= 1 ? ctx->LT[k] : nullptr;
-    const int r0 = (int)ctx->r[k], nk = (int)ctx->n[k], r1 = (int)ctx->r[k + 1];
-    if (back_fused_ok(r0, nk, r1)) {
-      launch_back_level(s, true, ctx->EL[k + 1], ctx->ldr[k + 1], Atab, ctx->ldr[k],
-                        ctx->U + ctx->core_off[k], r0, nk, r1, k >= 1 ? ctx->EL[k] : nullptr,
-                        ctx->ldr[k], ctx->NLk[k], ctx->Y + ctx->core_off[k], ctx->Ypart,
-                        ctx->Ypart_cap, ctx->sc, lc);
-      continue;
+  {
+    std::vector<BackwardLevel> BL, BR;
+    bool ok = true;
+    for (int k = KL - 1; k >= 0; --k) {
+      BackwardLevel t{true, ctx->EL[k + 1], ctx->ldr[k + 1], k >= 1 ? ctx->LT[k] : nullptr,
+                      ctx->ldr[k], ctx->U + ctx->core_off[k], (int)ctx->r[k], (int)ctx->n[k],
+                      (int)ctx->r[k + 1], k >= 1 ? ctx->EL[k] : nullptr, ctx->ldr[k], ctx->NLk[k],
+                      ctx->Y + ctx->core_off[k]};
+      ok = ok && level_back_ok(t.r0, t.nk, t.r1, t.wrow);
+      BL.push_back(t);
     }
-    launch_Y(s, true, Atab, ctx->ldr[k], ctx->EL[k + 1], ctx->ldr[k + 1], ctx->NLk[k], r0, nk, r1,
-             ctx->Y + ctx->core_off[k], ctx->Ypart, ctx->Ypart_cap, ctx->sc, lc);
-    if (k >= 1)
-      launch_E_down(s, ctx->EL[k + 1], ctx->ldr[k + 1], ctx->U + ctx->core_off[k], r0, nk, r1,
-                    ctx->EL[k], ctx->ldr[k], ctx->NLk[k], ctx->sc, lc);
-  }
-  for (int k = KL; k < d; ++k) {
-    const double* Btab = k + 1 < d ? ctx->RT[k + 1] : nullptr;
-    const int64_t nsum = k + 1 < d ? ctx->NRk[k + 1] : 1;
-    const int r0 = (int)ctx->r[k], nk = (int)ctx->n[k], r1 = (int)ctx->r[k + 1];
-    if (back_fused_ok(r0, nk, r1)) {
-      launch_back_level(s, false, ctx->FR[k], ctx->ldr[k], Btab, ctx->ldr[k + 1],
-                        ctx->U + ctx->core_off[k], r0, nk, r1, k + 1 < d ? ctx->FR[k + 1] : nullptr,
-                        ctx->ldr[k + 1], nsum, ctx->Y + ctx->core_off[k], ctx->Ypart,
-                        ctx->Ypart_cap, ctx->sc, lc);
-      continue;
+    for (int k = KL; k < d; ++k) {
+      BackwardLevel t{false, ctx->FR[k], ctx->ldr[k], k + 1 < d ? ctx->RT[k + 1] : nullptr,
+                      ctx->ldr[k + 1], ctx->U + ctx->core_off[k], (int)ctx->r[k], (int)ctx->n[k],
+                      (int)ctx->r[k + 1], k + 1 < d ? ctx->FR[k + 1] : nullptr, ctx->ldr[k + 1],
+                      k + 1 < d ? ctx->NRk[k + 1] : 1, ctx->Y + ctx->core_off[k]};
+      ok = ok && level_back_ok(t.r0, t.nk, t.r1, t.wrow);
+      BR.push_back(t);
     }
-    launch_Y(s, false, Btab, ctx->ldr[k + 1], ctx->FR[k], ctx->ldr[k], nsum, r0, nk, r1,
-             ctx->Y + ctx->core_off[k], ctx->Ypart, ctx->Ypart_cap, ctx->sc, lc);
-    if (k + 1 < d)
-      launch_F_up(s, ctx->FR[k], ctx->ldr[k], ctx->U + ctx->core_off[k], r0, nk, r1,
-                  ctx->FR[k + 1], ctx->ldr[k + 1], ctx->NRk[k + 1], ctx->sc, lc);
+    if (ok) {
+      launch_backward_levels(s, BL, BR, ctx->Ypart, ctx->Ypart_cap, ctx->sc, lc);
+    } else {
+      for (const BackwardLevel& t : BL) {
+        if (back_fused_ok(t.r0, t.nk, t.r1)) {
+          launch_back_level(s, true, t.X, t.wrow, t.V, t.ldV, t.core, t.r0, t.nk, t.r1, t.O, t.ldO,
+                            t.ngroups, t.Y, ctx->Ypart, ctx->Ypart_cap, ctx->sc, lc);
+          continue;
+        }
+        launch_Y(s, true, t.V, t.ldV, t.X, t.wrow, t.ngroups, t.r0, t.nk, t.r1, t.Y, ctx->Ypart,
+                 ctx->Ypart_cap, ctx->sc, lc);
+        if (t.O)
+          launch_E_down(s, t.X, t.wrow, t.core, t.r0, t.nk, t.r1, t.O, t.ldO, t.ngroups, ctx->sc, lc);
+      }
+      for (const BackwardLevel& t : BR) {
+        if (back_fused_ok(t.r0, t.nk, t.r1)) {
+          launch_back_level(s, false, t.X, t.wrow, t.V, t.ldV, t.core, t.r0, t.nk, t.r1, t.O,
+                            t.ldO, t.ngroups, t.Y, ctx->Ypart, ctx->Ypart_cap, ctx->sc, lc);
+          continue;
+        }
+        launch_Y(s, false, t.V, t.ldV, t.X, t.wrow, t.ngroups, t.r0, t.nk, t.r1, t.Y, ctx->Ypart,
+                 ctx->Ypart_cap, ctx->sc, lc);
+        if (t.O)
+          launch_F_up(s, t.X, t.wrow, t.core, t.r0, t.nk, t.r1, t.O, t.ldO, t.ngroups, ctx->sc, lc);
+      }
+    }
   }
   grp(ctx, 9, false);
   grp(ctx, 10, true);

@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 namespace prgd {
 
 constexpr int kMaxD = 64;
@@ -123,6 +125,54 @@ void launch_back_level(cudaStream_t s, bool left, const double* X, int ldX, cons
                        int ldV, const double* core, int r0, int nk, int r1, double* O, int ldO,
                        int64_t ngroups, double* Y, double* partial, int64_t partial_cap,
                        const Scalars* sc, int64_t* launches);  // shared-memory attributes (call once, outside capture)
+
+// DMMA table / backward kernels (tables.cu), used when tab_mma_ok / back_mma_ok hold.
+bool tab_mma_ok(int r0, int nk, int r1, int ld_out);
+void launch_tab_mma(cudaStream_t s, bool left, const double* in, int ld_in, const double* core,
+                    int r0, int nk, int r1, double* out, int ld_out, int64_t rows_out,
+                    const double* rowscale, const Scalars* sc, int64_t* launches);
+bool back_mma_ok(int r0, int nk, int r1, int wrow);
+int64_t back_mma_partial_need(int64_t ngroups, int r0, int nk, int r1, int wrow);
+void launch_back_mma(cudaStream_t s, bool left, const double* X, int wrow, const double* V, int ldV,
+                     const double* core, int r0, int nk, int r1, double* O, int ldO,
+                     int64_t ngroups, double* Y, double* partial, int64_t partial_cap,
+                     const Scalars* sc, int64_t* launches);
+void tables_mma_init();
+
+// levels.cu: table levels / backward recursions on DMMA with few launches.
+struct TableLevel {        // out (flat [rows_out / nk][nk * ld_out]) from in x core
+  bool left;
+  const double* in;        // null: the one parent row [1]
+  int ld_in;
+  const double* core;
+  int r0, nk, r1;
+  double* out;
+  int ld_out;
+  int64_t rows_out;
+  const double* rowscale;
+};
+struct BackwardLevel {     // O (next E / F level) and Y_k from X (E_{k+1} / F_k) and V (A_k / B_{k+1})
+  bool left;
+  const double* X;
+  int wrow;                // row stride of X's table level (flat row = nk * wrow)
+  const double* V;         // null: ones
+  int ldV;
+  const double* core;
+  int r0, nk, r1;
+  double* O;               // null: none
+  int ldO;
+  int64_t ngroups;
+  double* Y;
+};
+bool level_tab_ok(int r0, int nk, int r1, int ld_out);
+bool level_back_ok(int r0, int nk, int r1, int wrow);
+int64_t level_back_partial_need(int64_t ngroups, int r0, int nk, int r1, int wrow);
+void launch_table_levels(cudaStream_t s, const std::vector<TableLevel>& left,
+                         const std::vector<TableLevel>& right, const Scalars* sc, int64_t* lc);
+void launch_backward_levels(cudaStream_t s, const std::vector<BackwardLevel>& left,
+                            const std::vector<BackwardLevel>& right, double* part, int64_t part_cap,
+                            const Scalars* sc, int64_t* lc);
+void levels_init();
 
 // passes.cu
 enum SegMode { kSDDMM = 0, kGSQ = 1, kSPMM = 2 };
