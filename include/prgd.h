@@ -153,6 +153,15 @@ PRGD_API const char* tt_last_error(const tt_ctx* ctx);
  * Any output pointer may be NULL. */
 PRGD_API int tt_plan(int d, const int64_t* n, const int64_t* r, int* K_L, int64_t* N_L, int64_t* N_R);
 
+/* Host-only: the gather blocks of the two bucketing orders (A0).  The prefix order
+ * groups samples by the virtual row VP = floor(S nb_L / N_R) N_L + P, the suffix order
+ * by VS = floor(P nb_R / N_L) N_R + S, so that each pass over Omega gathers the other
+ * side's table rows one L2-resident block at a time; TT_DBG_OFFS_L / _R then have
+ * nb_L N_L + 1 / nb_R N_R + 1 entries.  Default nb = 1 (blocking measured slower on B200,
+ * DESIGN.md); the environment variable PRGD_GATHER_BLOCKS (a power of two) overrides.
+ * Validation and errors as tt_plan. */
+PRGD_API int tt_plan_blocks(int d, const int64_t* n, const int64_t* r, int* nb_L, int* nb_R);
+
 /* Counters: launches = kernels this context launched since creation (graph nodes
  * counted per replay); steps = tt_prgd_step calls. */
 typedef struct tt_stats {
@@ -177,9 +186,9 @@ PRGD_API const char* tt_profile_name(int group);
  * Returns the element count in *count.  Synchronises. */
 enum {
   TT_DBG_PERM_PRE = 1,   /* int32[m]   sample ids in prefix order            (A0) */
-  TT_DBG_OFFS_L = 2,     /* int64[N_L+1] prefix bucket offsets               (A0) */
+  TT_DBG_OFFS_L = 2,     /* int64[nb_L N_L+1] prefix virtual-row offsets     (A0) */
   TT_DBG_PERM_SUF = 3,   /* int32[m]   sample ids in suffix order            (A0) */
-  TT_DBG_OFFS_R = 4,     /* int64[N_R+1] suffix bucket offsets               (A0) */
+  TT_DBG_OFFS_R = 4,     /* int64[nb_R N_R+1] suffix virtual-row offsets     (A0) */
   TT_DBG_RESID = 5,      /* double[m]  g_s in ORIGINAL sample order          (A2) */
   TT_DBG_H = 6,          /* double[n_k] h_{k,j} of the last pass A           (A3) */
   TT_DBG_PHI = 7,        /* double[n_k] phi_{k,j} of the last step           (A3) */

@@ -414,12 +414,15 @@ def split_point(n: Sequence[int]) -> int:
     return best
 
 
-def stable_order(idx, n, K_L):
+def stable_order(idx, n, K_L, nb_L=1, nb_R=1):
     """A0 as built here: samples bucketed by prefix index
     P(s) = mixed radix of (x_1..x_{K_L}) (x_1 most significant) and by suffix index
-    S(s) = mixed radix of (x_{K_L+1}..x_d) (x_d most significant).
-    Prefix order = stable argsort of key P*2^bS + S; suffix order = stable argsort of
-    S*2^bP + P.  Returns dict(perm_pre, offs_L, perm_suf, offs_R, P, S)."""
+    S(s) = mixed radix of (x_{K_L+1}..x_d) (x_d most significant), grouped first by the
+    gather block of the other index: virtual rows VP = floor(S nb_L / N_R) N_L + P and
+    VS = floor(P nb_R / N_L) N_R + S (nb = 1: plain P / S buckets).
+    Prefix order = stable argsort of key VP*2^bS + S; suffix order = stable argsort of
+    VS*2^bP + P.  Returns dict(perm_pre, offs_L, perm_suf, offs_R, P, S) with offsets over
+    the nb_L N_L (nb_R N_R) virtual rows."""
     idx = np.asarray(idx, dtype=np.int64)
     d = len(n)
     P = np.zeros(idx.shape[0], dtype=np.int64)
@@ -430,12 +433,14 @@ def stable_order(idx, n, K_L):
         S = S * n[k] + idx[:, k]
     NL, NR = math.prod(n[:K_L]), math.prod(n[K_L:])
     bP, bS = max(1, int(NL - 1).bit_length()), max(1, int(NR - 1).bit_length())
-    kpre = (P << bS) | S
-    ksuf = (S << bP) | P
+    VP = (S * nb_L // NR) * NL + P
+    VS = (P * nb_R // NL) * NR + S
+    kpre = (VP << bS) | S
+    ksuf = (VS << bP) | P
     perm_pre = np.argsort(kpre, kind="stable")
     perm_suf = np.argsort(ksuf, kind="stable")
-    offs_L = np.concatenate([[0], np.cumsum(np.bincount(P, minlength=NL))])
-    offs_R = np.concatenate([[0], np.cumsum(np.bincount(S, minlength=NR))])
+    offs_L = np.concatenate([[0], np.cumsum(np.bincount(VP, minlength=NL * nb_L))])
+    offs_R = np.concatenate([[0], np.cumsum(np.bincount(VS, minlength=NR * nb_R))])
     return dict(perm_pre=perm_pre, offs_L=offs_L, perm_suf=perm_suf, offs_R=offs_R, P=P, S=S)
 
 

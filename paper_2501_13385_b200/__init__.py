@@ -75,6 +75,8 @@ def load() -> ctypes.CDLL:
         "tt_last_error": (ctypes.c_char_p, [P]),
         "tt_plan": (ctypes.c_int, [ctypes.c_int, i64p, i64p, ctypes.POINTER(ctypes.c_int),
                                    i64p, i64p]),
+        "tt_plan_blocks": (ctypes.c_int, [ctypes.c_int, i64p, i64p, ctypes.POINTER(ctypes.c_int),
+                                          ctypes.POINTER(ctypes.c_int)]),
         "tt_get_stats": (ctypes.c_int, [P, ctypes.POINTER(_Stats)]),
         "tt_set_profiling": (ctypes.c_int, [P, ctypes.c_int]),
         "tt_get_profile": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_double), ctypes.c_int,
@@ -103,6 +105,16 @@ def plan(n: Sequence[int], r: Sequence[int]):
     if rc != TT_OK:
         raise PRGDError(rc, "tt_plan")
     return kl.value, nl.value, nr.value
+
+
+def plan_blocks(n: Sequence[int], r: Sequence[int]):
+    """Host-only gather-block planning (tt_plan_blocks): returns (nb_L, nb_R)."""
+    lib = load()
+    bl, br = ctypes.c_int(), ctypes.c_int()
+    rc = lib.tt_plan_blocks(len(n), _i64(n), _i64(r), ctypes.byref(bl), ctypes.byref(br))
+    if rc != TT_OK:
+        raise PRGDError(rc, "tt_plan_blocks")
+    return bl.value, br.value
 
 
 def _ptr(a: np.ndarray) -> int:
@@ -257,7 +269,8 @@ class TTContext:
             return self._m_query()
         if code in (2, 4):
             kl, nl, nr = plan(self.n, self.r)
-            return (nl if code == 2 else nr) + 1
+            bl, br = plan_blocks(self.n, self.r)
+            return (nl * bl if code == 2 else nr * br) + 1
         if code in (6, 7):
             return self.n[k]
         if code == 8:
@@ -270,7 +283,8 @@ class TTContext:
 
     def _m_query(self):
         kl, nl, nr = plan(self.n, self.r)
-        offs = np.empty(nl + 1, dtype=np.int64)
+        bl, br = plan_blocks(self.n, self.r)
+        offs = np.empty(nl * bl + 1, dtype=np.int64)
         cnt = ctypes.c_int64()
         rc = self.lib.tt_debug_get(self._h, 2, 0, _ptr(offs), offs.shape[0], ctypes.byref(cnt))
         if rc != TT_OK or cnt.value == 0:

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -40,7 +41,23 @@ int64_t sat_mul(int64_t a, int64_t b) {
 struct Plan {
   int KL = 0;
   int64_t NL = 0, NR = 0;
+  int nbL = 1, nbR = 1;   // gather blocks of the prefix / suffix orders (A0)
 };
+
+// Number of column blocks for a bucketing side whose gathered table has `rows` rows of
+// `ld` doubles.  Measured on B200 at config 5 (profiles/r01_gather_blocks.md): 2, 4, 8 blocks
+// made every pass slower (1.06 -> 1.52 / 2.57 / 4.67 ms for pass A), i.e. the passes are bound
+// by per-row work, not by gather misses, so the default is 1; PRGD_GATHER_BLOCKS overrides.
+int gather_blocks(int64_t rows, int ld) {
+  const char* env = getenv("PRGD_GATHER_BLOCKS");
+  if (env && *env) {
+    int v = atoi(env);
+    if (v >= 1 && v <= 64 && (v & (v - 1)) == 0) return v;
+  }
+  (void)rows;
+  (void)ld;
+  return 1;
+}
 
 int validate_and_plan(int d, const int64_t* n, const int64_t* r, Plan* pl, std::string* msg) {
   if (d < 2 || d > kMaxD || !n || !r) {
@@ -96,6 +113,10 @@ int validate_and_plan(int d, const int64_t* n, const int64_t* r, Plan* pl, std::
   pl->KL = best;
   pl->NL = bNL;
   pl->NR = bNR;
+  int rk = 2;
+  while (rk < r[best]) rk <<= 1;
+  pl->nbL = gather_blocks(bNR, rk);   // prefix order gathers right-table rows
+  pl->nbR = gather_blocks(bNL, rk);   // suffix order gathers left-table rows
   return TT_OK;
 }
 
@@ -127,6 +148,9 @@ struct tt_ctx {
   Scalars* sc_host = nullptr;
   std::vector<double*> LT, EL, RT, FR;
   double *HL = nullptr, *HR = nullptr, *psiL = nullptr, *psiR = nullptr, *Ypart = nullptr;
+  double* margp = nullptr;      // marginal chunk partials, 32 * sum(n)
+  double* g_suf = nullptr;      // residual in suffix order (written by pass A)
+  int32_t* pre2suf = nullptr;   // suffix position of prefix position t
   int64_t Ypart_cap = 0;
 
   bool obs_set = false;
@@ -260,8 +284,10 @@ int ensure_base(tt_ctx* ctx) {
     if (!A(ctx, &ctx->RT[k], sz, L) || !A(ctx, &ctx->FR[k], sz, L))
       return fail(ctx, TT_ERR_OOM, "device allocation failed (right tables)");
   }
-  if (!A(ctx, &ctx->HL, ctx->plan.NL, L) || !A(ctx, &ctx->HR, ctx->plan.NR, L) ||
-      !A(ctx, &ctx->psiL, ctx->plan.NL, L) || !A(ctx, &ctx->psiR, ctx->plan.NR, L))
+  if (!A(ctx, &ctx->HL, ctx->plan.NL * ctx->plan.nbL, L) ||
+      !A(ctx, &ctx->HR, ctx->plan.NR * ctx->plan.nbR, L) ||
+      !A(ctx, &ctx->psiL, ctx->plan.NL, L) || !A(ctx, &ctx->psiR, ctx->plan.NR, L) ||
+      !A(ctx, &ctx->margp, 32 * ctx->phi_off[d], L))
     return fail(ctx, TT_ERR_OOM, "device allocation failed (H / psi)");
   int64_t ycap = 1;
   for (int k = 0; k < d; ++k) {
@@ -385,13 +411,15 @@ void enqueue_evaluate(tt_ctx* ctx, int64_t* lc) {
     b.ld = ctx->ldr[KL];
     b.perm = ctx->pos_suf;
     b.g = ctx->g;
+    b.g2 = ctx->g_suf;      // the gathered g, stored in suffix order for pass B
     b.out = ctx->HR;
     launch_seg(s, b, nullptr, lc);
     grp(ctx, 2, false);
     grp(ctx, 3, true);
-    launch_marginals(s, ctx->HL, ctx->plan.NL, KL, ctx->n_i.data(), true, ctx->h, lc);
-    launch_marginals(s, ctx->HR, ctx->plan.NR, d - KL, ctx->n_i.data() + KL, false,
-                     ctx->h + ctx->phi_off[KL], lc);
+    launch_marginals(s, ctx->HL, ctx->plan.NL * ctx->plan.nbL, KL, ctx->n_i.data(), true, ctx->h,
+                     ctx->margp, lc);
+    launch_marginals(s, ctx->HR, ctx->plan.NR * ctx->plan.nbR, d - KL, ctx->n_i.data() + KL, false,
+                     ctx->h + ctx->phi_off[KL], ctx->margp + 32 * ctx->phi_off[KL], lc);
     launch_gather_sq_sum(s, ctx->h, ctx->n_i[0], ctx->sc, lc);
     grp(ctx, 3, false);
   }
@@ -431,8 +459,7 @@ void enqueue_update(tt_ctx* ctx, int64_t* lc) {
   b.mode = kSPMM;
   b.ld = ctx->ldr[KL];
   b.col = ctx->Psuf;
-  b.perm = ctx->pos_suf;
-  b.g = ctx->g;
+  b.g = ctx->g_suf;
   b.coltab = ctx->LT[KL];
   b.rowscale = ctx->psiR;
   b.out = ctx->FR[KL];
@@ -554,44 +581,62 @@ int collect_profile(tt_ctx* ctx, int g0, int g1) {
   return TT_OK;
 }
 
-void build_plan_host(const std::vector<int64_t>& offs, int64_t nrows, std::vector<int32_t>& vrow_row,
-                     std::vector<int64_t>& vrow_begin, std::vector<int32_t>& vrow_cnt,
-                     std::vector<int32_t>& vrow_part, std::vector<int64_t>& warp_vbegin,
-                     std::vector<int32_t>& split_row, std::vector<int64_t>& split_first,
-                     int64_t* npart) {
+// Virtual-row plan of one bucketing side: rows are (gather block b, row R) = b*nrow + R in
+// sample order; rows with > kSplit samples are split over several virtual rows whose partial
+// results are reduced in slot order (k_seg_fix).  Warps pack virtual rows up to kWarpTarget
+// samples and never straddle a gather-block boundary (per-block launches of the SpMM pass).
+void build_plan_host(const std::vector<int64_t>& offs, int64_t nrow, int nblk,
+                     std::vector<int32_t>& vrow_row, std::vector<int64_t>& vrow_begin,
+                     std::vector<int32_t>& vrow_cnt, std::vector<int32_t>& vrow_part,
+                     std::vector<int64_t>& warp_vbegin, std::vector<int32_t>& split_row,
+                     std::vector<int64_t>& split_first, std::vector<int64_t>& blk_warp,
+                     std::vector<int64_t>& blk_split, int64_t* npart) {
   int64_t np = 0;
-  for (int64_t P = 0; P < nrows; ++P) {
-    const int64_t b = offs[P], cnt = offs[P + 1] - offs[P];
-    if (cnt <= kSplit) {
-      vrow_row.push_back((int32_t)P);
-      vrow_begin.push_back(b);
-      vrow_cnt.push_back((int32_t)cnt);
-      vrow_part.push_back(-1);
-    } else {
-      split_row.push_back((int32_t)P);
-      split_first.push_back(np);
-      for (int64_t o = 0; o < cnt; o += kSplit) {
+  std::vector<int64_t> blk_vrow(nblk + 1, 0);
+  blk_split.assign(nblk + 1, 0);
+  for (int b = 0; b < nblk; ++b) {
+    blk_vrow[b] = (int64_t)vrow_row.size();
+    blk_split[b] = (int64_t)split_row.size();
+    for (int64_t R = 0; R < nrow; ++R) {
+      const int64_t P = (int64_t)b * nrow + R;
+      const int64_t beg = offs[P], cnt = offs[P + 1] - offs[P];
+      if (cnt <= kSplit) {
         vrow_row.push_back((int32_t)P);
-        vrow_begin.push_back(b + o);
-        vrow_cnt.push_back((int32_t)std::min<int64_t>(kSplit, cnt - o));
-        vrow_part.push_back((int32_t)np++);
+        vrow_begin.push_back(beg);
+        vrow_cnt.push_back((int32_t)cnt);
+        vrow_part.push_back(-1);
+      } else {
+        split_row.push_back((int32_t)P);
+        split_first.push_back(np);
+        for (int64_t o = 0; o < cnt; o += kSplit) {
+          vrow_row.push_back((int32_t)P);
+          vrow_begin.push_back(beg + o);
+          vrow_cnt.push_back((int32_t)std::min<int64_t>(kSplit, cnt - o));
+          vrow_part.push_back((int32_t)np++);
+        }
       }
     }
   }
+  blk_vrow[nblk] = (int64_t)vrow_row.size();
+  blk_split[nblk] = (int64_t)split_row.size();
   split_first.push_back(np);
   *npart = np;
+  blk_warp.assign(nblk + 1, 0);
   warp_vbegin.push_back(0);
-  int64_t acc = 0, nv = 0;
-  for (size_t v = 0; v < vrow_row.size(); ++v) {
-    acc += vrow_cnt[v] + 1;
-    ++nv;
-    if (acc >= kWarpTarget || nv >= kMaxVrowsPerWarp) {
-      warp_vbegin.push_back((int64_t)v + 1);
-      acc = 0;
-      nv = 0;
+  for (int b = 0; b < nblk; ++b) {
+    blk_warp[b] = (int64_t)warp_vbegin.size() - 1;
+    int64_t acc = 0, nv = 0;
+    for (int64_t v = blk_vrow[b]; v < blk_vrow[b + 1]; ++v) {
+      acc += vrow_cnt[v] + 1;
+      ++nv;
+      if (acc >= kWarpTarget || nv >= kMaxVrowsPerWarp || v + 1 == blk_vrow[b + 1]) {
+        warp_vbegin.push_back(v + 1);
+        acc = 0;
+        nv = 0;
+      }
     }
   }
-  if (warp_vbegin.back() != (int64_t)vrow_row.size()) warp_vbegin.push_back((int64_t)vrow_row.size());
+  blk_warp[nblk] = (int64_t)warp_vbegin.size() - 1;
 }
 
 template <class T>
@@ -602,14 +647,19 @@ int upload(tt_ctx* ctx, T** dst, const std::vector<T>& src) {
   return TT_OK;
 }
 
-int make_plan(tt_ctx* ctx, const std::vector<int64_t>& offs, int64_t nrows, int ld, SegPlan* pl) {
+int make_plan(tt_ctx* ctx, const std::vector<int64_t>& offs, int64_t nrow, int nblk, int ld,
+              SegPlan* pl) {
   std::vector<int32_t> vrow_row, vrow_cnt, vrow_part, split_row;
-  std::vector<int64_t> vrow_begin, warp_vbegin, split_first;
+  std::vector<int64_t> vrow_begin, warp_vbegin, split_first, blk_warp, blk_split;
   int64_t npart = 0;
-  build_plan_host(offs, nrows, vrow_row, vrow_begin, vrow_cnt, vrow_part, warp_vbegin, split_row,
-                  split_first, &npart);
+  build_plan_host(offs, nrow, nblk, vrow_row, vrow_begin, vrow_cnt, vrow_part, warp_vbegin,
+                  split_row, split_first, blk_warp, blk_split, &npart);
   *pl = SegPlan();
-  pl->nrows = nrows;
+  pl->nrows = nrow * nblk;
+  pl->nrow_real = nrow;
+  pl->nblk = nblk;
+  pl->blk_warp = blk_warp;
+  pl->blk_split = blk_split;
   pl->nvrows = (int64_t)vrow_row.size();
   pl->nwarps = (int64_t)warp_vbegin.size() - 1;
   pl->nsplit = (int64_t)split_row.size();
@@ -644,6 +694,16 @@ int tt_plan(int d, const int64_t* n, const int64_t* r, int* K_L, int64_t* N_L, i
   if (K_L) *K_L = pl.KL;
   if (N_L) *N_L = pl.NL;
   if (N_R) *N_R = pl.NR;
+  return TT_OK;
+}
+
+int tt_plan_blocks(int d, const int64_t* n, const int64_t* r, int* nb_L, int* nb_R) {
+  Plan pl;
+  std::string msg;
+  int rc = validate_and_plan(d, n, r, &pl, &msg);
+  if (rc != TT_OK) return rc;
+  if (nb_L) *nb_L = pl.nbL;
+  if (nb_R) *nb_R = pl.nbR;
   return TT_OK;
 }
 
@@ -776,6 +836,8 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
   ctx->m = 0;
   const int d = ctx->d, KL = ctx->plan.KL;
   const int64_t NL = ctx->plan.NL, NR = ctx->plan.NR;
+  const int nbL = ctx->plan.nbL, nbR = ctx->plan.nbR;
+  const int64_t NLv = NL * nbL, NRv = NR * nbR;   // virtual rows (gather block, row)
   auto& OL = ctx->obs_allocs;
   std::vector<void*> tmp;
   int32_t* idx_dev = nullptr;
@@ -791,23 +853,27 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
             A(ctx, &hist, hl, tmp) && A(ctx, &ctx->Spre, m, OL) && A(ctx, &ctx->ypre, m, OL) &&
             A(ctx, &ctx->g, m, OL) && A(ctx, &ctx->sid_pre, m, OL) && A(ctx, &ctx->pos_suf, m, OL) &&
             A(ctx, &ctx->Psuf, m, OL) && A(ctx, &ctx->sid_suf, m, OL) &&
-            A(ctx, &ctx->offsL, NL + 1, OL) && A(ctx, &ctx->offsR, NR + 1, OL);
+            A(ctx, &ctx->g_suf, m, OL) && A(ctx, &ctx->pre2suf, m, OL) &&
+            A(ctx, &ctx->offsL, NLv + 1, OL) && A(ctx, &ctx->offsR, NRv + 1, OL);
   auto cleanup = [&]() { dfree_all(ctx, tmp); };
   if (!ok) {
     cleanup();
     dfree_all(ctx, OL);
     return fail(ctx, TT_ERR_OOM, "device allocation failed (observations)");
   }
-  int bitsP = 1, bitsS = 1;
+  int bitsP = 1, bitsS = 1, bitsVP = 1, bitsVS = 1;
   while (((int64_t)1 << bitsP) < NL) ++bitsP;
   while (((int64_t)1 << bitsS) < NR) ++bitsS;
+  while (((int64_t)1 << bitsVP) < NLv) ++bitsVP;
+  while (((int64_t)1 << bitsVS) < NRv) ++bitsVS;
   cudaStream_t s = ctx->stream;
   int64_t lc = 0;
   if (m > 0) {
     CK(cudaMemcpyAsync(idx_dev, h_idx, (size_t)m * d * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(y_orig, h_vals, (size_t)m * sizeof(double), cudaMemcpyHostToDevice, s));
     CK(cudaMemsetAsync(&ctx->sc->index_err, 0, sizeof(int), s));
-    launch_make_keys(s, idx_dev, m, d, ctx->n_dev, KL, bitsP, bitsS, kpre, ksuf, vals, ctx->sc, &lc);
+    launch_make_keys(s, idx_dev, m, d, ctx->n_dev, KL, bitsP, bitsS, NL, NR, nbL, nbR, kpre, ksuf,
+                     vals, ctx->sc, &lc);
     CK(cudaMemcpyAsync(vals2, vals, (size_t)m * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -818,15 +884,15 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
     }
     uint64_t* ko;
     uint32_t* vo;
-    radix_sort_pairs(s, kpre, vals, ktmp, vtmp, m, bitsP + bitsS, hist, hl, &ko, &vo, &lc);
-    launch_after_sort_pre(s, ko, vo, m, bitsS, NL, y_orig, ctx->Spre, ctx->ypre, ctx->sid_pre, inv,
+    radix_sort_pairs(s, kpre, vals, ktmp, vtmp, m, bitsVP + bitsS, hist, hl, &ko, &vo, &lc);
+    launch_after_sort_pre(s, ko, vo, m, bitsS, NLv, y_orig, ctx->Spre, ctx->ypre, ctx->sid_pre, inv,
                           ctx->offsL, &lc);
-    radix_sort_pairs(s, ksuf, vals2, ktmp, vtmp, m, bitsP + bitsS, hist, hl, &ko, &vo, &lc);
-    launch_after_sort_suf(s, ko, vo, m, bitsP, NR, inv, ctx->pos_suf, ctx->Psuf, ctx->sid_suf,
-                          ctx->offsR, &lc);
+    radix_sort_pairs(s, ksuf, vals2, ktmp, vtmp, m, bitsVS + bitsP, hist, hl, &ko, &vo, &lc);
+    launch_after_sort_suf(s, ko, vo, m, bitsP, NRv, inv, ctx->pos_suf, ctx->Psuf, ctx->sid_suf,
+                          ctx->pre2suf, ctx->offsR, &lc);
   } else {
-    CK(cudaMemsetAsync(ctx->offsL, 0, (NL + 1) * sizeof(int64_t), s));
-    CK(cudaMemsetAsync(ctx->offsR, 0, (NR + 1) * sizeof(int64_t), s));
+    CK(cudaMemsetAsync(ctx->offsL, 0, (NLv + 1) * sizeof(int64_t), s));
+    CK(cudaMemsetAsync(ctx->offsR, 0, (NRv + 1) * sizeof(int64_t), s));
   }
   ctx->launches += lc;
   cudaError_t e = cudaGetLastError();
@@ -834,13 +900,13 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
     cleanup();
     return cuda_fail(ctx, e, "bucketing kernels");
   }
-  std::vector<int64_t> hoffsL(NL + 1), hoffsR(NR + 1);
-  CK(cudaMemcpyAsync(hoffsL.data(), ctx->offsL, (NL + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(hoffsR.data(), ctx->offsR, (NR + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  std::vector<int64_t> hoffsL(NLv + 1), hoffsR(NRv + 1);
+  CK(cudaMemcpyAsync(hoffsL.data(), ctx->offsL, (NLv + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hoffsR.data(), ctx->offsR, (NRv + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   cleanup();
-  if ((rc = make_plan(ctx, hoffsL, NL, ctx->ldr[KL], &ctx->planL))) return rc;
-  if ((rc = make_plan(ctx, hoffsR, NR, ctx->ldr[KL], &ctx->planR))) return rc;
+  if ((rc = make_plan(ctx, hoffsL, NL, nbL, ctx->ldr[KL], &ctx->planL))) return rc;
+  if ((rc = make_plan(ctx, hoffsR, NR, nbR, ctx->ldr[KL], &ctx->planR))) return rc;
   ctx->m = m;
   double nstar = 1.0;
   for (int k = 0; k < d; ++k) nstar *= (double)ctx->n[k];
@@ -997,8 +1063,8 @@ int tt_debug_get(tt_ctx* ctx, int what, int k, void* h_out, int64_t cap, int64_t
   switch (what) {
     case TT_DBG_PERM_PRE: src = ctx->sid_pre; cnt = ctx->m; esz = 4; break;
     case TT_DBG_PERM_SUF: src = ctx->sid_suf; cnt = ctx->m; esz = 4; break;
-    case TT_DBG_OFFS_L: src = ctx->offsL; cnt = ctx->obs_set ? ctx->plan.NL + 1 : 0; esz = 8; break;
-    case TT_DBG_OFFS_R: src = ctx->offsR; cnt = ctx->obs_set ? ctx->plan.NR + 1 : 0; esz = 8; break;
+    case TT_DBG_OFFS_L: src = ctx->offsL; cnt = ctx->obs_set ? ctx->plan.NL * ctx->plan.nbL + 1 : 0; esz = 8; break;
+    case TT_DBG_OFFS_R: src = ctx->offsR; cnt = ctx->obs_set ? ctx->plan.NR * ctx->plan.nbR + 1 : 0; esz = 8; break;
     case TT_DBG_H:
     case TT_DBG_PHI:
       if (!need_k()) return fail(ctx, TT_ERR_ARG, "bad k");

@@ -25,6 +25,9 @@ constexpr unsigned kFull = 0xffffffffu;
 
 struct SegDev {
   int64_t nwarps;
+  int64_t warp_off;       // first plan warp of this launch
+  int64_t nrow_real;      // table rows: virtual row v -> table row v % nrow_real
+  int accum;              // SpMM: add into out (gather blocks after the first)
   const int32_t* vrow_row;
   const int64_t* vrow_begin;
   const int32_t* vrow_cnt;
@@ -36,6 +39,8 @@ struct SegDev {
   const int32_t* perm;
   const double* y;
   double* g;
+  double* g2;             // SDDMM: g also scattered to g2[perm2[s]]; GSQ: gathered g stored to g2[s]
+  const int32_t* perm2;
   const double* rowtab;
   const double* coltab;
   const double* rowscale;
@@ -46,24 +51,31 @@ __device__ __forceinline__ double2 ld2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
 
+// Minimum resident CTAs per SM (register cap): measured on B200 at config 5, the SDDMM pass
+// is fastest at 4 (64 registers, no spills), the SpMM passes at 6 (40 registers).
+template <int MODE>
+struct SegOcc { static constexpr int v = MODE == kSDDMM ? 4 : (MODE == kSPMM ? 6 : 8); };
+
 template <int LPS, int MODE>
-__global__ void __launch_bounds__(256) k_seg(SegDev a, const Scalars* sc) {
+__global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Scalars* sc) {
   if (sc && sc->noop) return;
   constexpr int G = 32 / LPS;        // samples per warp step
   constexpr int STEPS = 32 / G;      // steps per 32-sample chunk (= LPS)
   constexpr int UNR = STEPS < 4 ? STEPS : 4;
   const int lane = threadIdx.x & 31;
   const int grp = lane / LPS, sub = lane - grp * LPS;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (warp >= a.nwarps) return;
+  const int64_t wl = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (wl >= a.nwarps) return;
+  const int64_t warp = wl + a.warp_off;
   const int ld = a.ld;
   const int64_t v0 = a.warp_vbegin[warp], v1 = a.warp_vbegin[warp + 1];
   for (int64_t v = v0; v < v1; ++v) {
     const int32_t row = a.vrow_row[v];
+    const int64_t trow = row % a.nrow_real;
     const int64_t beg = a.vrow_begin[v];
     const int cnt = a.vrow_cnt[v];
     double2 rv = make_double2(0.0, 0.0);
-    if (MODE == kSDDMM) rv = ld2(a.rowtab + (int64_t)row * ld + 2 * sub);
+    if (MODE == kSDDMM) rv = ld2(a.rowtab + trow * ld + 2 * sub);
     double accs = 0.0;
     double2 accv = make_double2(0.0, 0.0);
     for (int c0 = 0; c0 < cnt; c0 += 32) {
@@ -71,14 +83,19 @@ __global__ void __launch_bounds__(256) k_seg(SegDev a, const Scalars* sc) {
       const int64_t s = beg + c0 + lane;
       const bool have = lane < nc;
       // lane-parallel loads of this chunk's per-sample data (coalesced / independent)
-      int colv = 0;
+      int colv = 0, p2v = 0;
       double xv = 0.0;    // y (SDDMM) or g (GSQ, SPMM)
       if (have) {
         if (MODE != kGSQ) colv = a.col[s];
-        if (MODE == kSDDMM) xv = a.y[s];
-        else xv = a.perm ? a.g[a.perm[s]] : a.g[s];
+        if (MODE == kSDDMM) {
+          xv = a.y[s];
+          if (a.g2) p2v = a.perm2[s];
+        } else {
+          xv = a.perm ? a.g[a.perm[s]] : a.g[s];
+        }
       }
       if (MODE == kGSQ) {
+        if (have && a.g2) a.g2[s] = xv;
         accs = fma(xv, xv, accs);
         continue;
       }
@@ -101,10 +118,12 @@ __global__ void __launch_bounds__(256) k_seg(SegDev a, const Scalars* sc) {
             double part = fma(rv.x, b[u].x, rv.y * b[u].y);
 #pragma unroll
             for (int o = LPS / 2; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
+            const int p2 = a.g2 ? __shfl_sync(kFull, p2v, t & 31) : 0;
             if (t < nc) {
               const double gv = part - xs[u];
               if (sub == 0) {
                 a.g[beg + c0 + t] = gv;
+                if (a.g2) a.g2[p2] = gv;
                 accs = fma(gv, gv, accs);
               }
             }
@@ -141,10 +160,15 @@ __global__ void __launch_bounds__(256) k_seg(SegDev a, const Scalars* sc) {
       if (grp == 0) {
         double* dst;
         if (pslot < 0) {
-          const double f = a.rowscale ? a.rowscale[row] : 1.0;
+          const double f = a.rowscale ? a.rowscale[trow] : 1.0;
           accv.x *= f;
           accv.y *= f;
-          dst = a.out + (int64_t)row * ld + 2 * sub;
+          dst = a.out + trow * ld + 2 * sub;
+          if (a.accum) {
+            const double2 o = *reinterpret_cast<const double2*>(dst);
+            accv.x += o.x;
+            accv.y += o.y;
+          }
         } else {
           dst = a.part + (int64_t)pslot * ld + 2 * sub;
         }
@@ -155,23 +179,26 @@ __global__ void __launch_bounds__(256) k_seg(SegDev a, const Scalars* sc) {
 }
 
 // Sum the partial slots of split buckets in slot order.
-__global__ void k_seg_fix(int vec, int64_t nsplit, const int32_t* __restrict__ split_row,
+__global__ void k_seg_fix(int vec, int64_t s0, int64_t nsplit, const int32_t* __restrict__ split_row,
                           const int64_t* __restrict__ split_first, const double* __restrict__ part,
                           int ld, const double* __restrict__ rowscale, double* __restrict__ out,
-                          const Scalars* sc) {
+                          int64_t nrow_real, int accum, const Scalars* sc) {
   if (sc && sc->noop) return;
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int w = vec ? ld : 1;
   int64_t i = e / w;
   int c = (int)(e - i * w);
   if (i >= nsplit) return;
+  i += s0;
   const int32_t row = split_row[i];
   double acc = 0.0;
   for (int64_t sl = split_first[i]; sl < split_first[i + 1]; ++sl)
     acc += vec ? part[sl * ld + c] : part[sl];
   if (vec) {
-    if (rowscale) acc *= rowscale[row];
-    out[(int64_t)row * ld + c] = acc;
+    const int64_t trow = row % nrow_real;
+    if (rowscale) acc *= rowscale[trow];
+    double* dst = out + trow * ld + c;
+    *dst = accum ? *dst + acc : acc;
   } else {
     out[row] = acc;
   }
@@ -186,21 +213,32 @@ struct MargArgs {
   int64_t N;
 };
 
-// One block per (mode, slice j): h[j] = sum_{hi, lo} H[(hi*n + j)*stride + lo], fixed order.
-__global__ void k_marginals(const double* __restrict__ H, MargArgs ma, double* __restrict__ h) {
+// Marginals in two deterministic stages.  Block (bin = (mode, j), chunk) sums its chunk of
+// the (hi, lo) index space of H[(hi*n + j)*stride + lo] (fixed thread order + tree), then
+// one warp per bin adds the chunk partials in chunk order.
+constexpr int kMargChunks = 32;
+__global__ void k_marg_partial(const double* __restrict__ H, MargArgs ma, double* __restrict__ part) {
   __shared__ double red[256];
-  int b = blockIdx.x;
+  const int bin = blockIdx.x, chunk = blockIdx.y;
   int m = 0;
-  while (m + 1 < ma.nm && ma.blk_off[m + 1] <= b) ++m;
-  const int j = b - (int)ma.blk_off[m];
+  while (m + 1 < ma.nm && ma.blk_off[m + 1] <= bin) ++m;
+  const int j = bin - (int)ma.blk_off[m];
   const int64_t st = ma.stride[m];
   const int64_t span = (int64_t)ma.n[m] * st;
-  const int64_t nhi = ma.N / span;
-  const int64_t total = nhi * st;
+  const int64_t total = (ma.N / span) * st;
+  const int64_t per = (total + kMargChunks - 1) / kMargChunks;
+  const int64_t e0 = chunk * per, e1 = e0 + per < total ? e0 + per : total;
   double acc = 0.0;
-  for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
-    int64_t hi = e / st, lo = e - hi * st;
-    acc += H[hi * span + (int64_t)j * st + lo];
+  if (st >= 32) {
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      const int64_t hi = e / st, lo = e - hi * st;
+      acc += H[hi * span + (int64_t)j * st + lo];
+    }
+  } else {
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      const int64_t hi = e / st, lo = e - hi * st;
+      acc += H[hi * span + (int64_t)j * st + lo];
+    }
   }
   red[threadIdx.x] = acc;
   __syncthreads();
@@ -208,7 +246,20 @@ __global__ void k_marginals(const double* __restrict__ H, MargArgs ma, double* _
     if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) h[ma.out_off[m] + j] = red[0];
+  if (threadIdx.x == 0) part[(int64_t)bin * kMargChunks + chunk] = red[0];
+}
+
+__global__ void k_marg_final(const double* __restrict__ part, int nbins, const int64_t* __restrict__ dummy,
+                             MargArgs ma, double* __restrict__ h) {
+  const int bin = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (bin >= nbins) return;
+  double v = lane < kMargChunks ? part[(int64_t)bin * kMargChunks + lane] : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  int m = 0;
+  while (m + 1 < ma.nm && ma.blk_off[m + 1] <= bin) ++m;
+  if (lane == 0) h[ma.out_off[m] + (bin - ma.blk_off[m])] = v;
+  (void)dummy;
 }
 
 __global__ void k_weights(const double* __restrict__ h, int d, int64_t nsum, int n0, int eps_rule,
@@ -352,6 +403,9 @@ void launch_seg(cudaStream_t s, const SegArgs& a, const Scalars* sc, int64_t* la
   if (p.nwarps == 0) return;
   SegDev dv;
   dv.nwarps = p.nwarps;
+  dv.warp_off = 0;
+  dv.nrow_real = p.nrow_real > 0 ? p.nrow_real : p.nrows;
+  dv.accum = 0;
   dv.vrow_row = p.vrow_row;
   dv.vrow_begin = p.vrow_begin;
   dv.vrow_cnt = p.vrow_cnt;
@@ -363,32 +417,48 @@ void launch_seg(cudaStream_t s, const SegArgs& a, const Scalars* sc, int64_t* la
   dv.perm = a.perm;
   dv.y = a.y;
   dv.g = a.g;
+  dv.g2 = a.g2;
+  dv.perm2 = a.perm2;
   dv.rowtab = a.rowtab;
   dv.coltab = a.coltab;
   dv.rowscale = a.rowscale;
   dv.out = a.out;
-  unsigned grid = blocks_for(p.nwarps * 32, 256);
-  switch (a.ld / 2) {
-    case 1: seg_dispatch_mode<1>(s, a.mode, dv, grid, sc); break;
-    case 2: seg_dispatch_mode<2>(s, a.mode, dv, grid, sc); break;
-    case 4: seg_dispatch_mode<4>(s, a.mode, dv, grid, sc); break;
-    case 8: seg_dispatch_mode<8>(s, a.mode, dv, grid, sc); break;
-    default: seg_dispatch_mode<16>(s, a.mode, dv, grid, sc); break;
-  }
-  ++*launches;
-  if (p.nsplit > 0) {
-    const int vec = a.mode == kSPMM ? 1 : 0;
-    int64_t n = p.nsplit * (vec ? a.ld : 1);
-    k_seg_fix<<<blocks_for(n, 256), 256, 0, s>>>(vec, p.nsplit, p.split_row, p.split_first,
-                                                 p.part, a.ld, a.rowscale, a.out, sc);
-    ++*launches;
+  const int vec = a.mode == kSPMM ? 1 : 0;
+  // SpMM outputs are table rows shared by all gather blocks: one launch per block, the later
+  // ones accumulating (launch order = fixed summation order).  Scalar outputs are per virtual
+  // row: one launch.
+  const int nb = (vec && p.nblk > 1) ? p.nblk : 1;
+  for (int b = 0; b < nb; ++b) {
+    const int64_t w0 = nb > 1 ? p.blk_warp[b] : 0, w1 = nb > 1 ? p.blk_warp[b + 1] : p.nwarps;
+    const int64_t s0 = nb > 1 ? p.blk_split[b] : 0, s1 = nb > 1 ? p.blk_split[b + 1] : p.nsplit;
+    dv.warp_off = w0;
+    dv.nwarps = w1 - w0;
+    dv.accum = b > 0 ? 1 : 0;
+    if (dv.nwarps > 0) {
+      unsigned grid = blocks_for(dv.nwarps * 32, 256);
+      switch (a.ld / 2) {
+        case 1: seg_dispatch_mode<1>(s, a.mode, dv, grid, sc); break;
+        case 2: seg_dispatch_mode<2>(s, a.mode, dv, grid, sc); break;
+        case 4: seg_dispatch_mode<4>(s, a.mode, dv, grid, sc); break;
+        case 8: seg_dispatch_mode<8>(s, a.mode, dv, grid, sc); break;
+        default: seg_dispatch_mode<16>(s, a.mode, dv, grid, sc); break;
+      }
+      ++*launches;
+    }
+    if (s1 > s0) {
+      int64_t n = (s1 - s0) * (vec ? a.ld : 1);
+      k_seg_fix<<<blocks_for(n, 256), 256, 0, s>>>(vec, s0, s1 - s0, p.split_row, p.split_first,
+                                                   p.part, a.ld, a.rowscale, a.out, dv.nrow_real,
+                                                   dv.accum, sc);
+      ++*launches;
+    }
   }
 }
 
 // n_modes / strides are passed in n_dev_modes as host pointer to an int array of
 // [nm] sizes (host!), msd_first: left side (first mode most significant).
 void launch_marginals(cudaStream_t s, const double* H, int64_t N, int nm, const int* n_host,
-                      bool msd_first, double* h_out, int64_t* launches) {
+                      bool msd_first, double* h_out, double* scratch, int64_t* launches) {
   MargArgs ma;
   ma.nm = nm;
   ma.N = N;
@@ -407,8 +477,11 @@ void launch_marginals(cudaStream_t s, const double* H, int64_t N, int nm, const 
     off += n_host[m];
     ma.blk_off[m + 1] = off;
   }
-  k_marginals<<<(unsigned)off, 256, 0, s>>>(H, ma, h_out);
-  ++*launches;
+  static_assert(kMargChunks <= 32, "one warp per bin");
+  k_marg_partial<<<dim3((unsigned)off, kMargChunks), 256, 0, s>>>(H, ma, scratch);
+  k_marg_final<<<(unsigned)((off * 32 + 255) / 256), 256, 0, s>>>(scratch, (int)off, nullptr, ma,
+                                                                  h_out);
+  *launches += 2;
 }
 
 void launch_weights(cudaStream_t s, const double* h, int d, const int* n_host, int64_t nsum,

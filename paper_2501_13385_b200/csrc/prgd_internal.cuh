@@ -41,7 +41,11 @@ enum ErrBits { kErrNaN = 1, kErrChol = 2, kErrSVD = 4 };
 
 // CSR-like "virtual row" plan of one bucketing side (host-built, device copy).
 struct SegPlan {
-  int64_t nrows = 0;        // real rows (N_L or N_R)
+  int64_t nrows = 0;        // virtual rows (nblk * nrow_real)
+  int64_t nrow_real = 0;    // table rows (N_L or N_R)
+  int nblk = 1;             // gather blocks
+  std::vector<int64_t> blk_warp;    // [nblk+1] warp range of each gather block (host)
+  std::vector<int64_t> blk_split;   // [nblk+1] split-row range of each gather block (host)
   int64_t nvrows = 0;
   int64_t nwarps = 0;
   int64_t nsplit = 0;       // rows split over several vrows
@@ -84,8 +88,9 @@ struct DenseArgs {
 // ------------------------------------------------------------------ kernels (launchers)
 // sort.cu
 void launch_make_keys(cudaStream_t s, const int32_t* idx, int64_t m, int d, const int* n_dev,
-                      int KL, int bitsP, int bitsS, uint64_t* kpre, uint64_t* ksuf,
-                      uint32_t* vals, Scalars* sc, int64_t* launches);
+                      int KL, int bitsP, int bitsS, int64_t NL, int64_t NR, int nbL, int nbR,
+                      uint64_t* kpre, uint64_t* ksuf, uint32_t* vals, Scalars* sc,
+                      int64_t* launches);
 void radix_sort_pairs(cudaStream_t s, uint64_t* keys, uint32_t* vals, uint64_t* keys_tmp,
                       uint32_t* vals_tmp, int64_t m, int bits, int* hist_buf, int64_t hist_len,
                       uint64_t** keys_out, uint32_t** vals_out, int64_t* launches);
@@ -96,7 +101,8 @@ void launch_after_sort_pre(cudaStream_t s, const uint64_t* keys, const uint32_t*
                            int64_t* launches);
 void launch_after_sort_suf(cudaStream_t s, const uint64_t* keys, const uint32_t* sids, int64_t m,
                            int bitsP, int64_t NR, const int32_t* inv, int32_t* pos_suf,
-                           int32_t* Psuf, int32_t* sid_suf, int64_t* offsR, int64_t* launches);
+                           int32_t* Psuf, int32_t* sid_suf, int32_t* pre2suf, int64_t* offsR,
+                           int64_t* launches);
 
 // tables.cu
 void launch_table_left(cudaStream_t s, const double* in, int ld_in, const double* core, int r0,
@@ -184,6 +190,8 @@ struct SegArgs {
   const int32_t* perm;  // per-sample index into g (GSQ, SPMM suffix side) or null
   const double* y;      // SDDMM
   double* g;            // SDDMM writes, GSQ/SPMM read
+  double* g2 = nullptr;         // SDDMM: also writes g2[perm2[s]] (g in the other order)
+  const int32_t* perm2 = nullptr;
   const double* rowtab; // SDDMM row vectors
   const double* coltab; // gathered table
   const double* rowscale;  // SPMM output scale (psi) or null
@@ -191,8 +199,9 @@ struct SegArgs {
 };
 void launch_seg(cudaStream_t s, const SegArgs& a, const Scalars* sc, int64_t* launches);
 // n_host / phi_off_host are HOST arrays (values are passed by kernel argument).
+// scratch: >= 32 * (sum of the nmodes mode sizes) doubles
 void launch_marginals(cudaStream_t s, const double* H, int64_t N, int nmodes, const int* n_host,
-                      bool msd_first, double* h_out, int64_t* launches);
+                      bool msd_first, double* h_out, double* scratch, int64_t* launches);
 void launch_weights(cudaStream_t s, const double* h, int d, const int* n_host, int64_t nsum,
                     int eps_rule, double eps_fixed, int step_rule, double* phi, Scalars* sc,
                     int64_t* launches);

@@ -2,8 +2,11 @@
 //
 // Each sample s gets a prefix index P(s) (mixed radix of x_0..x_{KL-1}, x_0 most
 // significant) and a suffix index S(s) (mixed radix of x_KL..x_{d-1}, x_{d-1} most
-// significant).  Prefix order = stable sort by key (P << bitsS) | S, suffix order =
-// stable sort by (S << bitsP) | P: an LSD radix sort whose passes are stable
+// significant).  The prefix order groups samples by the virtual row
+// VP = floor(S nbL / N_R) N_L + P (gather block of S first, so that a pass over it gathers
+// right-table rows from one L2-resident block at a time), the suffix order by
+// VS = floor(P nbR / N_L) N_R + S.  Prefix order = stable sort by key (VP << bitsS) | S,
+// suffix order = stable sort by (VS << bitsP) | P: an LSD radix sort whose passes are stable
 // counting sorts of 8-bit digits (histogram -> exclusive scan -> stable scatter).
 // The result is unique (stable sorts are), so it is compared bit-exactly with the
 // oracle's numpy argsort(kind="stable") on the same keys.
@@ -18,9 +21,9 @@ constexpr int kRsSub = 512;                     // items per warp per tile
 constexpr int kRsTile = kRsSub * kRsWarps;      // 4096 items per block
 
 __global__ void k_make_keys(const int32_t* __restrict__ idx, int64_t m, int d,
-                            const int* __restrict__ n, int KL, int bitsP, int bitsS,
-                            uint64_t* __restrict__ kpre, uint64_t* __restrict__ ksuf,
-                            uint32_t* __restrict__ vals, Scalars* sc) {
+                            const int* __restrict__ n, int KL, int bitsP, int bitsS, int64_t NL,
+                            int64_t NR, int nbL, int nbR, uint64_t* __restrict__ kpre,
+                            uint64_t* __restrict__ ksuf, uint32_t* __restrict__ vals, Scalars* sc) {
   int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= m) return;
   const int32_t* x = idx + s * d;
@@ -41,8 +44,11 @@ __global__ void k_make_keys(const int32_t* __restrict__ idx, int64_t m, int d,
     P = 0;
     S = 0;
   }
-  kpre[s] = (P << bitsS) | S;
-  ksuf[s] = (S << bitsP) | P;
+  // virtual rows: gather block of the other side's index first (A0)
+  const uint64_t VP = (S * (uint64_t)nbL / (uint64_t)NR) * (uint64_t)NL + P;
+  const uint64_t VS = (P * (uint64_t)nbR / (uint64_t)NL) * (uint64_t)NR + S;
+  kpre[s] = (VP << bitsS) | S;
+  ksuf[s] = (VS << bitsP) | P;
   vals[s] = (uint32_t)s;
 }
 
@@ -157,7 +163,8 @@ __global__ void k_after_pre(const uint64_t* __restrict__ keys, const uint32_t* _
 __global__ void k_after_suf(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ sids,
                             int64_t m, int bitsP, int64_t NR, const int32_t* __restrict__ inv,
                             int32_t* __restrict__ pos_suf, int32_t* __restrict__ Psuf,
-                            int32_t* __restrict__ sid_suf, int64_t* __restrict__ offsR) {
+                            int32_t* __restrict__ sid_suf, int32_t* __restrict__ pre2suf,
+                            int64_t* __restrict__ offsR) {
   int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (u >= m) return;
   const uint64_t mask = (1ull << bitsP) - 1ull;
@@ -166,6 +173,7 @@ __global__ void k_after_suf(const uint64_t* __restrict__ keys, const uint32_t* _
   uint32_t sid = sids[u];
   Psuf[u] = (int32_t)(key & mask);
   pos_suf[u] = inv[sid];
+  pre2suf[inv[sid]] = (int32_t)u;
   sid_suf[u] = (int32_t)sid;
   int64_t Sprev = u == 0 ? -1 : (int64_t)(keys[u - 1] >> bitsP);
   for (int64_t q = Sprev + 1; q <= S; ++q) offsR[q] = u;
@@ -185,11 +193,12 @@ int64_t radix_hist_len(int64_t m) {
 }
 
 void launch_make_keys(cudaStream_t s, const int32_t* idx, int64_t m, int d, const int* n_dev,
-                      int KL, int bitsP, int bitsS, uint64_t* kpre, uint64_t* ksuf,
-                      uint32_t* vals, Scalars* sc, int64_t* launches) {
+                      int KL, int bitsP, int bitsS, int64_t NL, int64_t NR, int nbL, int nbR,
+                      uint64_t* kpre, uint64_t* ksuf, uint32_t* vals, Scalars* sc,
+                      int64_t* launches) {
   if (m <= 0) return;
-  k_make_keys<<<grid_for(m, 256), 256, 0, s>>>(idx, m, d, n_dev, KL, bitsP, bitsS, kpre, ksuf,
-                                                vals, sc);
+  k_make_keys<<<grid_for(m, 256), 256, 0, s>>>(idx, m, d, n_dev, KL, bitsP, bitsS, NL, NR, nbL,
+                                                nbR, kpre, ksuf, vals, sc);
   ++*launches;
 }
 
@@ -233,10 +242,11 @@ void launch_after_sort_pre(cudaStream_t s, const uint64_t* keys, const uint32_t*
 
 void launch_after_sort_suf(cudaStream_t s, const uint64_t* keys, const uint32_t* sids, int64_t m,
                            int bitsP, int64_t NR, const int32_t* inv, int32_t* pos_suf,
-                           int32_t* Psuf, int32_t* sid_suf, int64_t* offsR, int64_t* launches) {
+                           int32_t* Psuf, int32_t* sid_suf, int32_t* pre2suf, int64_t* offsR,
+                           int64_t* launches) {
   if (m <= 0) return;
   k_after_suf<<<grid_for(m, 256), 256, 0, s>>>(keys, sids, m, bitsP, NR, inv, pos_suf, Psuf,
-                                                sid_suf, offsR);
+                                                sid_suf, pre2suf, offsR);
   ++*launches;
 }
 

@@ -379,3 +379,36 @@ def test_split_point():
     assert oracle.split_point((50,) * 4) == 2
     assert oracle.split_point((256, 256, 128)) == 1
     assert oracle.split_point((20, 20, 20)) == 1
+
+
+def test_blocked_stable_order_matches_python_sort():
+    # Gather-blocked A0 order: prefix order sorted by
+    # (block of S, P, S), block = floor(S nb / N_R), stable; suffix by (block of P, S, P).
+    rng = np.random.default_rng(15)
+    n = (3, 5, 2, 4)
+    m = 300
+    idx = np.stack([rng.integers(0, nk, m) for nk in n], axis=1).astype(np.int32)
+    KL = oracle.split_point(n)
+    NL, NR = int(np.prod(n[:KL])), int(np.prod(n[KL:]))
+    for nbL, nbR in [(2, 4), (4, 2), (1, 1)]:
+        o = oracle.stable_order(idx, n, KL, nbL, nbR)
+
+        def P(s):
+            v = 0
+            for k in range(KL):
+                v = v * n[k] + int(idx[s, k])
+            return v
+
+        def S(s):
+            v = 0
+            for k in range(len(n) - 1, KL - 1, -1):
+                v = v * n[k] + int(idx[s, k])
+            return v
+
+        pre = sorted(range(m), key=lambda s: (S(s) * nbL // NR, P(s), S(s), s))
+        suf = sorted(range(m), key=lambda s: (P(s) * nbR // NL, S(s), P(s), s))
+        assert list(o["perm_pre"]) == pre and list(o["perm_suf"]) == suf
+        assert len(o["offs_L"]) == nbL * NL + 1 and len(o["offs_R"]) == nbR * NR + 1
+        vp = [(S(s) * nbL // NR) * NL + P(s) for s in pre]
+        for v in range(nbL * NL):
+            assert o["offs_L"][v + 1] - o["offs_L"][v] == vp.count(v)
