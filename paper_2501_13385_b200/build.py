@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libprgd.so")
 SOURCES = ["api.cu", "sort.cu", "tables.cu", "levels.cu", "passes.cu", "dense.cu"]
-INCLUDES = ["round_cluster.inc"]
+INCLUDES = ["round_cs.inc"]
 HEADERS = ["prgd_internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

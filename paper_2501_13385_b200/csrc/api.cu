@@ -256,6 +256,7 @@ int ensure_base(tt_ctx* ctx) {
   {
     int64_t S = 2, nmax = 1;
     for (int k = 0; k <= d; ++k) S = std::max<int64_t>(S, 2 * ctx->r[k]);
+    S = S <= 8 ? 8 : (S <= 16 ? 16 : std::max<int64_t>(S, 32));   // template sizes of k_round_cs
     for (int k = 0; k < d; ++k) nmax = std::max<int64_t>(nmax, ctx->n[k]);
     const int64_t nc = round_cluster_size();
     const int64_t lds = S <= 4 ? 4 : ((S + 11) / 16) * 16 + 4;

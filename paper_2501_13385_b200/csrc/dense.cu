@@ -771,6 +771,9 @@ __device__ __noinline__ bool blk_jacobi(double* X, int rows, int kc, double* V, 
 // Norms of the kc columns of X (rows x kc col-major) into nrm, and the permutation
 // perm sorting them by norm (descending, ties by index).  Ends with a barrier.
 __device__ __noinline__ void col_norms_sorted(const double* X, int rows, int kc, double* nrm, int* perm) {
+  __builtin_assume(__isShared(X));
+  __builtin_assume(__isShared(nrm));
+  __builtin_assume(__isShared(perm));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int c = warp; c < kc; c += nw) {
     double s = 0.0;
@@ -1266,7 +1269,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
   }
 }
 
-#include "round_cluster.inc"
+#include "round_cs.inc"
 
 }  // namespace
 
@@ -1277,7 +1280,7 @@ void dense_init() {
   cudaFuncSetAttribute(k_dense_orth, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_dense_round, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cudaFuncSetAttribute(k_project, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cudaFuncSetAttribute(k_round_cl, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  round_cs_init(bytes);
 }
 
 int round_cluster_size() { return kNC; }
@@ -1297,8 +1300,7 @@ void launch_dense_orth(cudaStream_t s, const DenseArgs& a, int64_t* launches) {
 void launch_dense_round(cudaStream_t s, const DenseArgs& a, int64_t* launches) {
   const size_t bytes = (size_t)a.smem_doubles * sizeof(double);
   k_project<<<a.d, kDenseThreads, bytes, s>>>(a);
-  if (a.clw && round_cluster_ok(a.d, a.r)) k_round_cl<<<kNC, kDenseThreads, bytes, s>>>(a);
-  else k_dense_round<<<1, kDenseThreads, bytes, s>>>(a);
+  if (!(a.clw && launch_round_cs(s, a, bytes))) k_dense_round<<<1, kDenseThreads, bytes, s>>>(a);
   *launches += 2;
 }
 
