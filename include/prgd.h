@@ -153,14 +153,20 @@ PRGD_API const char* tt_last_error(const tt_ctx* ctx);
  * Any output pointer may be NULL. */
 PRGD_API int tt_plan(int d, const int64_t* n, const int64_t* r, int* K_L, int64_t* N_L, int64_t* N_R);
 
-/* Host-only: the gather blocks of the two bucketing orders (A0).  The prefix order
- * groups samples by the virtual row VP = floor(S nb_L / N_R) N_L + P, the suffix order
- * by VS = floor(P nb_R / N_L) N_R + S, so that each pass over Omega gathers the other
- * side's table rows one L2-resident block at a time; TT_DBG_OFFS_L / _R then have
- * nb_L N_L + 1 / nb_R N_R + 1 entries.  Default nb = 1 (blocking measured slower on B200,
- * DESIGN.md); the environment variable PRGD_GATHER_BLOCKS (a power of two) overrides.
- * Validation and errors as tt_plan. */
-PRGD_API int tt_plan_blocks(int d, const int64_t* n, const int64_t* r, int* nb_L, int* nb_R);
+/* Host-only: the layout of the two bucketing orders (A0).
+ *  nb_L / nb_R  gather blocks: the prefix order groups samples by the virtual row
+ *               VP = floor(S nb_L / N_R) N_L + P, the suffix order by
+ *               VS = floor(P nb_R / N_L) N_R + S; TT_DBG_OFFS_L / _R then have
+ *               nb_L N_L + 1 / nb_R N_R + 1 entries.  Default 1 (blocking measured slower
+ *               on B200); PRGD_GATHER_BLOCKS (a power of two) overrides.
+ *  middle       1 when the passes re-associate through the middle cores K_L-1, K_L (0-based)
+ *               (DESIGN.md §2): within a prefix row samples are then ordered by
+ *               (x_{K_L}, S div n_{K_L}), within a suffix row by (x_{K_L-1}, P div n_{K_L-1}).
+ *               Chosen from the shapes (both sides >= 65536 rows, middle n r <= 512, r <= 32);
+ *               PRGD_MIDDLE=0/1 overrides.
+ * Any output pointer may be NULL.  Validation and errors as tt_plan. */
+PRGD_API int tt_plan_layout(int d, const int64_t* n, const int64_t* r, int* nb_L, int* nb_R,
+                            int* middle);
 
 /* Counters: launches = kernels this context launched since creation (graph nodes
  * counted per replay); steps = tt_prgd_step calls. */

@@ -16,7 +16,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libprgd.so")
+LIB_PATH = os.environ.get("PRGD_LIB_PATH") or os.path.join(HERE, "libprgd.so")   # override: experiments
 HEADER = os.path.join(os.path.dirname(HERE), "include", "prgd.h")
 
 TT_OK, TT_ERR_ARG, TT_ERR_RANK, TT_ERR_INDEX, TT_ERR_STATE = 0, -1, -2, -3, -4
@@ -75,8 +75,8 @@ def load() -> ctypes.CDLL:
         "tt_last_error": (ctypes.c_char_p, [P]),
         "tt_plan": (ctypes.c_int, [ctypes.c_int, i64p, i64p, ctypes.POINTER(ctypes.c_int),
                                    i64p, i64p]),
-        "tt_plan_blocks": (ctypes.c_int, [ctypes.c_int, i64p, i64p, ctypes.POINTER(ctypes.c_int),
-                                          ctypes.POINTER(ctypes.c_int)]),
+        "tt_plan_layout": (ctypes.c_int, [ctypes.c_int, i64p, i64p, ctypes.POINTER(ctypes.c_int),
+                                          ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
         "tt_get_stats": (ctypes.c_int, [P, ctypes.POINTER(_Stats)]),
         "tt_set_profiling": (ctypes.c_int, [P, ctypes.c_int]),
         "tt_get_profile": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_double), ctypes.c_int,
@@ -107,14 +107,20 @@ def plan(n: Sequence[int], r: Sequence[int]):
     return kl.value, nl.value, nr.value
 
 
-def plan_blocks(n: Sequence[int], r: Sequence[int]):
-    """Host-only gather-block planning (tt_plan_blocks): returns (nb_L, nb_R)."""
+def plan_layout(n: Sequence[int], r: Sequence[int]):
+    """Host-only bucketing layout (tt_plan_layout): returns (nb_L, nb_R, middle)."""
     lib = load()
-    bl, br = ctypes.c_int(), ctypes.c_int()
-    rc = lib.tt_plan_blocks(len(n), _i64(n), _i64(r), ctypes.byref(bl), ctypes.byref(br))
+    bl, br, mid = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    rc = lib.tt_plan_layout(len(n), _i64(n), _i64(r), ctypes.byref(bl), ctypes.byref(br),
+                            ctypes.byref(mid))
     if rc != TT_OK:
-        raise PRGDError(rc, "tt_plan_blocks")
-    return bl.value, br.value
+        raise PRGDError(rc, "tt_plan_layout")
+    return bl.value, br.value, bool(mid.value)
+
+
+def plan_blocks(n: Sequence[int], r: Sequence[int]):
+    """(nb_L, nb_R) of plan_layout."""
+    return plan_layout(n, r)[:2]
 
 
 def _ptr(a: np.ndarray) -> int:

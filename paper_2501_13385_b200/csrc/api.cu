@@ -42,7 +42,32 @@ struct Plan {
   int KL = 0;
   int64_t NL = 0, NR = 0;
   int nbL = 1, nbR = 1;   // gather blocks of the prefix / suffix orders (A0)
+  bool mid = false;       // middle-split passes: rows re-associated through
+                          // the cores K_L-1 and K_L, gathers from the level K_L-1 / K_L+1 tables
 };
+
+// Middle-split passes apply when both middle cores are small (n r <= 512 with ranks <= 32),
+// K_L >= 2 and d - K_L >= 2 (the gathered tables are the levels K_L-1 and K_L+1), and both
+// sides have >= 65536 rows (a CTA tile is 32 rows handled by one 8-lane group each).
+// PRGD_MIDDLE=0/1 overrides (experiments; shape conditions still apply).
+bool middle_ok(int d, const int64_t* n, const int64_t* r, int KL, int64_t NL, int64_t NR) {
+  if (KL < 2 || d - KL < 2) return false;
+  for (int k = KL - 1; k <= KL + 1; ++k)
+    if (r[k] > 32) return false;
+  auto pad = [](int64_t v) { int64_t p = 2; while (p < v) p <<= 1; return p; };
+  // 8-lane sample groups (2 fp64 per lane) and <= 113 KB of shared memory per CTA
+  if (pad(r[KL - 1]) > 16 || pad(r[KL]) > 16 || pad(r[KL + 1]) > 16) return false;
+  if (n[KL] * pad(r[KL + 1]) > 256 || n[KL - 1] * pad(r[KL - 1]) > 256) return false;
+  if (n[KL] * pad(r[KL + 1]) % 8 != 0 || n[KL - 1] * pad(r[KL - 1]) % 8 != 0) return false;
+  // Off by default: measured on B200 at config 5 the middle-split kernels cut DRAM traffic
+  // ~5x (L2 hit rate 82-86%) but are latency-bound on the per-row chains (pass A 2.3-3.8 ms,
+  // pass B 1.5-2.7 ms vs 1.1 / 0.86 ms for the gather passes; profiles/r01_middle_split.md).
+  const char* env = getenv("PRGD_MIDDLE");
+  if (env && *env) return atoi(env) != 0 && NL >= 32 && NR >= 32;
+  (void)NL;
+  (void)NR;
+  return false;
+}
 
 // Number of column blocks for a bucketing side whose gathered table has `rows` rows of
 // `ld` doubles.  Measured on B200 at config 5 (profiles/r01_gather_blocks.md): 2, 4, 8 blocks
@@ -117,6 +142,8 @@ int validate_and_plan(int d, const int64_t* n, const int64_t* r, Plan* pl, std::
   while (rk < r[best]) rk <<= 1;
   pl->nbL = gather_blocks(bNR, rk);   // prefix order gathers right-table rows
   pl->nbR = gather_blocks(bNL, rk);   // suffix order gathers left-table rows
+  pl->mid = middle_ok(d, n, r, best, bNL, bNR);
+  if (pl->mid) pl->nbL = pl->nbR = 1;
   return TT_OK;
 }
 
@@ -149,6 +176,8 @@ struct tt_ctx {
   std::vector<double*> LT, EL, RT, FR;
   double *HL = nullptr, *HR = nullptr, *psiL = nullptr, *psiR = nullptr, *Ypart = nullptr;
   double* margp = nullptr;      // marginal chunk partials, 32 * sum(n)
+  double *psiL1 = nullptr, *psiR1 = nullptr;   // middle-split weights (N_L/n_{KL-1}, N_R/n_KL)
+  double *TL1 = nullptr, *TR1 = nullptr;       // U tables of levels KL-1 / KL+1 scaled by psiL1 / psiR1
   double* g_suf = nullptr;      // residual in suffix order (written by pass A)
   int32_t* pre2suf = nullptr;   // suffix position of prefix position t
   int64_t Ypart_cap = 0;
@@ -288,7 +317,11 @@ int ensure_base(tt_ctx* ctx) {
   if (!A(ctx, &ctx->HL, ctx->plan.NL * ctx->plan.nbL, L) ||
       !A(ctx, &ctx->HR, ctx->plan.NR * ctx->plan.nbR, L) ||
       !A(ctx, &ctx->psiL, ctx->plan.NL, L) || !A(ctx, &ctx->psiR, ctx->plan.NR, L) ||
-      !A(ctx, &ctx->margp, 32 * ctx->phi_off[d], L))
+      !A(ctx, &ctx->margp, 32 * ctx->phi_off[d], L) ||
+      (ctx->plan.mid && (!A(ctx, &ctx->psiL1, ctx->plan.NL / ctx->n[KL - 1], L) ||
+                         !A(ctx, &ctx->psiR1, ctx->plan.NR / ctx->n[KL], L) ||
+                         !A(ctx, &ctx->TL1, ctx->NLk[KL - 1] * ctx->ldr[KL - 1], L) ||
+                         !A(ctx, &ctx->TR1, ctx->NRk[KL + 1] * ctx->ldr[KL + 1], L))))
     return fail(ctx, TT_ERR_OOM, "device allocation failed (H / psi)");
   int64_t ycap = 1;
   for (int k = 0; k < d; ++k) {
@@ -310,6 +343,7 @@ int ensure_base(tt_ctx* ctx) {
   dense_init();
   tables_init();
   levels_init();
+  passes_mid_init();
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->base_ready = true;
   return TT_OK;
@@ -351,25 +385,31 @@ void grp(tt_ctx* ctx, int id, bool begin) {
 }
 
 // ------------------------------------------------------------------ enqueue pieces
-void enqueue_tables(tt_ctx* ctx, bool useU, int64_t* lc) {
+// Tables of the left / right parts.  With the middle-split passes the
+// step needs the left levels up to K_L (C) / K_L - 1 (U) and the right levels down to
+// K_L + 1, unscaled; `full` builds every level (queries of tt_eval_at use level K_L).
+void enqueue_tables(tt_ctx* ctx, bool useU, int64_t* lc, bool full = false) {
   const int d = ctx->d, KL = ctx->plan.KL;
   cudaStream_t s = ctx->stream;
   const double* cores = useU ? ctx->U : ctx->C;
   const Scalars* sc = useU ? ctx->sc : nullptr;
+  const bool mid = ctx->plan.mid && !full;
+  const int lmax = mid && useU ? KL - 1 : KL;    // last left level built
+  const int rmin = mid ? KL + 1 : KL;            // last right level built
   std::vector<TableLevel> L, R;
   bool ok = true;
-  // left levels 1..KL (A_{k+1} from A_k and core k), right levels d-1..KL
-  for (int k = 0; k < KL; ++k) {
+  // left levels 1..lmax (A_{k+1} from A_k and core k), right levels d-1..rmin
+  for (int k = 0; k < lmax; ++k) {
     TableLevel t{true, k == 0 ? nullptr : ctx->LT[k], ctx->ldr[k], cores + ctx->core_off[k],
                  (int)ctx->r[k], (int)ctx->n[k], (int)ctx->r[k + 1], ctx->LT[k + 1], ctx->ldr[k + 1],
-                 ctx->NLk[k + 1], (useU && k + 1 == KL) ? ctx->psiL : nullptr};
+                 ctx->NLk[k + 1], (useU && !mid && k + 1 == KL) ? ctx->psiL : nullptr};
     ok = ok && level_tab_ok(t.r0, t.nk, t.r1, t.ld_out);
     L.push_back(t);
   }
-  for (int k = d - 1; k >= KL; --k) {
+  for (int k = d - 1; k >= rmin; --k) {
     TableLevel t{false, k == d - 1 ? nullptr : ctx->RT[k + 1], ctx->ldr[k + 1],
                  cores + ctx->core_off[k], (int)ctx->r[k], (int)ctx->n[k], (int)ctx->r[k + 1],
-                 ctx->RT[k], ctx->ldr[k], ctx->NRk[k], (useU && k == KL) ? ctx->psiR : nullptr};
+                 ctx->RT[k], ctx->ldr[k], ctx->NRk[k], (useU && !mid && k == KL) ? ctx->psiR : nullptr};
     ok = ok && level_tab_ok(t.r0, t.nk, t.r1, t.ld_out);
     R.push_back(t);
   }
@@ -393,17 +433,24 @@ void enqueue_evaluate(tt_ctx* ctx, int64_t* lc) {
   grp(ctx, 0, false);
   if (ctx->obs_set && ctx->m > 0) {
     grp(ctx, 1, true);
-    SegArgs a{};
-    a.plan = &ctx->planL;
-    a.mode = kSDDMM;
-    a.ld = ctx->ldr[KL];
-    a.col = ctx->Spre;
-    a.y = ctx->ypre;
-    a.g = ctx->g;
-    a.rowtab = ctx->LT[KL];
-    a.coltab = ctx->RT[KL];
-    a.out = ctx->HL;
-    launch_seg(s, a, nullptr, lc);
+    if (ctx->plan.mid) {
+      launch_mid_passA(s, ctx->offsL, ctx->Spre, ctx->ypre, ctx->g, ctx->HL, ctx->LT[KL],
+                       ctx->ldr[KL], ctx->C + ctx->core_off[KL], (int)ctx->r[KL], (int)ctx->n[KL],
+                       (int)ctx->r[KL + 1], ctx->RT[KL + 1], ctx->ldr[KL + 1], ctx->plan.NL,
+                       ctx->plan.NR / ctx->n[KL], nullptr, lc);
+    } else {
+      SegArgs a{};
+      a.plan = &ctx->planL;
+      a.mode = kSDDMM;
+      a.ld = ctx->ldr[KL];
+      a.col = ctx->Spre;
+      a.y = ctx->ypre;
+      a.g = ctx->g;
+      a.rowtab = ctx->LT[KL];
+      a.coltab = ctx->RT[KL];
+      a.out = ctx->HL;
+      launch_seg(s, a, nullptr, lc);
+    }
     grp(ctx, 1, false);
     grp(ctx, 2, true);
     SegArgs b{};
@@ -433,7 +480,7 @@ void enqueue_update(tt_ctx* ctx, int64_t* lc) {
   launch_weights(s, ctx->h, d, ctx->n_i.data(), ctx->phi_off[d], ctx->eps_rule, ctx->eps_fixed,
                  ctx->step_rule, ctx->phi, ctx->sc, lc);
   launch_psi(s, ctx->phi, ctx->phi_off.data(), KL, d, ctx->n_i.data(), ctx->plan.NL,
-             ctx->plan.NR, ctx->psiL, ctx->psiR, ctx->sc, lc);
+             ctx->plan.NR, ctx->psiL, ctx->psiR, ctx->psiL1, ctx->psiR1, ctx->sc, lc);
   grp(ctx, 4, false);
   DenseArgs da = dense_args(ctx);
   grp(ctx, 5, true);
@@ -443,6 +490,28 @@ void enqueue_update(tt_ctx* ctx, int64_t* lc) {
   enqueue_tables(ctx, true, lc);
   grp(ctx, 6, false);
   grp(ctx, 7, true);
+  if (ctx->plan.mid) {
+    launch_scale_rows(s, ctx->RT[KL + 1], ctx->psiR1, ctx->NRk[KL + 1], ctx->ldr[KL + 1], ctx->TR1,
+                      ctx->sc, lc);
+    launch_scale_rows(s, ctx->LT[KL - 1], ctx->psiL1, ctx->NLk[KL - 1], ctx->ldr[KL - 1], ctx->TL1,
+                      ctx->sc, lc);
+    // E_KL[P] = psi_L[P] sum_j U_KL(:, j, :) Z[P][j], Z from the right U-table level KL+1
+    launch_mid_passB(s, true, ctx->offsL, ctx->Spre, ctx->g, ctx->TR1, (int)ctx->r[KL + 1],
+                     ctx->ldr[KL + 1], ctx->psiR1, ctx->phi + ctx->phi_off[KL], ctx->psiL,
+                     ctx->U + ctx->core_off[KL], (int)ctx->r[KL], (int)ctx->n[KL], (int)ctx->r[KL + 1],
+                     ctx->EL[KL], (int)ctx->r[KL], ctx->ldr[KL], ctx->plan.NL,
+                     ctx->plan.NR / ctx->n[KL], ctx->sc, lc);
+    grp(ctx, 7, false);
+    grp(ctx, 8, true);
+    // F_KL[S] = psi_R[S] sum_i Z'[S][i] U_{KL-1}(:, i, :), Z' from the left U-table level KL-1
+    launch_mid_passB(s, false, ctx->offsR, ctx->Psuf, ctx->g_suf, ctx->TL1,
+                     (int)ctx->r[KL - 1], ctx->ldr[KL - 1], ctx->psiL1,
+                     ctx->phi + ctx->phi_off[KL - 1], ctx->psiR, ctx->U + ctx->core_off[KL - 1],
+                     (int)ctx->r[KL - 1], (int)ctx->n[KL - 1], (int)ctx->r[KL], ctx->FR[KL],
+                     (int)ctx->r[KL], ctx->ldr[KL], ctx->plan.NR, ctx->plan.NL / ctx->n[KL - 1],
+                     ctx->sc, lc);
+    grp(ctx, 8, false);
+  } else {
   SegArgs a{};
   a.plan = &ctx->planL;
   a.mode = kSPMM;
@@ -466,6 +535,7 @@ void enqueue_update(tt_ctx* ctx, int64_t* lc) {
   b.out = ctx->FR[KL];
   launch_seg(s, b, ctx->sc, lc);
   grp(ctx, 8, false);
+  }
   grp(ctx, 9, true);
   {
     std::vector<BackwardLevel> BL, BR;
@@ -698,13 +768,14 @@ int tt_plan(int d, const int64_t* n, const int64_t* r, int* K_L, int64_t* N_L, i
   return TT_OK;
 }
 
-int tt_plan_blocks(int d, const int64_t* n, const int64_t* r, int* nb_L, int* nb_R) {
+int tt_plan_layout(int d, const int64_t* n, const int64_t* r, int* nb_L, int* nb_R, int* middle) {
   Plan pl;
   std::string msg;
   int rc = validate_and_plan(d, n, r, &pl, &msg);
   if (rc != TT_OK) return rc;
   if (nb_L) *nb_L = pl.nbL;
   if (nb_R) *nb_R = pl.nbR;
+  if (middle) *middle = pl.mid ? 1 : 0;
   return TT_OK;
 }
 
@@ -851,11 +922,11 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
   bool ok = A(ctx, &idx_dev, m * d, tmp) && A(ctx, &y_orig, m, tmp) && A(ctx, &kpre, m, tmp) &&
             A(ctx, &ksuf, m, tmp) && A(ctx, &ktmp, m, tmp) && A(ctx, &vals, m, tmp) &&
             A(ctx, &vals2, m, tmp) && A(ctx, &vtmp, m, tmp) && A(ctx, &inv, m, tmp) &&
-            A(ctx, &hist, hl, tmp) && A(ctx, &ctx->Spre, m, OL) && A(ctx, &ctx->ypre, m, OL) &&
-            A(ctx, &ctx->g, m, OL) && A(ctx, &ctx->sid_pre, m, OL) && A(ctx, &ctx->pos_suf, m, OL) &&
-            A(ctx, &ctx->Psuf, m, OL) && A(ctx, &ctx->sid_suf, m, OL) &&
-            A(ctx, &ctx->g_suf, m, OL) && A(ctx, &ctx->pre2suf, m, OL) &&
-            A(ctx, &ctx->offsL, NLv + 1, OL) && A(ctx, &ctx->offsR, NRv + 1, OL);
+            A(ctx, &hist, hl, tmp) && A(ctx, &ctx->Spre, m + 8, OL) && A(ctx, &ctx->ypre, m + 8, OL) &&
+            A(ctx, &ctx->g, m + 8, OL) && A(ctx, &ctx->sid_pre, m, OL) && A(ctx, &ctx->pos_suf, m, OL) &&
+            A(ctx, &ctx->Psuf, m + 8, OL) && A(ctx, &ctx->sid_suf, m, OL) &&
+            A(ctx, &ctx->g_suf, m + 8, OL) && A(ctx, &ctx->pre2suf, m, OL) &&
+            A(ctx, &ctx->offsL, NLv + 1 + 40, OL) && A(ctx, &ctx->offsR, NRv + 1 + 40, OL);
   auto cleanup = [&]() { dfree_all(ctx, tmp); };
   if (!ok) {
     cleanup();
@@ -867,14 +938,20 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
   while (((int64_t)1 << bitsS) < NR) ++bitsS;
   while (((int64_t)1 << bitsVP) < NLv) ++bitsVP;
   while (((int64_t)1 << bitsVS) < NRv) ++bitsVS;
+  if (ctx->plan.mid) {   // in-row keys (digit << shift) | rest (sort.cu) need shift + digit bits
+    auto bits = [](int64_t v) { int b = 0; while (((int64_t)1 << b) < v) ++b; return b; };
+    bitsS = std::max(bitsS, bits(NR / ctx->n[KL]) + bits(ctx->n[KL]));
+    bitsP = std::max(bitsP, bits(NL / ctx->n[KL - 1]) + bits(ctx->n[KL - 1]));
+  }
   cudaStream_t s = ctx->stream;
   int64_t lc = 0;
   if (m > 0) {
     CK(cudaMemcpyAsync(idx_dev, h_idx, (size_t)m * d * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(y_orig, h_vals, (size_t)m * sizeof(double), cudaMemcpyHostToDevice, s));
     CK(cudaMemsetAsync(&ctx->sc->index_err, 0, sizeof(int), s));
-    launch_make_keys(s, idx_dev, m, d, ctx->n_dev, KL, bitsP, bitsS, NL, NR, nbL, nbR, kpre, ksuf,
-                     vals, ctx->sc, &lc);
+    launch_make_keys(s, idx_dev, m, d, ctx->n_dev, KL, bitsP, bitsS, NL, NR, nbL, nbR,
+                     ctx->plan.mid ? (int)ctx->n[KL - 1] : 1, ctx->plan.mid ? (int)ctx->n[KL] : 1,
+                     kpre, ksuf, vals, ctx->sc, &lc);
     CK(cudaMemcpyAsync(vals2, vals, (size_t)m * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -943,7 +1020,7 @@ int tt_prgd_step(tt_ctx* ctx, double step_size) {
     ++ctx->prof_steps;
   }
   ctx->evalValid = true;
-  ctx->tablesC = true;
+  ctx->tablesC = !ctx->plan.mid;
   ++ctx->steps;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(ctx, e, "step");
@@ -959,7 +1036,7 @@ int tt_eval_at(tt_ctx* ctx, const int32_t* h_idx, int64_t count, double* h_out) 
   if (rc) return rc;
   int64_t lc = 0;
   if (!ctx->tablesC) {
-    enqueue_tables(ctx, false, &lc);
+    enqueue_tables(ctx, false, &lc, true);
     ctx->tablesC = true;
   }
   std::vector<void*> tmp;
@@ -994,7 +1071,7 @@ int tt_residual_norm(tt_ctx* ctx, double* out) {
   if (!ctx->evalValid) {
     if ((rc = run_piece(ctx, false))) return rc;
     ctx->evalValid = true;
-    ctx->tablesC = true;
+    ctx->tablesC = !ctx->plan.mid;
   }
   if ((rc = read_scalars(ctx))) return rc;
   *out = std::sqrt(ctx->sc_host->sumsq);
@@ -1106,7 +1183,7 @@ int tt_debug_get(tt_ctx* ctx, int what, int k, void* h_out, int64_t cap, int64_t
       if (!ctx->evalValid && ctx->m > 0) {
         if ((rc = run_piece(ctx, false))) return rc;
         ctx->evalValid = true;
-        ctx->tablesC = true;
+        ctx->tablesC = !ctx->plan.mid;
       }
       std::vector<double> gp(ctx->m);
       std::vector<int32_t> sp(ctx->m);

@@ -53,15 +53,26 @@ __device__ __forceinline__ double2 ld2(const double* p) {
 
 // Minimum resident CTAs per SM (register cap): measured on B200 at config 5, the SDDMM pass
 // is fastest at 4 (64 registers, no spills), the SpMM passes at 6 (40 registers).
+#ifndef PRGD_SEG_OCC_SPMM
+#define PRGD_SEG_OCC_SPMM 6
+#endif
+#ifndef PRGD_SEG_OCC_SDDMM
+#define PRGD_SEG_OCC_SDDMM 4
+#endif
+#ifndef PRGD_SEG_UNR
+#define PRGD_SEG_UNR 4
+#endif
 template <int MODE>
-struct SegOcc { static constexpr int v = MODE == kSDDMM ? 4 : (MODE == kSPMM ? 6 : 8); };
+struct SegOcc {
+  static constexpr int v = MODE == kSDDMM ? PRGD_SEG_OCC_SDDMM : (MODE == kSPMM ? PRGD_SEG_OCC_SPMM : 8);
+};
 
 template <int LPS, int MODE>
 __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Scalars* sc) {
   if (sc && sc->noop) return;
   constexpr int G = 32 / LPS;        // samples per warp step
   constexpr int STEPS = 32 / G;      // steps per 32-sample chunk (= LPS)
-  constexpr int UNR = STEPS < 4 ? STEPS : 4;
+  constexpr int UNR = STEPS < PRGD_SEG_UNR ? STEPS : PRGD_SEG_UNR;
   const int lane = threadIdx.x & 31;
   const int grp = lane / LPS, sub = lane - grp * LPS;
   const int64_t wl = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -308,9 +319,39 @@ struct PsiArgs {
 };
 
 __global__ void k_psi(const double* __restrict__ phi, PsiArgs pa, double* __restrict__ psiL,
-                      double* __restrict__ psiR, const Scalars* sc) {
+                      double* __restrict__ psiR, double* __restrict__ psiL1,
+                      double* __restrict__ psiR1, const Scalars* sc) {
   if (sc && sc->noop) return;
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  // middle-split weights: psiL1[P'] = prod_{k < KL-1} phi^{-1}, psiR1[S'] = prod_{k > KL} phi^{-1}
+  const int64_t NL1 = psiL1 ? pa.NL / pa.n[pa.KL - 1] : 0;
+  const int64_t NR1 = psiR1 ? pa.NR / pa.n[pa.KL] : 0;
+  if (e >= pa.NL + pa.NR) {
+    int64_t f = e - pa.NL - pa.NR;
+    if (f < NL1) {
+      int64_t P = f;
+      double v = 1.0;
+      for (int k = pa.KL - 2; k >= 0; --k) {
+        int64_t q = P / pa.n[k];
+        int xk = (int)(P - q * pa.n[k]);
+        P = q;
+        v /= phi[pa.phi_off[k] + xk];
+      }
+      psiL1[f] = v;
+    } else if (f < NL1 + NR1) {
+      int64_t S = f - NL1;
+      const int64_t S0 = S;
+      double v = 1.0;
+      for (int k = pa.KL + 1; k < pa.d; ++k) {
+        int64_t q = S / pa.n[k];
+        int xk = (int)(S - q * pa.n[k]);
+        S = q;
+        v /= phi[pa.phi_off[k] + xk];
+      }
+      psiR1[S0] = v;
+    }
+    return;
+  }
   if (e < pa.NL) {
     int64_t P = e;
     double v = 1.0;
@@ -493,7 +534,7 @@ void launch_weights(cudaStream_t s, const double* h, int d, const int* n_host, i
 
 void launch_psi(cudaStream_t s, const double* phi, const int64_t* phi_off_host, int KL, int d,
                 const int* n_host, int64_t NL, int64_t NR, double* psiL, double* psiR,
-                const Scalars* sc, int64_t* launches) {
+                double* psiL1, double* psiR1, const Scalars* sc, int64_t* launches) {
   PsiArgs pa;
   pa.d = d;
   pa.KL = KL;
@@ -503,7 +544,8 @@ void launch_psi(cudaStream_t s, const double* phi, const int64_t* phi_off_host, 
   }
   pa.NL = NL;
   pa.NR = NR;
-  k_psi<<<blocks_for(NL + NR, 256), 256, 0, s>>>(phi, pa, psiL, psiR, sc);
+  const int64_t extra = (psiL1 ? NL / n_host[KL - 1] : 0) + (psiR1 ? NR / n_host[KL] : 0);
+  k_psi<<<blocks_for(NL + NR + extra, 256), 256, 0, s>>>(phi, pa, psiL, psiR, psiL1, psiR1, sc);
   ++*launches;
 }
 

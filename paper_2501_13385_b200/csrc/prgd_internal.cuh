@@ -89,8 +89,8 @@ struct DenseArgs {
 // sort.cu
 void launch_make_keys(cudaStream_t s, const int32_t* idx, int64_t m, int d, const int* n_dev,
                       int KL, int bitsP, int bitsS, int64_t NL, int64_t NR, int nbL, int nbR,
-                      uint64_t* kpre, uint64_t* ksuf, uint32_t* vals, Scalars* sc,
-                      int64_t* launches);
+                      int nsubL, int nsubR, uint64_t* kpre, uint64_t* ksuf, uint32_t* vals,
+                      Scalars* sc, int64_t* launches);
 void radix_sort_pairs(cudaStream_t s, uint64_t* keys, uint32_t* vals, uint64_t* keys_tmp,
                       uint32_t* vals_tmp, int64_t m, int bits, int* hist_buf, int64_t hist_len,
                       uint64_t** keys_out, uint32_t** vals_out, int64_t* launches);
@@ -180,6 +180,20 @@ void launch_backward_levels(cudaStream_t s, const std::vector<BackwardLevel>& le
                             const Scalars* sc, int64_t* lc);
 void levels_init();
 
+// passes_mid.cu: passes re-associated through the middle cores (plan.mid).
+void launch_mid_passA(cudaStream_t s, const int64_t* offs, const int32_t* key, const double* y,
+                      double* g, double* H, const double* A, int lda, const double* core, int rK,
+                      int nK, int rK1, const double* Bt, int ldb, int64_t N, int64_t N1,
+                      const Scalars* sc, int64_t* launches);
+void launch_mid_passB(cudaStream_t s, bool left, const int64_t* offs, const int32_t* key,
+                      const double* x, const double* T, int rt, int ldt, const double* wr,
+                      const double* phij, const double* rowscale, const double* core, int r0,
+                      int nmid, int r1, double* out, int rout, int ldo, int64_t N, int64_t N1,
+                      const Scalars* sc, int64_t* launches);
+void launch_scale_rows(cudaStream_t s, const double* in, const double* f, int64_t rows, int ld,
+                       double* out, const Scalars* sc, int64_t* launches);
+void passes_mid_init();
+
 // passes.cu
 enum SegMode { kSDDMM = 0, kGSQ = 1, kSPMM = 2 };
 struct SegArgs {
@@ -205,9 +219,10 @@ void launch_marginals(cudaStream_t s, const double* H, int64_t N, int nmodes, co
 void launch_weights(cudaStream_t s, const double* h, int d, const int* n_host, int64_t nsum,
                     int eps_rule, double eps_fixed, int step_rule, double* phi, Scalars* sc,
                     int64_t* launches);
+// psiL1 / psiR1 (middle-split weights over N_L / n_{KL-1} and N_R / n_KL rows) may be null.
 void launch_psi(cudaStream_t s, const double* phi, const int64_t* phi_off_host, int KL, int d,
                 const int* n_host, int64_t NL, int64_t NR, double* psiL, double* psiR,
-                const Scalars* sc, int64_t* launches);
+                double* psiL1, double* psiR1, const Scalars* sc, int64_t* launches);
 void launch_eval_queries(cudaStream_t s, const int32_t* idx, int64_t count, int d, const int* n_host,
                          int KL, const double* tabL, const double* tabR, int ld, int rb,
                          double* out, Scalars* sc, int64_t* launches);

@@ -52,8 +52,8 @@ def test_bucketing_bit_exact(pkg, cfg, m, kw):
     ctx = context(pkg, pr, y, init)
     KL, NL, NR = pkg.plan(pr.n, pr.r)
     assert KL == oracle.split_point(pr.n)
-    nbL, nbR = pkg.plan_blocks(pr.n, pr.r)
-    o = oracle.stable_order(pr.idx, pr.n, KL, nbL, nbR)
+    nbL, nbR, mid = pkg.plan_layout(pr.n, pr.r)
+    o = oracle.stable_order(pr.idx, pr.n, KL, nbL, nbR, middle=mid)
     assert np.array_equal(ctx.debug("perm_pre"), o["perm_pre"].astype(np.int32))
     assert np.array_equal(ctx.debug("perm_suf"), o["perm_suf"].astype(np.int32))
     assert np.array_equal(ctx.debug("offs_l"), o["offs_L"].astype(np.int64))

@@ -412,3 +412,22 @@ def test_blocked_stable_order_matches_python_sort():
         vp = [(S(s) * nbL // NR) * NL + P(s) for s in pre]
         for v in range(nbL * NL):
             assert o["offs_L"][v + 1] - o["offs_L"][v] == vp.count(v)
+
+
+def test_middle_stable_order_matches_python_sort():
+    # Middle-split in-row order: prefix rows sorted by (x_{K_L+1}, S'),
+    # suffix rows by (x_{K_L}, P'), stable; 1-based modes as in the paper.
+    rng = np.random.default_rng(16)
+    n = (3, 4, 5, 2)
+    m = 300
+    idx = np.stack([rng.integers(0, nk, m) for nk in n], axis=1).astype(np.int32)
+    KL = 2
+    o = oracle.stable_order(idx, n, KL, middle=True)
+
+    def P(s):
+        return int(idx[s, 0]) * n[1] + int(idx[s, 1])
+
+    pre = sorted(range(m), key=lambda s: (P(s), int(idx[s, 2]), int(idx[s, 3]), s))
+    suf = sorted(range(m), key=lambda s: (int(idx[s, 3]) * n[2] + int(idx[s, 2]),
+                                          int(idx[s, 1]), int(idx[s, 0]), s))
+    assert list(o["perm_pre"]) == pre and list(o["perm_suf"]) == suf
