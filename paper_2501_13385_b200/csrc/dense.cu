@@ -1293,7 +1293,7 @@ bool round_cluster_ok(int d, const int* r) {
 
 void launch_dense_orth(cudaStream_t s, const DenseArgs& a, int64_t* launches) {
   const size_t bytes = (size_t)a.smem_doubles * sizeof(double);
-  k_dense_orth<<<1, kDenseThreads, bytes, s>>>(a);
+  if (!(a.clw && launch_orth_cs(s, a, bytes))) k_dense_orth<<<1, kDenseThreads, bytes, s>>>(a);
   ++*launches;
 }
 
