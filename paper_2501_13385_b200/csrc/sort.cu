@@ -86,31 +86,68 @@ __global__ void k_rs_hist(const uint64_t* __restrict__ keys, int64_t m, int shif
     hist[(int64_t)i * nblocks + blockIdx.x] = cnt[i];
 }
 
-// Exclusive scan of hist[0..len) in (digit, block) order; one block.
-__global__ void k_rs_scan(int* __restrict__ hist, int64_t len) {
-  __shared__ long long tot[1024];
-  int64_t chunk = (len + blockDim.x - 1) / blockDim.x;
-  int64_t b = threadIdx.x * chunk;
-  int64_t e = b + chunk < len ? b + chunk : len;
+// Exclusive scan of hist[0..len) in (digit, block) order, in three passes: segment sums
+// (kScanSeg elements per block, coalesced), a one-block scan of the segment sums, and the
+// in-order scan of each segment staged in shared memory.
+constexpr int kScanSeg = 8192;
+constexpr int kScanThreads = 256;
+constexpr int kScanPer = kScanSeg / kScanThreads;   // 32 contiguous elements per thread
+
+__global__ void k_scan_sums(const int* __restrict__ hist, int64_t len, long long* __restrict__ bsum) {
+  __shared__ long long red[kScanThreads];
+  const int64_t base = (int64_t)blockIdx.x * kScanSeg;
   long long s = 0;
-  for (int64_t i = b; i < e; ++i) s += hist[i];
+  for (int i = threadIdx.x; i < kScanSeg; i += kScanThreads)
+    if (base + i < len) s += hist[base + i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = kScanThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bsum[blockIdx.x] = red[0];
+}
+
+__global__ void k_scan_top(long long* __restrict__ bsum, int nb) {
+  if (threadIdx.x == 0) {
+    long long run = 0;
+    for (int i = 0; i < nb; ++i) {
+      const long long t = bsum[i];
+      bsum[i] = run;
+      run += t;
+    }
+  }
+}
+
+__global__ void k_scan_apply(int* __restrict__ hist, int64_t len, const long long* __restrict__ bsum) {
+  __shared__ int seg[kScanSeg];
+  __shared__ long long tot[kScanThreads];
+  const int64_t base = (int64_t)blockIdx.x * kScanSeg;
+  for (int i = threadIdx.x; i < kScanSeg; i += kScanThreads)
+    seg[i] = base + i < len ? hist[base + i] : 0;
+  __syncthreads();
+  long long s = 0;
+  for (int k = 0; k < kScanPer; ++k) s += seg[threadIdx.x * kScanPer + k];
   tot[threadIdx.x] = s;
   __syncthreads();
   if (threadIdx.x == 0) {
-    long long run = 0;
-    for (int i = 0; i < (int)blockDim.x; ++i) {
-      long long t = tot[i];
+    long long run = bsum[blockIdx.x];
+    for (int i = 0; i < kScanThreads; ++i) {
+      const long long t = tot[i];
       tot[i] = run;
       run += t;
     }
   }
   __syncthreads();
   long long run = tot[threadIdx.x];
-  for (int64_t i = b; i < e; ++i) {
-    int v = hist[i];
-    hist[i] = (int)run;
+  for (int k = 0; k < kScanPer; ++k) {
+    const int v = seg[threadIdx.x * kScanPer + k];
+    seg[threadIdx.x * kScanPer + k] = (int)run;
     run += v;
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kScanSeg; i += kScanThreads)
+    if (base + i < len) hist[base + i] = seg[i];
 }
 
 // Stable scatter: within a tile, warp w owns items [w*512, (w+1)*512) and walks them
@@ -208,7 +245,8 @@ inline unsigned grid_for(int64_t n, int threads) {
 int64_t radix_hist_len(int64_t m) {
   int64_t nb = (m + kRsTile - 1) / kRsTile;
   if (nb < 1) nb = 1;
-  return 256 * nb;
+  const int64_t len = 256 * nb;
+  return len + 2 + 2 * ((len + kScanSeg - 1) / kScanSeg + 1);   // + segment sums (int64)
 }
 
 void launch_make_keys(cudaStream_t s, const int32_t* idx, int64_t m, int d, const int* n_dev,
@@ -233,7 +271,15 @@ void radix_sort_pairs(cudaStream_t s, uint64_t* keys, uint32_t* vals, uint64_t* 
     (void)hist_len;
     for (int shift = 0; shift < bits; shift += 8) {
       k_rs_hist<<<(unsigned)nblocks, kRsThreads, 0, s>>>(kin, m, shift, hist, nblocks);
-      k_rs_scan<<<1, 1024, 0, s>>>(hist, 256 * nblocks);
+      {
+        const int64_t len = 256 * nblocks;
+        const int nb = (int)((len + kScanSeg - 1) / kScanSeg);
+        long long* bsum = reinterpret_cast<long long*>(hist + len + (len & 1));
+        k_scan_sums<<<nb, kScanThreads, 0, s>>>(hist, len, bsum);
+        k_scan_top<<<1, 32, 0, s>>>(bsum, nb);
+        k_scan_apply<<<nb, kScanThreads, 0, s>>>(hist, len, bsum);
+        *launches += 2;
+      }
       k_rs_scatter<<<(unsigned)nblocks, kRsThreads, 0, s>>>(kin, vin, ko, vo, m, shift, hist,
                                                             nblocks);
       *launches += 3;
