@@ -413,6 +413,176 @@ __global__ void __launch_bounds__(kMT, 1) k_mid_spmm(MidB p, const Scalars* sc) 
   }
 }
 
+// ---------------------------------------------------------------- register-only variants
+// The per-row state stays in registers (no shared-memory W / Z rows), so the number of rows
+// in flight is bounded by registers, not by shared memory: an 8-lane group owns a row (lane
+// l holds entries 2l, 2l+1 of every r-vector), W[P][j] = A_K[P] C_K(:, j, :) is formed once
+// per run of equal j (16 x 16 matvec from the core staged in shared memory) and, for pass B,
+// the run sum Z_j is folded into the row's output at the run's end, E += U_K(:, j, :) Z_j.
+
+// Pass A: shared memory holds Cs[a][j][c] (c fastest, ldb wide).
+__global__ void __launch_bounds__(kMT, 2) k_mid_sddmm_r(MidA p, const Scalars* sc) {
+  if (sc && sc->noop) return;
+  extern __shared__ __align__(16) double sm[];
+  const int K = p.rK, nK = p.nK, ldb = p.ldb;
+  double* Cs = sm;                                        // [K][nK][ldb]
+  for (int t = threadIdx.x; t < K * nK * ldb; t += blockDim.x) {
+    const int c = t % ldb, aj = t / ldb;
+    const int j = aj % nK, a = aj / nK;
+    Cs[t] = c < p.rK1 ? p.core[((int64_t)a * nK + j) * p.rK1 + c] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, sub = lane & 7, gbase = lane & 24;
+  const unsigned gmask = 0xffu << gbase;
+  const bool act = 2 * sub < ldb;
+  const int sh = p.shift, smask = (1 << sh) - 1;
+  const int64_t ngrp = (int64_t)gridDim.x * (kMT / 8);
+  for (int64_t P = (int64_t)blockIdx.x * (kMT / 8) + (threadIdx.x >> 3); P < p.N; P += ngrp) {
+    // A_K[P] replicated in the group's registers
+    double av[16];
+    {
+      const double2 mine = (2 * sub < p.lda && 2 * sub < 16)
+                               ? __ldg(reinterpret_cast<const double2*>(p.A + P * p.lda) + sub)
+                               : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        av[2 * q] = __shfl_sync(gmask, mine.x, gbase + q);
+        av[2 * q + 1] = __shfl_sync(gmask, mine.y, gbase + q);
+      }
+    }
+    const int64_t b = p.offs[P], e = p.offs[P + 1];
+    int jcur = -1;
+    double2 wv = make_double2(0.0, 0.0);
+    double acc = 0.0;
+    for (int64_t c0 = b; c0 < e; c0 += 8) {
+      const int nc = (int)(e - c0 < 8 ? e - c0 : 8);
+      const int kv = sub < nc ? p.key[c0 + sub] : 0;
+      const double yv = sub < nc ? p.y[c0 + sub] : 0.0;
+      double2 bv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int ku = __shfl_sync(gmask, kv, gbase + u);
+        bv[u] = make_double2(0.0, 0.0);
+        if (u < nc && act)
+          bv[u] = __ldg(reinterpret_cast<const double2*>(p.Bt + (int64_t)(ku & smask) * ldb) + sub);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (u >= nc) break;
+        const int j = __shfl_sync(gmask, kv, gbase + u) >> sh;
+        if (j != jcur) {
+          jcur = j;
+          double wx = 0.0, wy = 0.0;
+          if (act) {
+            const double* cj = Cs + (int64_t)j * ldb + 2 * sub;
+#pragma unroll
+            for (int a = 0; a < 16; ++a)
+              if (a < K) {
+                const double2 c = *reinterpret_cast<const double2*>(cj + (int64_t)a * nK * ldb);
+                wx = fma(av[a], c.x, wx);
+                wy = fma(av[a], c.y, wy);
+              }
+          }
+          wv = make_double2(wx, wy);
+        }
+        double part = fma(wv.x, bv[u].x, wv.y * bv[u].y);
+        part += __shfl_xor_sync(gmask, part, 4);
+        part += __shfl_xor_sync(gmask, part, 2);
+        part += __shfl_xor_sync(gmask, part, 1);
+        const double gv = part - __shfl_sync(gmask, yv, gbase + u);
+        if (sub == 0) p.g[c0 + u] = gv;
+        acc = fma(gv, gv, acc);
+      }
+    }
+    if (sub == 0) p.H[P] = acc;
+  }
+}
+
+// Pass B: shared memory holds the core as Us[j][x][o] (o fastest, ro wide): left
+// Us[j][c][i] = U[i][j][c], right Us[i][a][c] = U[a][i][c], and 1/phi of the middle mode.
+__global__ void __launch_bounds__(kMT, 2) k_mid_spmm_r(MidB p, const Scalars* sc) {
+  if (sc && sc->noop) return;
+  extern __shared__ __align__(16) double sm[];
+  const int nmid = p.nmid, ldt = p.ldt;
+  const int ro = (p.ldo + 1) & ~1;
+  double* Us = sm;                                  // [nmid][ldt][ro]
+  double* phinv = Us + (int64_t)nmid * ldt * ro;
+  for (int t = threadIdx.x; t < nmid * ldt * ro; t += blockDim.x) {
+    const int o = t % ro, jx = t / ro;
+    const int x = jx % ldt, j = jx / ldt;
+    double v = 0.0;
+    if (o < p.rout && x < p.rt) {
+      if (p.left) v = p.core[((int64_t)o * nmid + j) * p.r1 + x];   // U[o][j][x]
+      else v = p.core[((int64_t)x * nmid + j) * p.r1 + o];          // U[x][j][o]
+    }
+    Us[t] = v;
+  }
+  for (int t = threadIdx.x; t < nmid; t += blockDim.x) phinv[t] = 1.0 / p.phij[t];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, sub = lane & 7, gbase = lane & 24;
+  const unsigned gmask = 0xffu << gbase;
+  const bool act = 2 * sub < ldt;          // this lane holds table entries 2 sub, 2 sub + 1
+  const bool oact = 2 * sub < ro;          // ... and output entries 2 sub, 2 sub + 1
+  const int smask = (1 << p.shift) - 1;
+  const int64_t ngrp = (int64_t)gridDim.x * (kMT / 8);
+  for (int64_t row = (int64_t)blockIdx.x * (kMT / 8) + (threadIdx.x >> 3); row < p.N; row += ngrp) {
+    const int64_t b = p.offs[row], e = p.offs[row + 1];
+    int jcur = -1;
+    double2 z = make_double2(0.0, 0.0), eo = make_double2(0.0, 0.0);
+    auto fold = [&](int j) {           // eo += U(:, j, :) z  (z: the run sum, 2 per lane)
+      double zv[16];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        zv[2 * q] = __shfl_sync(gmask, z.x, gbase + q);
+        zv[2 * q + 1] = __shfl_sync(gmask, z.y, gbase + q);
+      }
+      if (oact) {
+        const double* uj = Us + (int64_t)j * ldt * ro + 2 * sub;
+#pragma unroll
+        for (int x = 0; x < 16; ++x)
+          if (x < ldt) {
+            const double2 u = *reinterpret_cast<const double2*>(uj + x * ro);
+            eo.x = fma(u.x, zv[x], eo.x);
+            eo.y = fma(u.y, zv[x], eo.y);
+          }
+      }
+    };
+    for (int64_t c0 = b; c0 < e; c0 += 8) {
+      const int nc = (int)(e - c0 < 8 ? e - c0 : 8);
+      const int kv = sub < nc ? p.key[c0 + sub] : 0;
+      const double xv = sub < nc ? p.x[c0 + sub] : 0.0;
+      double2 tv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int ku = __shfl_sync(gmask, kv, gbase + u);
+        tv[u] = make_double2(0.0, 0.0);
+        if (u < nc && act)
+          tv[u] = __ldg(reinterpret_cast<const double2*>(p.T + (int64_t)(ku & smask) * ldt) + sub);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (u >= nc) break;
+        const int j = __shfl_sync(gmask, kv, gbase + u) >> p.shift;
+        if (j != jcur) {
+          if (jcur >= 0) fold(jcur);
+          jcur = j;
+          z = make_double2(0.0, 0.0);
+        }
+        const double w = __shfl_sync(gmask, xv, gbase + u) * phinv[j];
+        z.x = fma(w, tv[u].x, z.x);
+        z.y = fma(w, tv[u].y, z.y);
+      }
+    }
+    if (jcur >= 0) fold(jcur);
+    if (oact) {
+      const double f = p.rowscale ? p.rowscale[row] : 1.0;
+      const int o = 2 * sub;
+      if (o < p.ldo) p.out[row * p.ldo + o] = o < p.rout ? eo.x * f : 0.0;
+      if (o + 1 < p.ldo) p.out[row * p.ldo + o + 1] = o + 1 < p.rout ? eo.y * f : 0.0;
+    }
+  }
+}
+
 __global__ void k_scale_rows(const double* __restrict__ in, const double* __restrict__ f, int64_t rows,
                              int ld, double* __restrict__ out, const Scalars* sc) {
   if (sc && sc->noop) return;
@@ -447,6 +617,14 @@ void launch_mid_passA(cudaStream_t s, const int64_t* offs, const int32_t* key, c
                        2 * stage) * sizeof(double);
   const int64_t ntiles = (N + kTR - 1) / kTR;
   const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sms_mid());
+  const size_t smem_r = (size_t)rK * nK * ldb * sizeof(double);
+  const int64_t ngr = (N + kMT / 8 - 1) / (kMT / 8);
+  const int grid_r = (int)std::min<int64_t>(ngr, (int64_t)sms_mid() * 2);
+  if (rK <= 16 && ldb <= 16 && lda <= 16) {
+    k_mid_sddmm_r<<<std::max(grid_r, 1), kMT, smem_r, s>>>(p, sc);
+    ++*launches;
+    return;
+  }
   k_mid_sddmm<<<std::max(grid, 1), kMT, smem, s>>>(p, sc);
   ++*launches;
 }
@@ -467,6 +645,15 @@ void launch_mid_passB(cudaStream_t s, bool left, const int64_t* offs, const int3
                        2 * stage) * sizeof(double);
   const int64_t ntiles = (N + kTR - 1) / kTR;
   const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sms_mid());
+  const int ro = (ldo + 1) & ~1;
+  const size_t smem_r = ((size_t)nmid * ldt * ro + nmid) * sizeof(double);
+  const int64_t ngr = (N + kMT / 8 - 1) / (kMT / 8);
+  const int grid_r = (int)std::min<int64_t>(ngr, (int64_t)sms_mid() * 2);
+  if (ldt <= 16 && ro <= 16) {
+    k_mid_spmm_r<<<std::max(grid_r, 1), kMT, smem_r, s>>>(p, sc);
+    ++*launches;
+    return;
+  }
   k_mid_spmm<<<std::max(grid, 1), kMT, smem, s>>>(p, sc);
   ++*launches;
 }
@@ -479,6 +666,8 @@ void launch_scale_rows(cudaStream_t s, const double* in, const double* f, int64_
 
 void passes_mid_init() {
   cudaFuncSetAttribute(k_mid_sddmm, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_mid_sddmm_r, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  cudaFuncSetAttribute(k_mid_spmm_r, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   cudaFuncSetAttribute(k_mid_spmm, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
