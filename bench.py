@@ -130,9 +130,18 @@ def run_ours(args, rank, ws, dist):
 
     dev = torch.cuda.current_device()
     t0 = time.perf_counter()
-    pr = synth.make_problem(args.config, seed=synth.BASE_SEED + args.config + 1000 * rank,
-                            m=args.m)
+    if ws > 1:
+        # sharded Omega: same truth and init on every rank, disjoint samples
+        pr = synth.make_problem(args.config, m=args.m, rank=rank, world=ws)
+    else:
+        pr = synth.make_problem(args.config, m=args.m)
     t_gen = time.perf_counter() - t0
+    m_global = pr.m
+    if dist is not None:
+        t = torch.tensor([float(pr.m)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t)
+        m_global = int(round(float(t.item())))
+    ar = pkg.torch_allreduce() if dist is not None else None
     # observations: T*(Omega) through the library (tt_eval_at), plus seeded noise
     tctx = pkg.TTContext(pr.n, pr.r)
     tctx.set_cores(pr.truth)
@@ -143,6 +152,8 @@ def run_ours(args, rank, ws, dist):
     KL, NL, NR = pkg.plan(pr.n, pr.r)
 
     ctx = pkg.TTContext(pr.n, pr.r)
+    if ar is not None:
+        ctx.set_allreduce(ar, m_global)
     stream = ctx.stream
     t1 = time.perf_counter()
     ctx.set_observations(pr.idx, y)
@@ -196,14 +207,15 @@ def run_ours(args, rank, ws, dist):
     ctx.close()
 
     out = dict(pr=pr, y=y, init=init, KL=KL, NL=NL, NR=NR, ms=ms_max, launches=launches,
+               m_global=m_global,
                clocks=clocks, prof=prof, t_gen=t_gen, t_setobs=t_setobs, res0=res0, res1=res1,
                dense_diag=dense_diag)
     if not args.no_e2e:
-        out["e2e"] = run_e2e(args, pr, y, init)
+        out["e2e"] = run_e2e(args, pr, y, init, ar, m_global, dist)
     return out
 
 
-def run_e2e(args, pr, y, init):
+def run_e2e(args, pr, y, init, ar=None, m_global=None, dist=None):
     """Same metric through the public API from pinned host buffers: upload + bucket
     Omega, set cores, K steps each followed by a residual read (D2H), cores out."""
     import torch
@@ -213,8 +225,12 @@ def run_e2e(args, pr, y, init):
     cores_p = [torch.from_numpy(np.ascontiguousarray(c)).pin_memory() for c in init]
     K = args.steps
     torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
     t0 = time.perf_counter()
     ctx = pkg.TTContext(pr.n, pr.r)
+    if ar is not None:
+        ctx.set_allreduce(ar, m_global)
     ctx.set_observations(idx_p.numpy(), y_p.numpy())
     for k, c in enumerate(cores_p):
         ctx.set_core(k, c.numpy())
@@ -224,10 +240,15 @@ def run_e2e(args, pr, y, init):
     cores = ctx.get_cores()
     t1 = time.perf_counter()
     ctx.close()
+    if dist is not None:   # whole-job time = slowest rank
+        t = torch.tensor([t1 - t0], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t0, t1 = 0.0, float(t.item())
     core_bytes = sum(c.nbytes for c in cores)
     h2d = idx_p.numel() * 4 + y_p.numel() * 8 + core_bytes
     d2h = K * 8 + core_bytes
-    return {"value": K / (t1 - t0), "unit": UNIT, "h2d_bytes_per_step": int(h2d / K),
+    ws = dist.get_world_size() if dist is not None else 1
+    return {"value": ws * K / (t1 - t0), "unit": UNIT, "h2d_bytes_per_step": int(h2d / K),
             "d2h_bytes_per_step": int(d2h / K), "wall_s": t1 - t0}
 
 
@@ -314,7 +335,7 @@ def main():
             "group_ms": {k: round(v, 4) for k, v in per.items()},
             "dominant_group": dom}
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and ws == 1:
         ms_ = min(args.cpu_sample, m)
         times = oracle_sample(pr, r["y"], r["init"], ms_, steps=1)
         t = times[0]
@@ -331,8 +352,11 @@ def main():
                                f"|Omega|={m}, noise {pr.noise_sigma} {pr.noise_kind}",
                    "d": pr.d, "n": list(pr.n), "r": list(pr.r), "m": m, "K_L": r["KL"],
                    "l2": "inputs larger than L2 (Omega arrays + tables > 126 MB); no flush",
-                   "parallelism": "replicas" if ws > 1 else "single"},
-        "entries_per_s": round(value * m, 1),
+                   "m_global": r["m_global"],
+                   "parallelism": (f"sharded Omega over {ws} GPUs (h and Y all-reduced, NCCL); "
+                                   "value = N x iter/s of the N-times-larger problem") if ws > 1
+                                  else "single"},
+        "entries_per_s": round(r["m_global"] * args.steps / (r["ms"] / 1e3), 1),
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": r.get("e2e"),

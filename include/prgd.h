@@ -145,6 +145,22 @@ PRGD_API int tt_sync(tt_ctx* ctx);
 /* Message for the last non-OK status on ctx (static "..." string for NULL ctx). */
 PRGD_API const char* tt_last_error(const tt_ctx* ctx);
 
+/* ------------------------------------------------------------------ sharded (multi-GPU) */
+
+/* Sharded mode: Omega is split over ranks, one context per
+ * rank (one GPU each) holding the same cores and its own observations; every h_{k,j}
+ * and every contraction Y_k is a sum over samples, so a step
+ * all-reduces exactly two buffers -- h (sum_k n_k doubles) after pass A and Y (sum_k
+ * r_k n_k r_{k+1} doubles) after pass B -- and replicates the small dense work, which keeps
+ * the iterates identical on all ranks.  fn(buf, count, stream, user) must enqueue an in-place
+ * fp64 sum over ranks of the DEVICE buffer buf[count] on `stream` (a cudaStream_t, e.g. NCCL
+ * through torch.distributed) and return; it is called from the host thread inside
+ * tt_prgd_step / tt_residual_norm.  m_global = |Omega| summed over ranks (p = m_global /
+ * prod(n), reading R3).  Must be called before tt_set_observations (TT_ERR_STATE); fn = NULL
+ * returns to the single-rank mode. */
+typedef void (*tt_allreduce_fn)(double* buf, int64_t count, void* stream, void* user);
+PRGD_API int tt_set_allreduce(tt_ctx* ctx, tt_allreduce_fn fn, void* user, int64_t m_global);
+
 /* ------------------------------------------------------------------ introspection */
 
 /* Host-only planning (no device needed): validates (d, n, r) like tt_create and

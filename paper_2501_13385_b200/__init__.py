@@ -44,6 +44,7 @@ class _Stats(ctypes.Structure):
 
 ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
 FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p)
 
 _lib = None
 
@@ -77,6 +78,7 @@ def load() -> ctypes.CDLL:
                                    i64p, i64p]),
         "tt_plan_layout": (ctypes.c_int, [ctypes.c_int, i64p, i64p, ctypes.POINTER(ctypes.c_int),
                                           ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
+        "tt_set_allreduce": (ctypes.c_int, [P, ALLREDUCE_FN, P, ctypes.c_int64]),
         "tt_get_stats": (ctypes.c_int, [P, ctypes.POINTER(_Stats)]),
         "tt_set_profiling": (ctypes.c_int, [P, ctypes.c_int]),
         "tt_get_profile": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_double), ctypes.c_int,
@@ -176,6 +178,17 @@ class TTContext:
         self._check(self.lib.tt_set_allocator(self._h, fa, ff, None), "tt_set_allocator")
         self._check(self.lib.tt_set_stream(self._h, ctypes.c_void_p(stream.cuda_stream)),
                     "tt_set_stream")
+
+    # -- sharded (multi-GPU) mode: Omega split over ranks, h and Y all-reduced (tt_set_allreduce)
+    def set_allreduce(self, fn, m_global: int):
+        """fn(buffer_ptr, count, stream_ptr): in-place fp64 sum over ranks of a device buffer,
+        enqueued on the given CUDA stream.  fn=None returns to single-rank mode."""
+        if fn is None:
+            self._check(self.lib.tt_set_allreduce(self._h, ALLREDUCE_FN(), None, 0), "tt_set_allreduce")
+            return
+        cb = ALLREDUCE_FN(lambda buf, count, stream, _user: fn(buf, count, stream))
+        self._keep.append(cb)
+        self._check(self.lib.tt_set_allreduce(self._h, cb, None, int(m_global)), "tt_set_allreduce")
 
     def _check(self, rc, what):
         if rc != TT_OK:
@@ -296,3 +309,26 @@ class TTContext:
         if rc != TT_OK or cnt.value == 0:
             return 0
         return int(offs[-1])
+
+
+def torch_allreduce(group=None):
+    """An all-reduce callback for TTContext.set_allreduce built on torch.distributed (NCCL on
+    GPUs): wraps the library's device buffer as a tensor (zero copy) and sums it in place
+    over the process group on the library's stream."""
+    import torch
+    import torch.distributed as dist
+
+    class _Buf:
+        def __init__(self, ptr, count):
+            self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8",
+                                             "data": (int(ptr), False), "version": 3,
+                                             "strides": None}
+
+    def fn(ptr, count, stream_ptr):
+        if count <= 0:
+            return
+        t = torch.as_tensor(_Buf(ptr, count), device="cuda")
+        with torch.cuda.stream(torch.cuda.ExternalStream(int(stream_ptr))):
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+    return fn

@@ -197,6 +197,12 @@ struct tt_ctx {
   double eps_fixed = 0.0;
 
   cudaGraphExec_t gA = nullptr, gB = nullptr;
+  // sharded (multi-rank) mode: Omega is split over ranks; h and Y are all-reduced
+  cudaGraphExec_t gA1 = nullptr, gB1 = nullptr, gB2 = nullptr;
+  int64_t nA1 = 0, nB1 = 0, nB2 = 0;
+  tt_allreduce_fn allreduce = nullptr;
+  void* ar_user = nullptr;
+  int64_t m_global = -1;
   int64_t nA = 0, nB = 0;
   int64_t launches = 0, steps = 0;
 
@@ -256,6 +262,10 @@ void drop_graphs(tt_ctx* ctx) {
   if (ctx->gA) cudaGraphExecDestroy(ctx->gA);
   if (ctx->gB) cudaGraphExecDestroy(ctx->gB);
   ctx->gA = ctx->gB = nullptr;
+  for (cudaGraphExec_t* g : {&ctx->gA1, &ctx->gB1, &ctx->gB2}) {
+    if (*g) cudaGraphExecDestroy(*g);
+    *g = nullptr;
+  }
 }
 
 int ensure_base(tt_ctx* ctx) {
@@ -425,13 +435,13 @@ void enqueue_tables(tt_ctx* ctx, bool useU, int64_t* lc, bool full = false) {
                        t.rowscale, sc, lc);
 }
 
-void enqueue_evaluate(tt_ctx* ctx, int64_t* lc) {
+void enqueue_evaluate(tt_ctx* ctx, int64_t* lc, bool with_sumsq = true) {
   const int d = ctx->d, KL = ctx->plan.KL;
   cudaStream_t s = ctx->stream;
   grp(ctx, 0, true);
   enqueue_tables(ctx, false, lc);
   grp(ctx, 0, false);
-  if (ctx->obs_set && ctx->m > 0) {
+  if (ctx->obs_set && (ctx->m > 0 || ctx->allreduce)) {
     grp(ctx, 1, true);
     if (ctx->plan.mid) {
       launch_mid_passA(s, ctx->offsL, ctx->Spre, ctx->ypre, ctx->g, ctx->HL, ctx->LT[KL],
@@ -468,14 +478,23 @@ void enqueue_evaluate(tt_ctx* ctx, int64_t* lc) {
                      ctx->margp, lc);
     launch_marginals(s, ctx->HR, ctx->plan.NR * ctx->plan.nbR, d - KL, ctx->n_i.data() + KL, false,
                      ctx->h + ctx->phi_off[KL], ctx->margp + 32 * ctx->phi_off[KL], lc);
-    launch_gather_sq_sum(s, ctx->h, ctx->n_i[0], ctx->sc, lc);
+    if (with_sumsq) launch_gather_sq_sum(s, ctx->h, ctx->n_i[0], ctx->sc, lc);
     grp(ctx, 3, false);
   }
 }
 
-void enqueue_update(tt_ctx* ctx, int64_t* lc) {
+// part 0: the whole update; part 1: up to the contractions Y (pass B + backward);
+// part 2: projection + rank-2r assembly + rounding (sharded mode all-reduces Y between).
+void enqueue_update(tt_ctx* ctx, int64_t* lc, int part = 0) {
   const int d = ctx->d, KL = ctx->plan.KL;
   cudaStream_t s = ctx->stream;
+  if (part == 2) {
+    DenseArgs da = dense_args(ctx);
+    grp(ctx, 10, true);
+    launch_dense_round(ctx->stream, da, lc);
+    grp(ctx, 10, false);
+    return;
+  }
   grp(ctx, 4, true);
   launch_weights(s, ctx->h, d, ctx->n_i.data(), ctx->phi_off[d], ctx->eps_rule, ctx->eps_fixed,
                  ctx->step_rule, ctx->phi, ctx->sc, lc);
@@ -584,19 +603,32 @@ void enqueue_update(tt_ctx* ctx, int64_t* lc) {
     }
   }
   grp(ctx, 9, false);
+  if (part == 1) return;
   grp(ctx, 10, true);
   launch_dense_round(s, da, lc);
   grp(ctx, 10, false);
 }
 
 // Run a piece either as a captured graph (cached) or directly (profiling).
-int run_piece(tt_ctx* ctx, bool update) {
-  cudaGraphExec_t* ge = update ? &ctx->gB : &ctx->gA;
-  int64_t* nl = update ? &ctx->nB : &ctx->nA;
+// Pieces: 0 evaluate (+ sum g^2), 1 update, 2 evaluate without sum g^2, 3 update up to Y,
+// 4 rounding.  Each runs as a captured CUDA graph (cached), or directly when profiling.
+int run_piece(tt_ctx* ctx, int piece) {
+  cudaGraphExec_t* slots[5] = {&ctx->gA, &ctx->gB, &ctx->gA1, &ctx->gB1, &ctx->gB2};
+  int64_t* counts[5] = {&ctx->nA, &ctx->nB, &ctx->nA1, &ctx->nB1, &ctx->nB2};
+  cudaGraphExec_t* ge = slots[piece];
+  int64_t* nl = counts[piece];
+  auto enqueue = [&](int64_t* lc) {
+    switch (piece) {
+      case 0: enqueue_evaluate(ctx, lc, true); break;
+      case 1: enqueue_update(ctx, lc, 0); break;
+      case 2: enqueue_evaluate(ctx, lc, false); break;
+      case 3: enqueue_update(ctx, lc, 1); break;
+      default: enqueue_update(ctx, lc, 2); break;
+    }
+  };
   if (ctx->profiling) {
     int64_t lc = 0;
-    if (update) enqueue_update(ctx, &lc);
-    else enqueue_evaluate(ctx, &lc);
+    enqueue(&lc);
     ctx->launches += lc;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
@@ -607,8 +639,7 @@ int run_piece(tt_ctx* ctx, bool update) {
     int64_t lc = 0;
     ctx->capturing = true;
     CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-    if (update) enqueue_update(ctx, &lc);
-    else enqueue_evaluate(ctx, &lc);
+    enqueue(&lc);
     cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
     ctx->capturing = false;
     if (e != cudaSuccess) return cuda_fail(ctx, e, "graph capture");
@@ -620,6 +651,30 @@ int run_piece(tt_ctx* ctx, bool update) {
   CK(cudaGraphLaunch(*ge, ctx->stream));
   ctx->launches += *nl;
   return TT_OK;
+}
+
+// Evaluate the current iterate: tables + pass A + marginals; in sharded mode the per-rank
+// marginals h (sum n_k doubles: every h_{k,j} is a sum over samples) are all-reduced before
+// sum g^2 and the weights use them (exchange 1).
+int run_evaluate(tt_ctx* ctx) {
+  int rc;
+  if (!ctx->allreduce) return run_piece(ctx, 0);
+  if ((rc = run_piece(ctx, 2))) return rc;
+  ctx->allreduce(ctx->h, ctx->phi_off[ctx->d], (void*)ctx->stream, ctx->ar_user);
+  int64_t lc = 0;
+  launch_gather_sq_sum(ctx->stream, ctx->h, ctx->n_i[0], ctx->sc, &lc);
+  ctx->launches += lc;
+  return TT_OK;
+}
+
+// Update: in sharded mode the contractions Y (sum_k r_k n_k r_{k+1} doubles, sums over
+// samples) are all-reduced before the replicated projection and rounding (exchange 2).
+int run_update(tt_ctx* ctx) {
+  int rc;
+  if (!ctx->allreduce) return run_piece(ctx, 1);
+  if ((rc = run_piece(ctx, 3))) return rc;
+  ctx->allreduce(ctx->Y, ctx->core_off[ctx->d], (void*)ctx->stream, ctx->ar_user);
+  return run_piece(ctx, 4);
 }
 
 int read_scalars(tt_ctx* ctx) {
@@ -765,6 +820,18 @@ int tt_plan(int d, const int64_t* n, const int64_t* r, int* K_L, int64_t* N_L, i
   if (K_L) *K_L = pl.KL;
   if (N_L) *N_L = pl.NL;
   if (N_R) *N_R = pl.NR;
+  return TT_OK;
+}
+
+int tt_set_allreduce(tt_ctx* ctx, tt_allreduce_fn fn, void* user, int64_t m_global) {
+  if (!ctx) return TT_ERR_ARG;
+  if (fn && m_global < 0) return fail(ctx, TT_ERR_ARG, "m_global must be >= 0");
+  if (ctx->obs_set) return fail(ctx, TT_ERR_STATE, "tt_set_allreduce must precede tt_set_observations");
+  ctx->allreduce = fn;
+  ctx->ar_user = user;
+  ctx->m_global = fn ? m_global : -1;
+  drop_graphs(ctx);
+  ctx->evalValid = false;
   return TT_OK;
 }
 
@@ -988,7 +1055,7 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
   ctx->m = m;
   double nstar = 1.0;
   for (int k = 0; k < d; ++k) nstar *= (double)ctx->n[k];
-  ctx->p = (double)m / nstar;
+  ctx->p = (double)(ctx->allreduce ? ctx->m_global : m) / nstar;
   CK(cudaMemcpyAsync(&ctx->sc->p, &ctx->p, sizeof(double), cudaMemcpyHostToDevice, s));
   CK(cudaStreamSynchronize(s));
   ctx->obs_set = true;
@@ -997,7 +1064,8 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
 
 int tt_prgd_step(tt_ctx* ctx, double step_size) {
   if (!ctx) return TT_ERR_ARG;
-  if (!ctx->obs_set || ctx->m == 0) return fail(ctx, TT_ERR_STATE, "no observations set (nonempty Omega required)");
+  const int64_t mtot = ctx->allreduce ? ctx->m_global : ctx->m;
+  if (!ctx->obs_set || mtot <= 0) return fail(ctx, TT_ERR_STATE, "no observations set (nonempty Omega required)");
   if (!all_cores_set(ctx)) return fail(ctx, TT_ERR_STATE, "all cores must be set before stepping");
   if (!std::isfinite(step_size)) return fail(ctx, TT_ERR_ARG, "step_size must be finite");
   if (ctx->profiling && !ctx->ev_ready) {
@@ -1009,12 +1077,12 @@ int tt_prgd_step(tt_ctx* ctx, double step_size) {
   ctx->launches += lc;
   int rc;
   if (!ctx->evalValid) {
-    if ((rc = run_piece(ctx, false))) return rc;
+    if ((rc = run_evaluate(ctx))) return rc;
     if (ctx->profiling) collect_profile(ctx, 0, 3);
   }
-  if ((rc = run_piece(ctx, true))) return rc;
+  if ((rc = run_update(ctx))) return rc;
   if (ctx->profiling) collect_profile(ctx, 4, 10);
-  if ((rc = run_piece(ctx, false))) return rc;
+  if ((rc = run_evaluate(ctx))) return rc;
   if (ctx->profiling) {
     collect_profile(ctx, 0, 3);
     ++ctx->prof_steps;
@@ -1063,13 +1131,13 @@ int tt_eval_at(tt_ctx* ctx, const int32_t* h_idx, int64_t count, double* h_out) 
 
 int tt_residual_norm(tt_ctx* ctx, double* out) {
   if (!ctx || !out) return TT_ERR_ARG;
-  if (!ctx->obs_set || ctx->m == 0) {
+  if (!ctx->obs_set || (ctx->allreduce ? ctx->m_global : ctx->m) <= 0) {
     *out = 0.0;
     return TT_OK;
   }
   int rc;
   if (!ctx->evalValid) {
-    if ((rc = run_piece(ctx, false))) return rc;
+    if ((rc = run_evaluate(ctx))) return rc;
     ctx->evalValid = true;
     ctx->tablesC = !ctx->plan.mid;
   }
@@ -1181,7 +1249,7 @@ int tt_debug_get(tt_ctx* ctx, int what, int k, void* h_out, int64_t cap, int64_t
       if (!ctx->obs_set) return fail(ctx, TT_ERR_STATE, "no observations");
       if (cap < ctx->m) return fail(ctx, TT_ERR_ARG, "capacity too small");
       if (!ctx->evalValid && ctx->m > 0) {
-        if ((rc = run_piece(ctx, false))) return rc;
+        if ((rc = run_evaluate(ctx))) return rc;
         ctx->evalValid = true;
         ctx->tablesC = !ctx->plan.mid;
       }

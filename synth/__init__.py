@@ -127,9 +127,13 @@ def _sq_norm_tt(cores):
 
 
 def make_problem(cfg: int, seed: Optional[int] = None, m: Optional[int] = None,
-                 n: Optional[tuple] = None, r: Optional[tuple] = None) -> Problem:
+                 n: Optional[tuple] = None, r: Optional[tuple] = None, rank: int = 0,
+                 world: int = 1) -> Problem:
     """Build config `cfg` (1..5).  `m`, `n`, `r` override sizes for reduced test
-    variants (same recipe, same value distributions)."""
+    variants (same recipe, same value distributions).  With world > 1 (config 5, sharded
+    multi-GPU runs) the truth and the init are those of `seed`, and rank `rank` draws its
+    own m multi-indices from the residue class lin = rank (mod world) of the linear index,
+    so the ranks' sets are disjoint and their union is uniform (weak scaling)."""
     if seed is None:
         seed = BASE_SEED + cfg
     rng = np.random.Generator(np.random.PCG64(seed))
@@ -192,13 +196,22 @@ def make_problem(cfg: int, seed: Optional[int] = None, m: Optional[int] = None,
         truth = _gaussian_cores(rng, n, r)
         nstar = math.prod(n)
         draws = 30_000_000 if m is None else m
-        codes = rng.integers(0, nstar, size=draws, dtype=np.int64)
+        if world > 1:
+            rr = np.random.Generator(np.random.PCG64([seed, 1 + rank]))
+            codes = rr.integers(0, (nstar - rank + world - 1) // world, size=draws,
+                                dtype=np.int64) * world + rank
+        else:
+            codes = rng.integers(0, nstar, size=draws, dtype=np.int64)
         _, first = np.unique(codes, return_index=True)
         first.sort()                       # keep first occurrence, original (random) order
         codes = codes[first]
         idx = _unravel(codes, n)
-        z = rng.standard_normal(idx.shape[0])
+        if world > 1:
+            z = rr.standard_normal(idx.shape[0])
+            rng = np.random.Generator(np.random.PCG64([seed, 0]))
+        else:
+            z = rng.standard_normal(idx.shape[0])
         init = _perturb(rng, truth, 0.1 / math.sqrt(d))
-        meta.update(draws=draws, duplicates=draws - idx.shape[0])
+        meta.update(draws=draws, duplicates=draws - idx.shape[0], rank=rank, world=world)
         return Problem(cfg, n, r, truth, idx, z, "rel", 1e-4, init, 50, meta)
     raise ValueError(f"unknown config {cfg}")
