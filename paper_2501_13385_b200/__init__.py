@@ -129,13 +129,19 @@ def _ptr(a: np.ndarray) -> int:
     return a.ctypes.data
 
 
+_SHARED_STREAMS = {}
+
+
 class TTContext:
     """One PRGD problem on the current CUDA device.
 
-    use_torch: route device allocations through PyTorch's caching allocator and run
-    on a dedicated torch.cuda.Stream (exposed as .stream)."""
+    use_torch: route device allocations through PyTorch's caching allocator and run on a
+    torch.cuda.Stream (exposed as .stream): by default one library stream per device shared
+    by all contexts, so the allocator's cached blocks (which belong to the stream they were
+    allocated on) are reused by the next context instead of fresh cudaMalloc calls; pass
+    stream= to give a context its own stream."""
 
-    def __init__(self, n: Sequence[int], r: Sequence[int], use_torch: bool = True):
+    def __init__(self, n: Sequence[int], r: Sequence[int], use_torch: bool = True, stream=None):
         self.lib = load()
         self.n = tuple(int(v) for v in n)
         self.r = tuple(int(v) for v in r)
@@ -147,16 +153,19 @@ class TTContext:
         self.stream = None
         self._keep = []
         if use_torch:
-            self._attach_torch()
+            self._attach_torch(stream)
 
     # -- plumbing: PyTorch device memory and stream
-    def _attach_torch(self):
+    def _attach_torch(self, stream=None):
         import torch
         if not torch.cuda.is_available():
             return
         dev = torch.cuda.current_device()
-        self.stream = torch.cuda.Stream(device=dev)
-        stream = self.stream
+        if stream is None:
+            stream = _SHARED_STREAMS.get(dev)
+            if stream is None:
+                stream = _SHARED_STREAMS[dev] = torch.cuda.Stream(device=dev)
+        self.stream = stream
 
         alloc_fn = torch.cuda.caching_allocator_alloc
         delete_fn = torch.cuda.caching_allocator_delete

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -28,8 +29,8 @@ const char* kGroupNames[kNumGroups] = {
     "tables_U",   "passB_prefix", "passB_suffix", "backward_Y", "dense_round"};
 
 constexpr int64_t kSplit = 256;        // max samples per virtual row
-constexpr int64_t kWarpTarget = 256;   // samples (+1 per row) per warp
-constexpr int64_t kMaxVrowsPerWarp = 32;
+constexpr int kVrowCost = 8;            // plan cost of a virtual row: samples + kVrowCost
+constexpr int64_t kWarpCost = 320;      // plan cost per warp (about 8 rows of 30 samples)
 
 int64_t sat_mul(int64_t a, int64_t b) {
   const int64_t cap = (int64_t)1 << 62;
@@ -163,6 +164,9 @@ struct tt_ctx {
   std::vector<void*> base_allocs, obs_allocs;
 
   cudaStream_t own_stream = nullptr, stream = nullptr;
+  cudaStream_t side = nullptr;               // uploads overlapped with the bucketing sorts
+  cudaStream_t cap = nullptr;                // private graph-capture stream
+  cudaEvent_t ev_side[2] = {nullptr, nullptr};
 
   bool base_ready = false;
   int* n_dev = nullptr;
@@ -251,6 +255,32 @@ void dfree_all(tt_ctx* ctx, std::vector<void*>& list) {
   }
   list.clear();
 }
+
+// Diagnostic host wall-clock phases (env PRGD_TIMING=1): each mark synchronises the stream.
+struct PhaseTimer {
+  cudaStream_t s;
+  const char* name;
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  std::string out;
+  PhaseTimer(cudaStream_t st, const char* nm) : s(st), name(nm) {
+    const char* e = std::getenv("PRGD_TIMING");
+    on = e && *e == '1';
+    t = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto n = std::chrono::steady_clock::now();
+    char buf[96];
+    std::snprintf(buf, sizeof buf, " %s=%.2fms", what, std::chrono::duration<double, std::milli>(n - t).count());
+    out += buf;
+    t = n;
+  }
+  ~PhaseTimer() {
+    if (on) std::fprintf(stderr, "[prgd] %s:%s\n", name, out.c_str());
+  }
+};
 
 template <class T>
 bool A(tt_ctx* ctx, T** out, int64_t count, std::vector<void*>& list) {
@@ -635,13 +665,21 @@ int run_piece(tt_ctx* ctx, int piece) {
     return TT_OK;
   }
   if (!*ge) {
+    // capture on a private stream (the launch stream may be shared with other contexts /
+    // threads), launch on ctx->stream
+    if (!ctx->cap) CK(cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking));
     cudaGraph_t graph;
     int64_t lc = 0;
+    cudaStream_t launch_stream = ctx->stream;
+    ctx->stream = ctx->cap;
     ctx->capturing = true;
-    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-    enqueue(&lc);
-    cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+    cudaError_t e = cudaStreamBeginCapture(ctx->cap, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      enqueue(&lc);
+      e = cudaStreamEndCapture(ctx->cap, &graph);
+    }
     ctx->capturing = false;
+    ctx->stream = launch_stream;
     if (e != cudaSuccess) return cuda_fail(ctx, e, "graph capture");
     e = cudaGraphInstantiate(ge, graph, 0);
     cudaGraphDestroy(graph);
@@ -707,97 +745,62 @@ int collect_profile(tt_ctx* ctx, int g0, int g1) {
   return TT_OK;
 }
 
-// Virtual-row plan of one bucketing side: rows are (gather block b, row R) = b*nrow + R in
-// sample order; rows with > kSplit samples are split over several virtual rows whose partial
-// results are reduced in slot order (k_seg_fix).  Warps pack virtual rows up to kWarpTarget
-// samples and never straddle a gather-block boundary (per-block launches of the SpMM pass).
-void build_plan_host(const std::vector<int64_t>& offs, int64_t nrow, int nblk,
-                     std::vector<int32_t>& vrow_row, std::vector<int64_t>& vrow_begin,
-                     std::vector<int32_t>& vrow_cnt, std::vector<int32_t>& vrow_part,
-                     std::vector<int64_t>& warp_vbegin, std::vector<int32_t>& split_row,
-                     std::vector<int64_t>& split_first, std::vector<int64_t>& blk_warp,
-                     std::vector<int64_t>& blk_split, int64_t* npart) {
-  int64_t np = 0;
-  std::vector<int64_t> blk_vrow(nblk + 1, 0);
-  blk_split.assign(nblk + 1, 0);
-  for (int b = 0; b < nblk; ++b) {
-    blk_vrow[b] = (int64_t)vrow_row.size();
-    blk_split[b] = (int64_t)split_row.size();
-    for (int64_t R = 0; R < nrow; ++R) {
-      const int64_t P = (int64_t)b * nrow + R;
-      const int64_t beg = offs[P], cnt = offs[P + 1] - offs[P];
-      if (cnt <= kSplit) {
-        vrow_row.push_back((int32_t)P);
-        vrow_begin.push_back(beg);
-        vrow_cnt.push_back((int32_t)cnt);
-        vrow_part.push_back(-1);
-      } else {
-        split_row.push_back((int32_t)P);
-        split_first.push_back(np);
-        for (int64_t o = 0; o < cnt; o += kSplit) {
-          vrow_row.push_back((int32_t)P);
-          vrow_begin.push_back(beg + o);
-          vrow_cnt.push_back((int32_t)std::min<int64_t>(kSplit, cnt - o));
-          vrow_part.push_back((int32_t)np++);
-        }
-      }
-    }
-  }
-  blk_vrow[nblk] = (int64_t)vrow_row.size();
-  blk_split[nblk] = (int64_t)split_row.size();
-  split_first.push_back(np);
-  *npart = np;
-  blk_warp.assign(nblk + 1, 0);
-  warp_vbegin.push_back(0);
-  for (int b = 0; b < nblk; ++b) {
-    blk_warp[b] = (int64_t)warp_vbegin.size() - 1;
-    int64_t acc = 0, nv = 0;
-    for (int64_t v = blk_vrow[b]; v < blk_vrow[b + 1]; ++v) {
-      acc += vrow_cnt[v] + 1;
-      ++nv;
-      if (acc >= kWarpTarget || nv >= kMaxVrowsPerWarp || v + 1 == blk_vrow[b + 1]) {
-        warp_vbegin.push_back(v + 1);
-        acc = 0;
-        nv = 0;
-      }
-    }
-  }
-  blk_warp[nblk] = (int64_t)warp_vbegin.size() - 1;
-}
-
-template <class T>
-int upload(tt_ctx* ctx, T** dst, const std::vector<T>& src) {
-  if (!A(ctx, dst, (int64_t)src.size(), ctx->obs_allocs)) return fail(ctx, TT_ERR_OOM, "device allocation failed (plan)");
-  if (!src.empty())
-    CK(cudaMemcpyAsync(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
-  return TT_OK;
-}
-
-int make_plan(tt_ctx* ctx, const std::vector<int64_t>& offs, int64_t nrow, int nblk, int ld,
+// Work plan of one pass side from the bucket offsets on the device (plan.cu): virtual rows
+// (rows with > kSplit samples split into partial slots), split-row table, warp runs.  Two
+// small device-to-host reads (totals, per-gather-block ranges); no per-row host work.
+int make_plan(tt_ctx* ctx, const int64_t* offs_dev, int64_t nrow, int nblk, int ld, int64_t m,
               SegPlan* pl) {
-  std::vector<int32_t> vrow_row, vrow_cnt, vrow_part, split_row;
-  std::vector<int64_t> vrow_begin, warp_vbegin, split_first, blk_warp, blk_split;
-  int64_t npart = 0;
-  build_plan_host(offs, nrow, nblk, vrow_row, vrow_begin, vrow_cnt, vrow_part, warp_vbegin,
-                  split_row, split_first, blk_warp, blk_split, &npart);
+  cudaStream_t s = ctx->stream;
+  const int64_t nr = nrow * nblk;
+  std::vector<void*> tmp;
+  auto cleanup = [&]() { dfree_all(ctx, tmp); };
+  int *nv = nullptr, *sp = nullptr, *np = nullptr, *cost = nullptr, *flag = nullptr;
+  int64_t *vbase = nullptr, *sbase = nullptr, *pbase = nullptr, *C = nullptr, *wid = nullptr,
+          *blk = nullptr;
+  long long* bsum = nullptr;
+  const int64_t vmax = nr + m / kSplit + 1;
+  if (!(A(ctx, &nv, nr, tmp) && A(ctx, &sp, nr, tmp) && A(ctx, &np, nr, tmp) && A(ctx, &vbase, nr + 1, tmp) &&
+        A(ctx, &sbase, nr + 1, tmp) && A(ctx, &pbase, nr + 1, tmp) &&
+        A(ctx, &bsum, plan_scan_scratch(std::max(nr, vmax)), tmp) && A(ctx, &blk, 3 * (nblk + 1), tmp))) {
+    cleanup();
+    return fail(ctx, TT_ERR_OOM, "device allocation failed (plan)");
+  }
+  int64_t lc = 0;
+  launch_plan_rows(s, offs_dev, nr, kSplit, nv, sp, np, vbase, sbase, pbase, bsum, &lc);
+  int64_t tot[3] = {0, 0, 0};
+  CK(cudaMemcpyAsync(&tot[0], vbase + nr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&tot[1], sbase + nr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&tot[2], pbase + nr, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
   *pl = SegPlan();
-  pl->nrows = nrow * nblk;
+  pl->nrows = nr;
   pl->nrow_real = nrow;
   pl->nblk = nblk;
-  pl->blk_warp = blk_warp;
-  pl->blk_split = blk_split;
-  pl->nvrows = (int64_t)vrow_row.size();
-  pl->nwarps = (int64_t)warp_vbegin.size() - 1;
-  pl->nsplit = (int64_t)split_row.size();
-  pl->npart = npart;
-  int rc;
-  if ((rc = upload(ctx, &pl->vrow_row, vrow_row)) || (rc = upload(ctx, &pl->vrow_begin, vrow_begin)) ||
-      (rc = upload(ctx, &pl->vrow_cnt, vrow_cnt)) || (rc = upload(ctx, &pl->vrow_part, vrow_part)) ||
-      (rc = upload(ctx, &pl->warp_vbegin, warp_vbegin)) || (rc = upload(ctx, &pl->split_row, split_row)) ||
-      (rc = upload(ctx, &pl->split_first, split_first)))
-    return rc;
-  if (!A(ctx, &pl->part, std::max<int64_t>(npart, 1) * ld, ctx->obs_allocs))
-    return fail(ctx, TT_ERR_OOM, "device allocation failed (partials)");
+  pl->nvrows = tot[0];
+  pl->nsplit = tot[1];
+  pl->npart = tot[2];
+  const int64_t nvr = pl->nvrows;
+  auto& OL = ctx->obs_allocs;
+  if (!(A(ctx, &pl->vrow_row, nvr, OL) && A(ctx, &pl->vrow_begin, nvr, OL) && A(ctx, &pl->vrow_cnt, nvr, OL) &&
+        A(ctx, &pl->vrow_part, nvr, OL) && A(ctx, &pl->warp_vbegin, nvr + 1, OL) &&
+        A(ctx, &pl->split_row, pl->nsplit, OL) && A(ctx, &pl->split_first, pl->nsplit + 1, OL) &&
+        A(ctx, &pl->part, std::max<int64_t>(pl->npart, 1) * ld, OL) && A(ctx, &cost, nvr, tmp) &&
+        A(ctx, &C, nvr + 1, tmp) && A(ctx, &flag, nvr, tmp) && A(ctx, &wid, nvr + 1, tmp))) {
+    cleanup();
+    return fail(ctx, TT_ERR_OOM, "device allocation failed (plan)");
+  }
+  launch_plan_fill(s, offs_dev, nr, nrow, nblk, kSplit, vbase, sbase, pbase, nvr, pl->vrow_row,
+                   pl->vrow_begin, pl->vrow_cnt, pl->vrow_part, pl->split_row, pl->split_first,
+                   kVrowCost, kWarpCost, cost, C, flag, wid, bsum, blk, &lc);
+  launch_plan_warps(s, flag, wid, nvr, pl->warp_vbegin, &lc);
+  std::vector<int64_t> hb(3 * (nblk + 1));
+  CK(cudaMemcpyAsync(hb.data(), blk, hb.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  ctx->launches += lc;
+  cleanup();
+  pl->blk_split.assign(hb.begin() + (nblk + 1), hb.begin() + 2 * (nblk + 1));
+  pl->blk_warp.assign(hb.begin() + 2 * (nblk + 1), hb.end());
+  pl->nwarps = pl->blk_warp[nblk];
   return TT_OK;
 }
 
@@ -896,6 +899,10 @@ int tt_destroy(tt_ctx* ctx) {
   if (ctx->ev_ready)
     for (auto& e : ctx->ev) cudaEventDestroy(e);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->cap) cudaStreamDestroy(ctx->cap);
+  for (cudaEvent_t e : ctx->ev_side)
+    if (e) cudaEventDestroy(e);
   delete ctx;
   return TT_OK;
 }
@@ -963,6 +970,7 @@ int tt_get_core(tt_ctx* ctx, int k, double* h_core_out) {
 
 int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals, int64_t m) {
   if (!ctx) return TT_ERR_ARG;
+  PhaseTimer ptm(ctx->stream, "set_observations");
   if (m < 0 || m >= ((int64_t)1 << 31)) return fail(ctx, TT_ERR_ARG, "m must be in [0, 2^31)");
   if (m > 0 && (!h_idx || !h_vals)) return fail(ctx, TT_ERR_ARG, "NULL idx or vals");
   int rc = ensure_base(ctx);
@@ -1000,6 +1008,7 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
     dfree_all(ctx, OL);
     return fail(ctx, TT_ERR_OOM, "device allocation failed (observations)");
   }
+  ptm.mark("alloc");
   int bitsP = 1, bitsS = 1, bitsVP = 1, bitsVS = 1;
   while (((int64_t)1 << bitsP) < NL) ++bitsP;
   while (((int64_t)1 << bitsS) < NR) ++bitsS;
@@ -1013,8 +1022,18 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
   cudaStream_t s = ctx->stream;
   int64_t lc = 0;
   if (m > 0) {
+    if (!ctx->side) {
+      CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&ctx->ev_side[0], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_side[1], cudaEventDisableTiming));
+    }
+    // idx first on the main stream; the values follow on the side stream (the link carries one
+    // copy at a time) while the keys are built and sorted; after_sort_pre waits for them.
     CK(cudaMemcpyAsync(idx_dev, h_idx, (size_t)m * d * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(y_orig, h_vals, (size_t)m * sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(ctx->ev_side[0], s));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_side[0], 0));
+    CK(cudaMemcpyAsync(y_orig, h_vals, (size_t)m * sizeof(double), cudaMemcpyHostToDevice, ctx->side));
+    CK(cudaEventRecord(ctx->ev_side[1], ctx->side));
     CK(cudaMemsetAsync(&ctx->sc->index_err, 0, sizeof(int), s));
     launch_make_keys(s, idx_dev, m, d, ctx->n_dev, KL, bitsP, bitsS, NL, NR, nbL, nbR,
                      ctx->plan.mid ? (int)ctx->n[KL - 1] : 1, ctx->plan.mid ? (int)ctx->n[KL] : 1,
@@ -1022,7 +1041,9 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
     CK(cudaMemcpyAsync(vals2, vals, (size_t)m * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    ptm.mark("h2d+keys");
     if (ctx->sc_host->index_err) {
+      cudaStreamSynchronize(ctx->side);   // the value upload still targets y_orig
       cleanup();
       dfree_all(ctx, OL);
       return fail(ctx, TT_ERR_INDEX, "an observed index is outside [0, n_k)");
@@ -1030,11 +1051,14 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
     uint64_t* ko;
     uint32_t* vo;
     radix_sort_pairs(s, kpre, vals, ktmp, vtmp, m, bitsVP + bitsS, hist, hl, &ko, &vo, &lc);
+    CK(cudaStreamWaitEvent(s, ctx->ev_side[1], 0));
     launch_after_sort_pre(s, ko, vo, m, bitsS, NLv, y_orig, ctx->Spre, ctx->ypre, ctx->sid_pre, inv,
                           ctx->offsL, &lc);
+    ptm.mark("sort_pre");
     radix_sort_pairs(s, ksuf, vals2, ktmp, vtmp, m, bitsVS + bitsP, hist, hl, &ko, &vo, &lc);
     launch_after_sort_suf(s, ko, vo, m, bitsP, NRv, inv, ctx->pos_suf, ctx->Psuf, ctx->sid_suf,
                           ctx->pre2suf, ctx->offsR, &lc);
+    ptm.mark("sort_suf");
   } else {
     CK(cudaMemsetAsync(ctx->offsL, 0, (NLv + 1) * sizeof(int64_t), s));
     CK(cudaMemsetAsync(ctx->offsR, 0, (NRv + 1) * sizeof(int64_t), s));
@@ -1045,13 +1069,12 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
     cleanup();
     return cuda_fail(ctx, e, "bucketing kernels");
   }
-  std::vector<int64_t> hoffsL(NLv + 1), hoffsR(NRv + 1);
-  CK(cudaMemcpyAsync(hoffsL.data(), ctx->offsL, (NLv + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(hoffsR.data(), ctx->offsR, (NRv + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
   cleanup();
-  if ((rc = make_plan(ctx, hoffsL, NL, nbL, ctx->ldr[KL], &ctx->planL))) return rc;
-  if ((rc = make_plan(ctx, hoffsR, NR, nbR, ctx->ldr[KL], &ctx->planR))) return rc;
+  ptm.mark("free_tmp");
+  if ((rc = make_plan(ctx, ctx->offsL, NL, nbL, ctx->ldr[KL], m, &ctx->planL))) return rc;
+  ptm.mark("plan_L");
+  if ((rc = make_plan(ctx, ctx->offsR, NR, nbR, ctx->ldr[KL], m, &ctx->planR))) return rc;
+  ptm.mark("plan_R");
   ctx->m = m;
   double nstar = 1.0;
   for (int k = 0; k < d; ++k) nstar *= (double)ctx->n[k];

@@ -104,6 +104,20 @@ void launch_after_sort_suf(cudaStream_t s, const uint64_t* keys, const uint32_t*
                            int32_t* Psuf, int32_t* sid_suf, int32_t* pre2suf, int64_t* offsR,
                            int64_t* launches);
 
+// plan.cu: device construction of the pass work plans (SegPlan)
+int64_t plan_scan_scratch(int64_t len);
+void launch_plan_rows(cudaStream_t s, const int64_t* offs, int64_t nr, int64_t split, int* nv, int* sp,
+                      int* np, int64_t* vbase, int64_t* sbase, int64_t* pbase, long long* bsum,
+                      int64_t* launches);
+void launch_plan_fill(cudaStream_t s, const int64_t* offs, int64_t nr, int64_t nrow, int nblk,
+                      int64_t split, const int64_t* vbase, const int64_t* sbase, const int64_t* pbase,
+                      int64_t nvrows, int32_t* vrow_row, int64_t* vrow_begin, int32_t* vrow_cnt,
+                      int32_t* vrow_part, int32_t* split_row, int64_t* split_first, int vcost,
+                      int64_t wcost, int* cost, int64_t* C, int* flag, int64_t* wid,
+                      long long* bsum, int64_t* blk_out, int64_t* launches);
+void launch_plan_warps(cudaStream_t s, const int* flag, const int64_t* wid, int64_t nvrows,
+                       int64_t* warp_vbegin, int64_t* launches);
+
 // tables.cu
 void launch_table_left(cudaStream_t s, const double* in, int ld_in, const double* core, int r0,
                        int nk, int r1, double* out, int ld_out, int64_t rows_out,
