@@ -28,7 +28,7 @@ __all__ = [
     "unweight", "step_length", "assemble", "tt_round", "prgd_step", "solve",
     "split_point", "stable_order", "stable_buckets", "to_dense", "tt_svd",
     "spectral_init", "tt_norm", "tt_diff_norm", "tt_add", "os_dim", "os_to_m",
-    "theory_step", "tangent_direction", "tangent_sum",
+    "theory_step", "tangent_direction", "tangent_sum", "tt_dot", "adaptive_step",
 ]
 
 CHUNK = 1 << 18   # samples per chunk (bounds interface memory; order of sums only)
@@ -255,7 +255,8 @@ def unweight(cores, phi):
 def step_length(step_size, eps, p, step_rule="theory"):
     """A12: alpha_l = step_size * eps_l^{1/2} / p (Thm 4.1 with step_size = 1.001,
     PAPER.md:384; reading R2), or alpha = step_size ("raw").  With W = I
-    (eps_rule "none") the theory rule is step_size / p."""
+    (eps_rule "none") the theory rule is step_size / p.  The adaptive rule needs the
+    direction: see adaptive_step."""
     if step_rule == "raw":
         return float(step_size)
     if step_rule != "theory":
@@ -268,6 +269,37 @@ def step_length(step_size, eps, p, step_rule="theory"):
 def theory_step(eps, p, mult=1.001):
     """alpha_l = 1.001 eps_l^{1/2} p^{-1}."""
     return mult * math.sqrt(eps) / p
+
+
+def tt_dot(a, b) -> float:
+    """<a, b>_F of two TTs with equal mode sizes: contract the cores left to right,
+    M <- sum_j a_k(:, j, :)^T M b_k(:, j, :), starting from M = [1]."""
+    M = np.ones((1, 1))
+    for ca, cb in zip(a, b):
+        M = np.einsum("ab,ajc,bjd->cd", M, ca, cb)
+    return float(M[0, 0])
+
+
+def adaptive_step(step_size, U, Ahat, Ttil, A, idx):
+    """A12, adaptive rule: the steepest step along the search direction in the tangent space
+    (eq. `PRGD stepsize`),
+        alpha_l = step_size * ||P~_T W^{-1} G||_W^2 / ||P_Omega P~_T W^{-1} G||_F^2,
+    which for W = I is RGD's alpha_l = ||P_T G||_F^2 / ||P_Omega P_T G||_F^2.
+    D = P~_T W^{-1} G = sum_k [Ttil_1..A_k..Ttil_d].  Numerator: the
+    components are W-orthogonal (Lemma `component orthogonal`), and
+    W^{1/2} [Ttil_1..A_k..Ttil_d] = [U_1..Ahat_k..U_d] (Prop. 3.1, PAPER.md:176, 293), so
+    ||D||_W^2 = sum_k ||[U_1..Ahat_k..U_d]||_F^2.  Denominator: D evaluated at every observed
+    index.  Returns (alpha, num, den); alpha = 0 when den = 0 (reading R20)."""
+    d = len(U)
+    num = 0.0
+    for k in range(d):
+        comp = [Ahat[i] if i == k else U[i] for i in range(d)]
+        num += tt_dot(comp, comp)
+    D = tangent_sum(Ttil, A)
+    v = eval_at(D, idx)
+    den = float(v @ v)
+    alpha = float(step_size) * num / den if den > 0.0 else 0.0
+    return alpha, num, den
 
 
 # --------------------------------------------------------------------------- A13
@@ -385,7 +417,11 @@ def prgd_step(cores, idx, y, n, r, step_size, eps_rule="vee", eps_value=None,
         return (new, info) if return_info else new
     ghat = precondition_residual(g, idx, phi)                    # A7
     tv = tangent_direction(cores, phi, idx, ghat)                # A4-A6, A8-A11
-    alpha = step_length(step_size, eps, p, step_rule)            # A12
+    if step_rule == "adaptive":                                  # A12
+        alpha, num, den = adaptive_step(step_size, tv["U"], tv["Ahat"], tv["Ttil"], tv["A"], idx)
+        info.update(adapt_num=num, adapt_den=den)
+    else:
+        alpha = step_length(step_size, eps, p, step_rule)        # A12
     B = assemble(tv["Ttil"], tv["A"], alpha)                     # A13
     new = tt_round(B, r)                                         # A14
     info.update(noop=False, w=w, phi=phi, ghat=ghat, alpha=alpha, B=B, **tv)

@@ -183,6 +183,64 @@ def test_gradient_equals_bruteforce_jacobian_projection(n, r, rule):
     np.testing.assert_allclose(got, ref, rtol=1e-9, atol=1e-10 * np.abs(ref).max())
 
 
+@pytest.mark.parametrize("n,r", [((3, 4, 3), (1, 2, 2, 1)), ((2, 3, 2, 3), (1, 2, 2, 2, 1))])
+@pytest.mark.parametrize("rule", ["vee", "none"])
+def test_adaptive_step_equals_bruteforce_steepest_step(n, r, rule):
+    # eq. `PRGD stepsize` and, for W = I, RGD's step:
+    # alpha = ||D||_W^2 / ||P_Omega D||^2 with D the dense brute-force W-projection of W^{-1}G.
+    # Also the line-search identity ||D||_W^2 = <G, D> (D is the W-orthogonal projection of
+    # W^{-1}G), so alpha minimises f(T - alpha D).  Catches a numerator without the weights,
+    # a dropped component, non-orthogonal components or a wrong denominator.
+    rng = np.random.default_rng(11)
+    d = len(n)
+    cores = rand_tt(rng, n, r)
+    N = math.prod(n)
+    idx = all_indices(n)[rng.choice(N, max(2, int(0.6 * N)), replace=False)]
+    g = rng.standard_normal(idx.shape[0])
+    eps, w, phi = oracle.build_weights(oracle.mode_sums(g, idx, n), d, rule)
+    ghat = oracle.precondition_residual(g, idx, phi)
+    tv = oracle.tangent_direction(cores, phi, idx, ghat)
+    alpha, num, den = oracle.adaptive_step(1.0, tv["U"], tv["Ahat"], tv["Ttil"], tv["A"], idx)
+    Dw = bf.weight_diag(n, w, d)
+    G = bf.sampled_dense(n, idx, g)
+    Dref = bf.weighted_tangent_projection(cores, Dw, G / Dw)
+    num_ref = float(np.sum(Dw * Dref * Dref))
+    dv = Dref[tuple(idx.T)]
+    den_ref = float(dv @ dv)
+    assert abs(num - num_ref) <= 1e-9 * num_ref
+    assert abs(den - den_ref) <= 1e-9 * den_ref
+    assert abs(num_ref - float(g @ dv)) <= 1e-9 * num_ref          # <G, D> = ||D||_W^2
+    assert abs(alpha - num_ref / den_ref) <= 1e-9 * alpha
+    assert abs(oracle.adaptive_step(0.5, tv["U"], tv["Ahat"], tv["Ttil"], tv["A"], idx)[0]
+               - 0.5 * alpha) <= 1e-12 * alpha
+
+
+def test_adaptive_prgd_step_minimises_objective_along_direction():
+    # The adaptive step is the exact minimiser of f(T_l - alpha D) over alpha
+    # (`argmin_alpha`), f = 1/2 sum_Omega (T - y)^2 evaluated densely.
+    rng = np.random.default_rng(12)
+    n, r = (4, 3, 4), (1, 2, 2, 1)
+    truth = rand_tt(rng, n, r)
+    T0 = oracle.tt_add(truth, rand_tt(rng, n, r, 0.3))
+    T0 = oracle.tt_round(T0, r)
+    N = math.prod(n)
+    idx = all_indices(n)[rng.choice(N, int(0.7 * N), replace=False)]
+    y = oracle.eval_at(truth, idx)
+    _, info = oracle.prgd_step(T0, idx, y, n, r, 1.0, step_rule="adaptive", return_info=True)
+    D = oracle.to_dense(oracle.tangent_sum(info["Ttil"], info["A"]))
+    T = bf.dense(T0)
+    Y = bf.sampled_dense(n, idx, y)
+    mask = bf.sampled_dense(n, idx, np.ones(idx.shape[0])) > 0
+
+    def f(a):
+        return 0.5 * float(np.sum(((T - a * D) - Y)[mask] ** 2))
+
+    a = info["alpha"]
+    assert a > 0
+    for t in (0.9, 0.99, 1.01, 1.1):
+        assert f(a) < f(t * a)
+
+
 def test_projection_idempotent_selfadjoint_and_components_orthogonal():
     # SPEC.md:306/322-323 idempotence & self-adjointness in <.,.>_W; Lemma component
     # orthogonal; Def. 3.2 weighted orthogonality.
