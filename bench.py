@@ -152,6 +152,8 @@ def run_ours(args, rank, ws, dist):
     KL, NL, NR = pkg.plan(pr.n, pr.r)
 
     ctx = pkg.TTContext(pr.n, pr.r)
+    if args.step_rule != "theory":
+        ctx.set_metric("vee", 0.0, args.step_rule)
     if ar is not None:
         ctx.set_allreduce(ar, m_global)
     stream = ctx.stream
@@ -229,6 +231,8 @@ def run_e2e(args, pr, y, init, ar=None, m_global=None, dist=None):
         dist.barrier()
     t0 = time.perf_counter()
     ctx = pkg.TTContext(pr.n, pr.r)
+    if args.step_rule != "theory":
+        ctx.set_metric("vee", 0.0, args.step_rule)
     if ar is not None:
         ctx.set_allreduce(ar, m_global)
     ctx.set_observations(idx_p.numpy(), y_p.numpy())
@@ -288,6 +292,9 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--m", type=int, default=None, help="override |Omega| draws (debug only)")
     ap.add_argument("--step-size", type=float, default=1.0)
+    ap.add_argument("--step-rule", choices=["theory", "adaptive"], default="theory",
+                    help="A12 rule: theory (Thm 4.1 form, the default) or adaptive (steepest step, "
+                         "PAPER.md:236-238; one more pass over Omega per step)")
     ap.add_argument("--profile-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -352,7 +359,7 @@ def main():
                                f"|Omega|={m}, noise {pr.noise_sigma} {pr.noise_kind}",
                    "d": pr.d, "n": list(pr.n), "r": list(pr.r), "m": m, "K_L": r["KL"],
                    "l2": "inputs larger than L2 (Omega arrays + tables > 126 MB); no flush",
-                   "m_global": r["m_global"],
+                   "m_global": r["m_global"], "step_rule": args.step_rule,
                    "parallelism": (f"sharded Omega over {ws} GPUs (h and Y all-reduced, NCCL); "
                                    "value = N x iter/s of the N-times-larger problem") if ws > 1
                                   else "single"},

@@ -67,9 +67,15 @@ typedef struct tt_ctx tt_ctx;
  * step rules (A12):
  *   TT_STEP_THEORY alpha_l = step_size * eps_l^{1/2} / p (Thm 4.1 with step_size =
  *                  1.001; with TT_EPS_NONE: step_size / p).  Default.
- *   TT_STEP_RAW    alpha_l = step_size. */
+ *   TT_STEP_RAW    alpha_l = step_size.
+ *   TT_STEP_ADAPTIVE  the steepest step along the search direction in the tangent space,
+ *                  alpha_l = step_size * ||P~_T W^{-1} G||_W^2 / ||P_Omega P~_T W^{-1} G||_F^2
+ *                  (eq. `PRGD stepsize`; with TT_EPS_NONE RGD's
+ *                  ||P_T G||^2 / ||P_Omega P_T G||^2).  Costs one more pass
+ *                  over Omega per step (the tangent vector evaluated at every sample);
+ *                  alpha_l = 0 if that vanishes.  Needs 2 r_k <= 32. */
 enum { TT_EPS_VEE = 0, TT_EPS_FIXED = 1, TT_EPS_NONE = 2 };
-enum { TT_STEP_THEORY = 0, TT_STEP_RAW = 1 };
+enum { TT_STEP_THEORY = 0, TT_STEP_RAW = 1, TT_STEP_ADAPTIVE = 2 };
 
 /* ------------------------------------------------------------------ lifecycle */
 
@@ -113,7 +119,8 @@ PRGD_API int tt_set_core(tt_ctx* ctx, int k, const double* h_core);
 PRGD_API int tt_get_core(tt_ctx* ctx, int k, double* h_core_out);
 
 /* Metric / step rules, see the enums above.  eps is used by TT_EPS_FIXED only
- * (must be > 0 then).  Defaults: TT_EPS_VEE, TT_STEP_THEORY. */
+ * (must be > 0 then).  Defaults: TT_EPS_VEE, TT_STEP_THEORY.  TT_STEP_ADAPTIVE allocates
+ * its buffers here (TT_ERR_OOM; TT_ERR_RANK if some 2 r_k > 32). */
 PRGD_API int tt_set_metric(tt_ctx* ctx, int eps_rule, double eps, int step_rule);
 
 /* ------------------------------------------------------------------ the hot path */

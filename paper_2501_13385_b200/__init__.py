@@ -25,7 +25,7 @@ STATUS_NAMES = {0: "TT_OK", -1: "TT_ERR_ARG", -2: "TT_ERR_RANK", -3: "TT_ERR_IND
                 -4: "TT_ERR_STATE", -5: "TT_ERR_NUMERIC", -6: "TT_ERR_CUDA", -7: "TT_ERR_OOM",
                 -8: "TT_ERR_UNSUPPORTED"}
 EPS_RULES = {"vee": 0, "fixed": 1, "none": 2}
-STEP_RULES = {"theory": 0, "raw": 1}
+STEP_RULES = {"theory": 0, "raw": 1, "adaptive": 2}
 DBG = {"perm_pre": 1, "offs_l": 2, "perm_suf": 3, "offs_r": 4, "resid": 5, "h": 6, "phi": 7,
        "eps": 8, "u": 9, "p": 10, "y": 11, "ahat": 12}
 

@@ -23,10 +23,10 @@ using namespace prgd;
 
 namespace {
 
-constexpr int kNumGroups = 11;
+constexpr int kNumGroups = 12;
 const char* kGroupNames[kNumGroups] = {
     "tables_C",   "passA_prefix", "passA_suffix", "marginals",   "weights_psi", "dense_orth",
-    "tables_U",   "passB_prefix", "passB_suffix", "backward_Y", "dense_round"};
+    "tables_U",   "passB_prefix", "passB_suffix", "backward_Y", "dense_round", "adaptive_step"};
 
 constexpr int64_t kSplit = 256;        // max samples per virtual row
 constexpr int kVrowCost = 8;            // plan cost of a virtual row: samples + kVrowCost
@@ -202,8 +202,10 @@ struct tt_ctx {
 
   cudaGraphExec_t gA = nullptr, gB = nullptr;
   // sharded (multi-rank) mode: Omega is split over ranks; h and Y are all-reduced
-  cudaGraphExec_t gA1 = nullptr, gB1 = nullptr, gB2 = nullptr;
-  int64_t nA1 = 0, nB1 = 0, nB2 = 0;
+  cudaGraphExec_t gA1 = nullptr, gB1 = nullptr, gB2 = nullptr, gB3 = nullptr;
+  int64_t nA1 = 0, nB1 = 0, nB2 = 0, nB3 = 0;
+  // adaptive step (TT_STEP_ADAPTIVE): stacked cores, concatenated table inputs, den partials
+  double *Dcore = nullptr, *dcatL = nullptr, *dcatR = nullptr, *dpart = nullptr;
   tt_allreduce_fn allreduce = nullptr;
   void* ar_user = nullptr;
   int64_t m_global = -1;
@@ -292,7 +294,7 @@ void drop_graphs(tt_ctx* ctx) {
   if (ctx->gA) cudaGraphExecDestroy(ctx->gA);
   if (ctx->gB) cudaGraphExecDestroy(ctx->gB);
   ctx->gA = ctx->gB = nullptr;
-  for (cudaGraphExec_t* g : {&ctx->gA1, &ctx->gB1, &ctx->gB2}) {
+  for (cudaGraphExec_t* g : {&ctx->gA1, &ctx->gB1, &ctx->gB2, &ctx->gB3}) {
     if (*g) cudaGraphExecDestroy(*g);
     *g = nullptr;
   }
@@ -418,6 +420,26 @@ DenseArgs dense_args(tt_ctx* ctx) {
   return a;
 }
 
+// Buffers of the adaptive step (allocated once, before any graph capture).
+int ensure_adaptive(tt_ctx* ctx) {
+  int rc = ensure_base(ctx);
+  if (rc) return rc;
+  if (ctx->Dcore) return TT_OK;
+  const int d = ctx->d, KL = ctx->plan.KL;
+  if (ctx->plan.mid) return fail(ctx, TT_ERR_STATE, "adaptive step not available with the middle-split passes");
+  for (int k = 0; k <= d; ++k)
+    if (2 * ctx->r[k] > kMaxRank) return fail(ctx, TT_ERR_RANK, "adaptive step needs 2 r_k <= 32");
+  int64_t lenL = 1, lenR = 1;
+  for (int k = 1; k < KL; ++k) lenL = std::max<int64_t>(lenL, ctx->NLk[k] * pad_rank(2 * (int)ctx->r[k]));
+  for (int k = KL; k + 1 < d; ++k)
+    lenR = std::max<int64_t>(lenR, ctx->NRk[k + 1] * pad_rank(2 * (int)ctx->r[k + 1]));
+  auto& L = ctx->base_allocs;
+  if (!A(ctx, &ctx->Dcore, 2 * ctx->core_off[d], L) || !A(ctx, &ctx->dcatL, lenL, L) ||
+      !A(ctx, &ctx->dcatR, lenR, L) || !A(ctx, &ctx->dpart, adapt_vsum_parts(), L))
+    return fail(ctx, TT_ERR_OOM, "device allocation failed (adaptive step)");
+  return TT_OK;
+}
+
 // ------------------------------------------------------------------ profiling groups
 void grp(tt_ctx* ctx, int id, bool begin) {
   if (!ctx->profiling || ctx->capturing || !ctx->ev_ready) return;
@@ -515,14 +537,111 @@ void enqueue_evaluate(tt_ctx* ctx, int64_t* lc, bool with_sumsq = true) {
 
 // part 0: the whole update; part 1: up to the contractions Y (pass B + backward);
 // part 2: projection + rank-2r assembly + rounding (sharded mode all-reduces Y between).
+// Adaptive step, front half: projection with the numerator terms, the
+// one-Ahat chain tables LD / RD (in the E / F buffers, free after the backward recursions),
+// the DPASS evaluation of D on Omega and the denominator.  The back half (alpha, assembly,
+// rounding) is enqueue_adaptive_back; in sharded mode the denominator is all-reduced between.
+void enqueue_adaptive_front(tt_ctx* ctx, int64_t* lc) {
+  const int d = ctx->d, KL = ctx->plan.KL;
+  cudaStream_t s = ctx->stream;
+  DenseArgs da = dense_args(ctx);
+  grp(ctx, 11, true);
+  launch_project(s, da, 1, lc);
+  std::vector<int> ni(d), ri(d + 1);
+  for (int k = 0; k < d; ++k) ni[k] = (int)ctx->n[k];
+  for (int k = 0; k <= d; ++k) ri[k] = (int)ctx->r[k];
+  launch_stack_cores(s, d, ni.data(), ri.data(), ctx->core_off.data(), KL, ctx->U, ctx->Ahat, ctx->Dcore,
+                     ctx->sc, lc);
+  const int nlev = std::max(KL, d - KL);
+  for (int i = 0; i < nlev; ++i) {
+    const bool hasL = i < KL, hasR = d - 1 - i >= KL;
+    const int kR = d - 1 - i;
+    const bool catL = hasL && i >= 1, catR = hasR && kR < d - 1;
+    const int ldcL = catL ? pad_rank(2 * (int)ctx->r[i]) : 0;
+    const int ldcR = catR ? pad_rank(2 * (int)ctx->r[kR + 1]) : 0;
+    if (catL || catR)
+      launch_concat2(s, catL ? ctx->dcatL : nullptr, ldcL, catL ? ctx->EL[i] : nullptr, ctx->ldr[i],
+                     catL ? ctx->LT[i] : nullptr, ctx->ldr[i], catL ? ctx->NLk[i] : 0, (int)ctx->r[i],
+                     catR ? ctx->dcatR : nullptr, ldcR, catR ? ctx->FR[kR + 1] : nullptr,
+                     ctx->ldr[kR + 1], catR ? ctx->RT[kR + 1] : nullptr, ctx->ldr[kR + 1],
+                     catR ? ctx->NRk[kR + 1] : 0, (int)ctx->r[kR + 1], ctx->sc, lc);
+    std::vector<TableLevel> L, R;
+    if (hasL) {
+      TableLevel t{true, catL ? ctx->dcatL : nullptr, ldcL,
+                   catL ? ctx->Dcore + 2 * ctx->core_off[i] : ctx->Ahat + ctx->core_off[i],
+                   catL ? 2 * (int)ctx->r[i] : (int)ctx->r[i], (int)ctx->n[i], (int)ctx->r[i + 1],
+                   ctx->EL[i + 1], ctx->ldr[i + 1], ctx->NLk[i + 1], i + 1 == KL ? ctx->psiL : nullptr};
+      L.push_back(t);
+    }
+    if (hasR) {
+      TableLevel t{false, catR ? ctx->dcatR : nullptr, ldcR,
+                   catR ? ctx->Dcore + 2 * ctx->core_off[kR] : ctx->Ahat + ctx->core_off[kR],
+                   (int)ctx->r[kR], (int)ctx->n[kR], catR ? 2 * (int)ctx->r[kR + 1] : (int)ctx->r[kR + 1],
+                   ctx->FR[kR], ctx->ldr[kR], ctx->NRk[kR], kR == KL ? ctx->psiR : nullptr};
+      R.push_back(t);
+    }
+    bool ok = true;
+    for (const TableLevel& t : L) ok = ok && level_tab_ok(t.r0, t.nk, t.r1, t.ld_out);
+    for (const TableLevel& t : R) ok = ok && level_tab_ok(t.r0, t.nk, t.r1, t.ld_out);
+    if (ok) {
+      launch_table_levels(s, L, R, ctx->sc, lc);
+    } else {
+      for (const TableLevel& t : L)
+        launch_table_left(s, t.in, t.ld_in, t.core, t.r0, t.nk, t.r1, t.out, t.ld_out, t.rows_out,
+                          t.rowscale, ctx->sc, lc);
+      for (const TableLevel& t : R)
+        launch_table_right(s, t.in, t.ld_in, t.core, t.r0, t.nk, t.r1, t.out, t.ld_out, t.rows_out,
+                           t.rowscale, ctx->sc, lc);
+    }
+  }
+  if (ctx->m > 0) {
+    SegArgs a{};
+    a.plan = &ctx->planL;
+    a.mode = kDPASS;
+    a.ld = ctx->ldr[KL];
+    a.col = ctx->Spre;
+    a.rowtab = ctx->EL[KL];     // LD (psi_L scaled)
+    a.rowtab2 = ctx->LT[KL];    // LU (psi_L scaled)
+    a.coltab = ctx->RT[KL];     // RU (psi_R scaled)
+    a.coltab2 = ctx->FR[KL];    // RD (psi_R scaled)
+    a.out = ctx->HL;
+    launch_seg(s, a, ctx->sc, lc);
+    launch_adapt_den(s, ctx->HL, ctx->plan.NL * ctx->plan.nbL, ctx->dpart, ctx->sc, lc);
+  } else {
+    cudaMemsetAsync(&ctx->sc->adapt_den, 0, sizeof(double), s);
+  }
+  grp(ctx, 11, false);
+}
+
+void enqueue_adaptive_back(tt_ctx* ctx, int64_t* lc) {
+  cudaStream_t s = ctx->stream;
+  DenseArgs da = dense_args(ctx);
+  grp(ctx, 10, true);
+  launch_adapt_alpha(s, ctx->d, ctx->sc, lc);
+  launch_project(s, da, 2, lc);
+  launch_round_only(s, da, lc);
+  grp(ctx, 10, false);
+}
+
+// part 0: the whole update; part 1: up to Y (sharded, before the Y all-reduce); part 2: after
+// the Y all-reduce (rounding, or the adaptive front half); part 3: adaptive back half.
 void enqueue_update(tt_ctx* ctx, int64_t* lc, int part = 0) {
   const int d = ctx->d, KL = ctx->plan.KL;
   cudaStream_t s = ctx->stream;
+  const bool adaptive = ctx->step_rule == TT_STEP_ADAPTIVE;
   if (part == 2) {
+    if (adaptive) {
+      enqueue_adaptive_front(ctx, lc);
+      return;
+    }
     DenseArgs da = dense_args(ctx);
     grp(ctx, 10, true);
     launch_dense_round(ctx->stream, da, lc);
     grp(ctx, 10, false);
+    return;
+  }
+  if (part == 3) {
+    enqueue_adaptive_back(ctx, lc);
     return;
   }
   grp(ctx, 4, true);
@@ -634,6 +753,11 @@ void enqueue_update(tt_ctx* ctx, int64_t* lc, int part = 0) {
   }
   grp(ctx, 9, false);
   if (part == 1) return;
+  if (adaptive) {
+    enqueue_adaptive_front(ctx, lc);
+    enqueue_adaptive_back(ctx, lc);
+    return;
+  }
   grp(ctx, 10, true);
   launch_dense_round(s, da, lc);
   grp(ctx, 10, false);
@@ -643,8 +767,8 @@ void enqueue_update(tt_ctx* ctx, int64_t* lc, int part = 0) {
 // Pieces: 0 evaluate (+ sum g^2), 1 update, 2 evaluate without sum g^2, 3 update up to Y,
 // 4 rounding.  Each runs as a captured CUDA graph (cached), or directly when profiling.
 int run_piece(tt_ctx* ctx, int piece) {
-  cudaGraphExec_t* slots[5] = {&ctx->gA, &ctx->gB, &ctx->gA1, &ctx->gB1, &ctx->gB2};
-  int64_t* counts[5] = {&ctx->nA, &ctx->nB, &ctx->nA1, &ctx->nB1, &ctx->nB2};
+  cudaGraphExec_t* slots[6] = {&ctx->gA, &ctx->gB, &ctx->gA1, &ctx->gB1, &ctx->gB2, &ctx->gB3};
+  int64_t* counts[6] = {&ctx->nA, &ctx->nB, &ctx->nA1, &ctx->nB1, &ctx->nB2, &ctx->nB3};
   cudaGraphExec_t* ge = slots[piece];
   int64_t* nl = counts[piece];
   auto enqueue = [&](int64_t* lc) {
@@ -653,7 +777,8 @@ int run_piece(tt_ctx* ctx, int piece) {
       case 1: enqueue_update(ctx, lc, 0); break;
       case 2: enqueue_evaluate(ctx, lc, false); break;
       case 3: enqueue_update(ctx, lc, 1); break;
-      default: enqueue_update(ctx, lc, 2); break;
+      case 4: enqueue_update(ctx, lc, 2); break;
+      default: enqueue_update(ctx, lc, 3); break;
     }
   };
   if (ctx->profiling) {
@@ -712,7 +837,10 @@ int run_update(tt_ctx* ctx) {
   if (!ctx->allreduce) return run_piece(ctx, 1);
   if ((rc = run_piece(ctx, 3))) return rc;
   ctx->allreduce(ctx->Y, ctx->core_off[ctx->d], (void*)ctx->stream, ctx->ar_user);
-  return run_piece(ctx, 4);
+  if ((rc = run_piece(ctx, 4))) return rc;
+  if (ctx->step_rule != TT_STEP_ADAPTIVE) return TT_OK;
+  ctx->allreduce(&ctx->sc->adapt_den, 1, (void*)ctx->stream, ctx->ar_user);   // sum over ranks
+  return run_piece(ctx, 5);
 }
 
 int read_scalars(tt_ctx* ctx) {
@@ -931,10 +1059,14 @@ int tt_set_allocator(tt_ctx* ctx, void* (*alloc)(size_t, void*), void (*release)
 int tt_set_metric(tt_ctx* ctx, int eps_rule, double eps, int step_rule) {
   if (!ctx) return TT_ERR_ARG;
   if (eps_rule < TT_EPS_VEE || eps_rule > TT_EPS_NONE || step_rule < TT_STEP_THEORY ||
-      step_rule > TT_STEP_RAW)
+      step_rule > TT_STEP_ADAPTIVE)
     return fail(ctx, TT_ERR_ARG, "unknown eps or step rule");
   if (eps_rule == TT_EPS_FIXED && !(eps > 0.0 && std::isfinite(eps)))
     return fail(ctx, TT_ERR_ARG, "TT_EPS_FIXED needs a finite eps > 0");
+  if (step_rule == TT_STEP_ADAPTIVE) {
+    int rc = ensure_adaptive(ctx);
+    if (rc) return rc;
+  }
   ctx->eps_rule = eps_rule;
   ctx->eps_fixed = eps;
   ctx->step_rule = step_rule;
@@ -1104,7 +1236,7 @@ int tt_prgd_step(tt_ctx* ctx, double step_size) {
     if (ctx->profiling) collect_profile(ctx, 0, 3);
   }
   if ((rc = run_update(ctx))) return rc;
-  if (ctx->profiling) collect_profile(ctx, 4, 10);
+  if (ctx->profiling) collect_profile(ctx, 4, 11);
   if ((rc = run_evaluate(ctx))) return rc;
   if (ctx->profiling) {
     collect_profile(ctx, 0, 3);

@@ -1042,7 +1042,9 @@ __global__ void __launch_bounds__(kDenseThreads) k_project(DenseArgs a) {
   const double* Y = a.Y + a.core_off[k];
   const double* U = a.U + a.core_off[k];
   double* Ah = a.Ahat + a.core_off[k];
-  if (k == d - 1) {
+  if (a.proj_mode == 2) {
+    // assembly only: Ahat from the projection launch, alpha from the adaptive step
+  } else if (k == d - 1) {
     blk_copy(Ah, Y, (int64_t)m * r1);
     __syncthreads();
   } else {
@@ -1103,6 +1105,35 @@ __global__ void __launch_bounds__(kDenseThreads) k_project(DenseArgs a) {
       Ah[e] = Z[(int64_t)row * zld + bb] - acc;
     }
     __syncthreads();
+  }
+  if (a.proj_mode == 1) {
+    // adaptive step numerator: the W-norm of component k of the tangent
+    // vector, ||[U_1..Ahat_k..U_d]||_F^2 = tr(L(Ahat_k) P_k L(Ahat_k)^T) = ||L(Ahat_k) chol(P_k)||^2
+    // (left part orthonormal; P_d = [1]); fixed-order CTA reduction
+    double acc = 0.0;
+    const double* Lk = a.L + a.p_off[k];
+    for (int row = threadIdx.x; row < m; row += blockDim.x) {
+      const double* ar = Ah + (int64_t)row * r1;
+      if (k == d - 1) {
+        for (int c = 0; c < r1; ++c) acc = fma(ar[c], ar[c], acc);
+      } else {
+        for (int c = 0; c < r1; ++c) {
+          double v = 0.0;
+          for (int i = c; i < r1; ++i) v = fma(ar[i], Lk[i * r1 + c], v);
+          acc = fma(v, v, acc);
+        }
+      }
+    }
+    double* red = smraw;
+    __syncthreads();
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+      if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) sc->adapt_num[k] = red[0];
+    return;
   }
   // A11 + A13: B_k from Ttil = U/phi and X = -alpha Ahat/phi
   const double* ph = a.phi + a.phi_off[k];
@@ -1302,6 +1333,19 @@ void launch_dense_round(cudaStream_t s, const DenseArgs& a, int64_t* launches) {
   k_project<<<a.d, kDenseThreads, bytes, s>>>(a);
   if (!(a.clw && launch_round_cs(s, a, bytes))) k_dense_round<<<1, kDenseThreads, bytes, s>>>(a);
   *launches += 2;
+}
+
+void launch_project(cudaStream_t s, const DenseArgs& a, int mode, int64_t* launches) {
+  DenseArgs b = a;
+  b.proj_mode = mode;
+  k_project<<<b.d, kDenseThreads, (size_t)b.smem_doubles * sizeof(double), s>>>(b);
+  ++*launches;
+}
+
+void launch_round_only(cudaStream_t s, const DenseArgs& a, int64_t* launches) {
+  const size_t bytes = (size_t)a.smem_doubles * sizeof(double);
+  if (!(a.clw && launch_round_cs(s, a, bytes))) k_dense_round<<<1, kDenseThreads, bytes, s>>>(a);
+  ++*launches;
 }
 
 }  // namespace prgd

@@ -43,6 +43,8 @@ struct SegDev {
   const int32_t* perm2;
   const double* rowtab;
   const double* coltab;
+  const double* rowtab2;  // DPASS second row / gathered tables
+  const double* coltab2;
   const double* rowscale;
   double* out;
 };
@@ -64,7 +66,8 @@ __device__ __forceinline__ double2 ld2(const double* p) {
 #endif
 template <int MODE>
 struct SegOcc {
-  static constexpr int v = MODE == kSDDMM ? PRGD_SEG_OCC_SDDMM : (MODE == kSPMM ? PRGD_SEG_OCC_SPMM : 8);
+  static constexpr int v = (MODE == kSDDMM || MODE == kDPASS) ? PRGD_SEG_OCC_SDDMM
+                                                             : (MODE == kSPMM ? PRGD_SEG_OCC_SPMM : 8);
 };
 
 template <int LPS, int MODE>
@@ -85,8 +88,9 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
     const int64_t trow = row % a.nrow_real;
     const int64_t beg = a.vrow_begin[v];
     const int cnt = a.vrow_cnt[v];
-    double2 rv = make_double2(0.0, 0.0);
-    if (MODE == kSDDMM) rv = ld2(a.rowtab + trow * ld + 2 * sub);
+    double2 rv = make_double2(0.0, 0.0), rv2 = make_double2(0.0, 0.0);
+    if (MODE == kSDDMM || MODE == kDPASS) rv = ld2(a.rowtab + trow * ld + 2 * sub);
+    if (MODE == kDPASS) rv2 = ld2(a.rowtab2 + trow * ld + 2 * sub);
     double accs = 0.0;
     double2 accv = make_double2(0.0, 0.0);
     for (int c0 = 0; c0 < cnt; c0 += 32) {
@@ -101,7 +105,7 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
         if (MODE == kSDDMM) {
           xv = a.y[s];
           if (a.g2) p2v = a.perm2[s];
-        } else {
+        } else if (MODE != kDPASS) {
           xv = a.perm ? a.g[a.perm[s]] : a.g[s];
         }
       }
@@ -112,7 +116,7 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
       }
 #pragma unroll
       for (int st0 = 0; st0 < STEPS; st0 += UNR) {
-        double2 b[UNR];
+        double2 b[UNR], b2[MODE == kDPASS ? UNR : 1];
         double xs[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
@@ -121,6 +125,10 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
           xs[u] = __shfl_sync(kFull, xv, t & 31);
           b[u] = make_double2(0.0, 0.0);
           if (t < nc) b[u] = ld2(a.coltab + (int64_t)cidx * ld + 2 * sub);
+          if constexpr (MODE == kDPASS) {
+            b2[u] = make_double2(0.0, 0.0);
+            if (t < nc) b2[u] = ld2(a.coltab2 + (int64_t)cidx * ld + 2 * sub);
+          }
         }
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
@@ -138,6 +146,14 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
                 accs = fma(gv, gv, accs);
               }
             }
+          } else if constexpr (MODE == kDPASS) {
+            // D(x_s) = rowtab.coltab + rowtab2.coltab2 (tangent vector at the sample)
+            double part = fma(rv.x, b[u].x, rv.y * b[u].y);
+            part = fma(rv2.x, b2[u].x, part);
+            part = fma(rv2.y, b2[u].y, part);
+#pragma unroll
+            for (int o = LPS / 2; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
+            if (t < nc && sub == 0) accs = fma(part, part, accs);
           } else {
             if (t < nc) {
               accv.x = fma(xs[u], b[u].x, accv.x);
@@ -155,7 +171,7 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
         if (pslot < 0) a.out[row] = accs;
         else a.part[pslot] = accs;
       }
-    } else if (MODE == kSDDMM) {
+    } else if (MODE == kSDDMM || MODE == kDPASS) {
 #pragma unroll
       for (int o = LPS; o < 32; o <<= 1) accs += __shfl_xor_sync(kFull, accs, o);
       if (lane == 0) {
@@ -433,6 +449,7 @@ template <int LPS>
 void seg_dispatch_mode(cudaStream_t s, int mode, const SegDev& dv, unsigned grid,
                        const Scalars* sc) {
   if (mode == kSDDMM) k_seg<LPS, kSDDMM><<<grid, 256, 0, s>>>(dv, sc);
+  else if (mode == kDPASS) k_seg<LPS, kDPASS><<<grid, 256, 0, s>>>(dv, sc);
   else if (mode == kGSQ) k_seg<1, kGSQ><<<grid, 256, 0, s>>>(dv, sc);
   else k_seg<LPS, kSPMM><<<grid, 256, 0, s>>>(dv, sc);
 }
@@ -462,6 +479,8 @@ void launch_seg(cudaStream_t s, const SegArgs& a, const Scalars* sc, int64_t* la
   dv.perm2 = a.perm2;
   dv.rowtab = a.rowtab;
   dv.coltab = a.coltab;
+  dv.rowtab2 = a.rowtab2;
+  dv.coltab2 = a.coltab2;
   dv.rowscale = a.rowscale;
   dv.out = a.out;
   const int vec = a.mode == kSPMM ? 1 : 0;

@@ -35,6 +35,8 @@ struct Scalars {
   int index_err;     // set by index validation kernels
   int pad;          // cumulative one-sided Jacobi sweeps (diagnostic)
   long long cyc[24]; // cumulative SM cycles / counters per dense phase (diagnostic)
+  double adapt_num[kMaxD];  // adaptive step: ||component k of the tangent vector||_W^2
+  double adapt_den;         // adaptive step: ||P_Omega D||^2 (this rank's samples)
 };
 
 enum ErrBits { kErrNaN = 1, kErrChol = 2, kErrSVD = 4 };
@@ -83,6 +85,7 @@ struct DenseArgs {
   int64_t clw_len;
   Scalars* sc;
   int smem_doubles;  // dynamic shared memory available to the kernel, in doubles
+  int proj_mode;     // k_project: 0 project + assemble, 1 project + adaptive numerator, 2 assemble
 };
 
 // ------------------------------------------------------------------ kernels (launchers)
@@ -209,7 +212,7 @@ void launch_scale_rows(cudaStream_t s, const double* in, const double* f, int64_
 void passes_mid_init();
 
 // passes.cu
-enum SegMode { kSDDMM = 0, kGSQ = 1, kSPMM = 2 };
+enum SegMode { kSDDMM = 0, kGSQ = 1, kSPMM = 2, kDPASS = 3 };
 struct SegArgs {
   const SegPlan* plan;  // host copy (device pointers inside)
   int mode;
@@ -222,8 +225,10 @@ struct SegArgs {
   const int32_t* perm2 = nullptr;
   const double* rowtab; // SDDMM row vectors
   const double* coltab; // gathered table
+  const double* rowtab2 = nullptr;  // DPASS: v_s = rowtab.coltab + rowtab2.coltab2
+  const double* coltab2 = nullptr;
   const double* rowscale;  // SPMM output scale (psi) or null
-  double* out;          // SDDMM/GSQ: scalar per row; SPMM: vector per row (ld)
+  double* out;          // SDDMM/GSQ/DPASS: scalar per row; SPMM: vector per row (ld)
 };
 void launch_seg(cudaStream_t s, const SegArgs& a, const Scalars* sc, int64_t* launches);
 // n_host / phi_off_host are HOST arrays (values are passed by kernel argument).
@@ -246,6 +251,23 @@ void launch_gather_sq_sum(cudaStream_t s, const double* h0, int n0, Scalars* sc,
 // dense.cu
 void launch_dense_orth(cudaStream_t s, const DenseArgs& a, int64_t* launches);
 void launch_dense_round(cudaStream_t s, const DenseArgs& a, int64_t* launches);
+// k_project alone (mode: 1 projection + adaptive numerator, 2 assembly with sc->alpha) and the
+// rounding alone (adaptive step: alpha is known only after the D pass)
+void launch_project(cudaStream_t s, const DenseArgs& a, int mode, int64_t* launches);
+void launch_round_only(cudaStream_t s, const DenseArgs& a, int64_t* launches);
+
+// adaptive.cu: the adaptive (steepest) step
+void launch_stack_cores(cudaStream_t s, int d, const int* n, const int* r, const int64_t* core_off,
+                        int KL, const double* U, const double* Ahat, double* st, const Scalars* sc,
+                        int64_t* launches);
+void launch_concat2(cudaStream_t s, double* o0, int ldo0, const double* x0, int ldx0, const double* y0,
+                    int ldy0, int64_t rows0, int w0, double* o1, int ldo1, const double* x1, int ldx1,
+                    const double* y1, int ldy1, int64_t rows1, int w1, const Scalars* sc,
+                    int64_t* launches);
+int adapt_vsum_parts();
+void launch_adapt_den(cudaStream_t s, const double* x, int64_t n, double* part, Scalars* sc,
+                      int64_t* launches);
+void launch_adapt_alpha(cudaStream_t s, int d, Scalars* sc, int64_t* launches);
 int dense_smem_doubles();
 int round_cluster_size();
 bool round_cluster_ok(int d, const int* r);   // cluster rounding applies (2 max r <= 32)

@@ -147,6 +147,27 @@ def test_rules_rgd_fixed_raw(pkg):
         ctx.close()
 
 
+# Adaptive (steepest) step, PAPER.md:236-238 (and RGD's, 150-152, with eps_rule "none"): one
+# more pass over Omega (the tangent vector at every sample).  Configs 1-3 and a config-5
+# subsample: every table level shape, split buckets and the DMMA / fallback table kernels.
+@pytest.mark.parametrize("cfg,m,eps_rule", [(1, None, "vee"), (2, 50_000, "vee"), (2, 50_000, "none"),
+                                            (3, 100_000, "vee"), (5, 200_000, "vee")])
+def test_adaptive_step_matches_oracle(pkg, cfg, m, eps_rule):
+    pr, y, init = problem(cfg, m)
+    ctx = context(pkg, pr, y, init)
+    ctx.set_metric(eps_rule, 0.0, "adaptive")
+    T = init
+    for it in range(3):
+        ctx.step(1.0)
+        T, info = oracle.prgd_step(T, pr.idx, y, pr.n, pr.r, 1.0, eps_rule=eps_rule,
+                                   step_rule="adaptive", return_info=True)
+        alpha = ctx.debug("eps")[2]
+        assert abs(alpha - info["alpha"]) <= 1e-10 * info["alpha"], (it, alpha, info["alpha"])
+        err = oracle.tt_diff_norm(ctx.get_cores(), T)
+        assert err <= 1e-10, (it, err)
+    ctx.close()
+
+
 def test_exact_fit_is_noop_and_edge_cases(pkg):
     pr, _, init = problem(1)
     # Integer cores: every chain product is exact in fp64 in any order, so G = 0

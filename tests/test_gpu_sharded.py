@@ -45,8 +45,9 @@ class PairAllreduce:
         return call
 
 
-@pytest.mark.parametrize("cfg,m,steps", [(2, 20000, 3), (5, 60000, 2)])
-def test_sharded_two_contexts_match_oracle(cfg, m, steps):
+@pytest.mark.parametrize("cfg,m,steps,rule", [(2, 20000, 3, "theory"), (5, 60000, 2, "theory"),
+                                              (2, 20000, 2, "adaptive")])
+def test_sharded_two_contexts_match_oracle(cfg, m, steps, rule):
     import paper_2501_13385_b200 as pkg
     pkg.load()
     pr = synth.make_problem(cfg, m=m)
@@ -57,6 +58,7 @@ def test_sharded_two_contexts_match_oracle(cfg, m, steps):
     ctxs = []
     for rank in range(2):
         c = pkg.TTContext(pr.n, pr.r)
+        c.set_metric("vee", 0.0, rule)
         c.set_allreduce(ar.fn(rank), pr.m)
         c.set_observations(pr.idx[rank::2], y[rank::2])
         c.set_cores(init)
@@ -82,7 +84,7 @@ def test_sharded_two_contexts_match_oracle(cfg, m, steps):
     assert not errs, errs
     ref = init
     for _ in range(steps):
-        ref = oracle.prgd_step(ref, pr.idx, y, pr.n, pr.r, 1.0)
+        ref = oracle.prgd_step(ref, pr.idx, y, pr.n, pr.r, 1.0, step_rule=rule)
     for rank in range(2):
         assert oracle.tt_diff_norm(res[rank][0], ref) <= 1e-11
     for a, b in zip(res[0][0], res[1][0]):

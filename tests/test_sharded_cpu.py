@@ -26,9 +26,10 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def sharded_step(cores, idx, y, n, r, step_size, m_global, allreduce):
+def sharded_step(cores, idx, y, n, r, step_size, m_global, allreduce, step_rule="theory"):
     """One PRGD step where idx / y are this rank's shard; allreduce(np.ndarray) sums in place
-    over ranks.  Mirrors tt_prgd_step in sharded mode."""
+    over ranks.  Mirrors tt_prgd_step in sharded mode (adaptive rule: a third exchange, the
+    denominator ||P_Omega D||^2)."""
     d = len(n)
     p = m_global / math.prod(n)
     g = oracle.residual(cores, idx, y)
@@ -49,12 +50,19 @@ def sharded_step(cores, idx, y, n, r, step_size, m_global, allreduce):
     offs = np.cumsum([0] + [yk.size for yk in Y])
     Y = [flat[offs[k]:offs[k + 1]].reshape(Y[k].shape) for k in range(d)]
     Ahat = oracle.project(U, P, Y)
-    alpha = oracle.step_length(step_size, eps, p, "theory")
-    B = oracle.assemble(oracle.unweight(U, phi), oracle.unweight(Ahat, phi), alpha)
+    Ttil, A = oracle.unweight(U, phi), oracle.unweight(Ahat, phi)
+    if step_rule == "adaptive":
+        _, num, den = oracle.adaptive_step(1.0, U, Ahat, Ttil, A, idx)   # den: this shard only
+        buf = np.array([den])
+        allreduce(buf)                                          # exchange 3: den
+        alpha = step_size * num / buf[0] if buf[0] > 0 else 0.0
+    else:
+        alpha = oracle.step_length(step_size, eps, p, "theory")
+    B = oracle.assemble(Ttil, A, alpha)
     return oracle.tt_round(B, r)
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, step_rule="theory"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -70,23 +78,25 @@ def _worker(rank, world, port, out):
 
         cores = init
         for _ in range(3):
-            cores = sharded_step(cores, pr.idx[shard], y[shard], pr.n, pr.r, 1.0, pr.m, allreduce)
+            cores = sharded_step(cores, pr.idx[shard], y[shard], pr.n, pr.r, 1.0, pr.m, allreduce,
+                                 step_rule)
         out[rank] = np.concatenate([c.ravel() for c in cores])
     finally:
         dist.destroy_process_group()
 
 
-def test_sharded_step_matches_single_process():
+@pytest.mark.parametrize("step_rule", ["theory", "adaptive"])
+def test_sharded_step_matches_single_process(step_rule):
     world = 2
     port = _free_port()
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, out, step_rule), nprocs=world, join=True)
     pr = synth.make_problem(2, m=4000)
     y = oracle.eval_at(pr.truth, pr.idx) + 1e-3 * pr.noise_unit
     ref = pr.init
     for _ in range(3):
-        ref = oracle.prgd_step(ref, pr.idx, y, pr.n, pr.r, 1.0)
+        ref = oracle.prgd_step(ref, pr.idx, y, pr.n, pr.r, 1.0, step_rule=step_rule)
     offs = np.cumsum([0] + [c.size for c in ref])
     for rank in range(world):
         got = [out[rank][offs[k]:offs[k + 1]].reshape(ref[k].shape) for k in range(len(ref))]
