@@ -23,6 +23,15 @@ Recipes (BASELINE.json:7-11):
         40-bit code with duplicates removed keeping first occurrence (sample
         order left random), noise sigma = 1e-4 * RMS.
 
+Beyond BASELINE's five (the paper's QST workload shape):
+  cfg6  Pauli-measurement tensor of n = 10 qubits: a random complex MPS u of bond 2
+        (complex Gaussian cores, normalised so tr(rho) = ||u||^2 = 1), rho = u u^dagger,
+        T*(a) = sum_{i,j} rho(i, j) W_a(i, j) with W_a = sigma_{a_1} x ... x sigma_{a_n}
+        (Y_k(:, alpha, :) = sum_{i,j} X_k(:, i, j, :) sigma_alpha(i, j), PAPER.md:633), held as a
+        REAL TT of ranks s_k^2 = 4 (mode size 4) by writing each bond's Hermitian s x s
+        environment in an orthonormal Hermitian basis; OS = 200 (80,000 of 4^10 = 7.63%,
+        PAPER.md:635) without replacement, no noise, perturbed-truth init.
+
 RMS for relative noise is the root mean square of the clean observed values
 (an unbiased estimate of ||T*||_F / sqrt(N*) under uniform sampling); the
 consumer computes it, since it needs T*(Omega).
@@ -129,7 +138,7 @@ def _sq_norm_tt(cores):
 def make_problem(cfg: int, seed: Optional[int] = None, m: Optional[int] = None,
                  n: Optional[tuple] = None, r: Optional[tuple] = None, rank: int = 0,
                  world: int = 1) -> Problem:
-    """Build config `cfg` (1..5).  `m`, `n`, `r` override sizes for reduced test
+    """Build config `cfg` (1..5, and 6 = the QST workload shape).  `m`, `n`, `r` override sizes for reduced test
     variants (same recipe, same value distributions).  With world > 1 (config 5, sharded
     multi-GPU runs) the truth and the init are those of `seed`, and rank `rank` draws its
     own m multi-indices from the residue class lin = rank (mod world) of the linear index,
@@ -214,4 +223,71 @@ def make_problem(cfg: int, seed: Optional[int] = None, m: Optional[int] = None,
         init = _perturb(rng, truth, 0.1 / math.sqrt(d))
         meta.update(draws=draws, duplicates=draws - idx.shape[0], rank=rank, world=world)
         return Problem(cfg, n, r, truth, idx, z, "rel", 1e-4, init, 50, meta)
+    if cfg == 6:
+        d = 10 if n is None else len(n)
+        n = (4,) * d
+        s_b = mps_ranks(d, 2)                                  # bond dims of the state, qubits
+        r = tuple(b * b for b in s_b)
+        truth, mps = _pauli_tt(rng, s_b)
+        nstar = math.prod(n)
+        if m is None:   # OS = 200 x manifold dimension
+            dim = sum(r[k] * n[k] * r[k + 1] for k in range(d)) - sum(r[k] ** 2 for k in range(1, d))
+            m = 200 * dim
+        idx = _unravel(rng.choice(nstar, size=m, replace=False), n)
+        init = _perturb(rng, truth, 0.1 / math.sqrt(d))
+        meta.update(state_bond=s_b, mps=mps)
+        return Problem(cfg, n, r, truth, idx, None, None, 0.0, init, 200, meta)
     raise ValueError(f"unknown config {cfg}")
+
+
+# Pauli matrices in the paper's order sigma_1..sigma_4 = I, X, Y, Z
+PAULI = np.array([[[1, 0], [0, 1]], [[0, 1], [1, 0]], [[0, -1j], [1j, 0]], [[1, 0], [0, -1]]],
+                 dtype=np.complex128)
+
+
+def _herm_basis(s: int) -> np.ndarray:
+    """Orthonormal basis (under <A, B> = tr(A B)) of the real space of Hermitian s x s matrices:
+    E_ii, (E_ij + E_ji)/sqrt(2), i(E_ij - E_ji)/sqrt(2) for i < j.  [s*s, s, s]."""
+    out = []
+    for i in range(s):
+        e = np.zeros((s, s), dtype=np.complex128)
+        e[i, i] = 1.0
+        out.append(e)
+    for i in range(s):
+        for j in range(i + 1, s):
+            e = np.zeros((s, s), dtype=np.complex128)
+            e[i, j] = e[j, i] = 1.0 / math.sqrt(2.0)
+            out.append(e)
+            e = np.zeros((s, s), dtype=np.complex128)
+            e[i, j], e[j, i] = 1j / math.sqrt(2.0), -1j / math.sqrt(2.0)
+            out.append(e)
+    return np.array(out)
+
+
+def _pauli_tt(rng, s_b) -> List[np.ndarray]:
+    """Real TT of the Pauli-measurement tensor of rho = u u^dagger (config 6).  With the left
+    environment E_k = sum_{i,j} sigma_a(i,j) U_k(:,i,:)^T E_{k-1} conj(U_k(:,j,:)) (Hermitian,
+    E_0 = [1], T*(a) = E_d), core k maps the real coordinates h_m = tr(B_m E_{k-1}) to those of
+    E_k: core[m, a, q] = tr(B'_q F_a(B_m)), a real linear map since F_a keeps Hermiticity."""
+    d = len(s_b) - 1
+    U = [(rng.standard_normal((s_b[k], 2, s_b[k + 1])) + 1j * rng.standard_normal((s_b[k], 2, s_b[k + 1])))
+         / math.sqrt(2.0) for k in range(d)]
+    # ||u||^2 by the transfer-matrix recursion; scale so tr(rho) = 1
+    g = np.ones((1, 1), dtype=np.complex128)
+    for c in U:
+        g = np.einsum("ab,aic,bid->cd", g, c, np.conj(c))
+    U[0] = U[0] / math.sqrt(float(g[0, 0].real))
+    cores = []
+    for k in range(d):
+        Bin, Bout = _herm_basis(s_b[k]), _herm_basis(s_b[k + 1])
+        core = np.empty((Bin.shape[0], 4, Bout.shape[0]))
+        for a in range(4):
+            for mm in range(Bin.shape[0]):
+                F = np.zeros((s_b[k + 1], s_b[k + 1]), dtype=np.complex128)
+                for i in range(2):
+                    for j in range(2):
+                        if PAULI[a, i, j] != 0:
+                            F += PAULI[a, i, j] * (U[k][:, i, :].T @ Bin[mm] @ np.conj(U[k][:, j, :]))
+                core[mm, a, :] = np.einsum("qxy,yx->q", Bout, F).real
+        cores.append(core)
+    return cores, U

@@ -43,6 +43,7 @@ CASES = [
     (3, 200_000, {}),
     (4, 200_000, {}),
     (5, 400_000, {}),
+    (6, None, {}),     # QST workload shape: d=10, n=4, r=4, 80,000 samples
 ]
 
 
@@ -117,7 +118,7 @@ def test_one_step_parity(pkg, cfg, m, kw):
     ctx.close()
 
 
-@pytest.mark.parametrize("cfg,m,steps", [(1, None, 50), (2, None, 50), (4, 100_000, 50)])
+@pytest.mark.parametrize("cfg,m,steps", [(1, None, 50), (2, None, 50), (4, 100_000, 50), (6, None, 50)])
 def test_many_steps_parity(pkg, cfg, m, steps):
     pr, y, init = problem(cfg, m)
     ctx = context(pkg, pr, y, init)
@@ -151,6 +152,7 @@ def test_rules_rgd_fixed_raw(pkg):
 # more pass over Omega (the tangent vector at every sample).  Configs 1-3 and a config-5
 # subsample: every table level shape, split buckets and the DMMA / fallback table kernels.
 @pytest.mark.parametrize("cfg,m,eps_rule", [(1, None, "vee"), (2, 50_000, "vee"), (2, 50_000, "none"),
+                                            (6, None, "vee"), (6, None, "none"),
                                             (3, 100_000, "vee"), (5, 200_000, "vee")])
 def test_adaptive_step_matches_oracle(pkg, cfg, m, eps_rule):
     pr, y, init = problem(cfg, m)
