@@ -123,6 +123,17 @@ PRGD_API int tt_get_core(tt_ctx* ctx, int k, double* h_core_out);
  * its buffers here (TT_ERR_OOM; TT_ERR_RANK if some 2 r_k > 32). */
 PRGD_API int tt_set_metric(tt_ctx* ctx, int eps_rule, double eps, int step_rule);
 
+/* Spectral initialisation at scale: set every core to
+ * T_0 = SVD_r^tt(p^{-1} P_Omega(y)), Alg. 1 (TT-SVD) applied to the sparse
+ * zero-filled, rescaled observations (the "TT-SVD spectral initialization" of PAPER.md:42;
+ * BASELINE.json config 1) without densifying it: step k takes the top r_k eigenvectors of the
+ * Gram of the projected unfolding, accumulated over the samples grouped by (x_{k+1..d}, x_k)
+ * (DESIGN.md §2).  Gram-based, so the kept subspace is accurate to ~u ||G|| / eigen-gap.
+ * Needs observations (TT_ERR_STATE otherwise, and in sharded mode), prod(n) < 2^62 and
+ * r_{k-1} n_k <= 1024 for k < d (TT_ERR_ARG).  Synchronous.  Output cores 0..d-2 have
+ * orthonormal columns L(T_k). */
+PRGD_API int tt_spectral_init(tt_ctx* ctx);
+
 /* ------------------------------------------------------------------ the hot path */
 
 /* One PRGD iteration (Alg. 2; no Trim):

@@ -78,6 +78,7 @@ def load() -> ctypes.CDLL:
                                    i64p, i64p]),
         "tt_plan_layout": (ctypes.c_int, [ctypes.c_int, i64p, i64p, ctypes.POINTER(ctypes.c_int),
                                           ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
+        "tt_spectral_init": (ctypes.c_int, [P]),
         "tt_set_allreduce": (ctypes.c_int, [P, ALLREDUCE_FN, P, ctypes.c_int64]),
         "tt_get_stats": (ctypes.c_int, [P, ctypes.POINTER(_Stats)]),
         "tt_set_profiling": (ctypes.c_int, [P, ctypes.c_int]),
@@ -242,6 +243,10 @@ class TTContext:
 
     def get_cores(self):
         return [self.get_core(k) for k in range(self.d)]
+
+    def spectral_init(self):
+        """Cores <- SVD_r^tt(p^{-1} P_Omega(y)) computed on the GPU (tt_spectral_init)."""
+        self._check(self.lib.tt_spectral_init(self._h), "tt_spectral_init")
 
     def set_metric(self, eps_rule: str = "vee", eps: float = 0.0, step_rule: str = "theory"):
         self._check(self.lib.tt_set_metric(self._h, EPS_RULES[eps_rule], float(eps),

@@ -1217,6 +1217,79 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
   return TT_OK;
 }
 
+int tt_spectral_init(tt_ctx* ctx) {
+  if (!ctx) return TT_ERR_ARG;
+  if (!ctx->obs_set || ctx->m <= 0) return fail(ctx, TT_ERR_STATE, "spectral init needs a nonempty Omega");
+  if (ctx->allreduce) return fail(ctx, TT_ERR_STATE, "spectral init is single-rank (sharded mode set)");
+  if (ctx->plan.mid) return fail(ctx, TT_ERR_STATE, "spectral init not available with the middle-split layout");
+  const int d = ctx->d;
+  long double nstar = 1;
+  int Wmax = 1, cs = 1;
+  for (int k = 0; k < d; ++k) {
+    nstar *= (long double)ctx->n[k];
+    Wmax = std::max<int>(Wmax, (int)(ctx->r[k] * ctx->n[k]));
+    cs = std::max<int>(cs, (int)ctx->r[k + 1]);
+  }
+  if (nstar >= (long double)(1ull << 62)) return fail(ctx, TT_ERR_ARG, "spectral init needs prod(n) < 2^62");
+  int64_t Wuse = 1;
+  for (int k = 0; k + 1 < d; ++k) Wuse = std::max<int64_t>(Wuse, ctx->r[k] * ctx->n[k]);
+  if (Wuse > 1024) return fail(ctx, TT_ERR_ARG, "spectral init needs r_{k-1} n_k <= 1024 for k < d");
+  for (int k = 0; k + 1 < d; ++k)
+    if ((ctx->r[k] <= 8 ? 64 : (ctx->r[k] <= 16 ? 256 : 1024)) * ctx->n[k] > 25 * 1024)
+      return fail(ctx, TT_ERR_ARG, "spectral init needs pad(r_{k-1})^2 n_k <= 25600");
+  int rc = ensure_base(ctx);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  const int64_t m = ctx->m;
+  SpectralArgs a{};
+  a.d = d;
+  a.KL = ctx->plan.KL;
+  for (int k = 0; k < d; ++k) a.n[k] = (int)ctx->n[k];
+  for (int k = 0; k <= d; ++k) {
+    a.r[k] = (int)ctx->r[k];
+    a.core_off[k] = ctx->core_off[k];
+  }
+  a.m = m;
+  a.NL = ctx->plan.NL;
+  a.nrows = ctx->plan.NL * ctx->plan.nbL;
+  a.p = ctx->p;
+  a.offsL = ctx->offsL;
+  a.Spre = ctx->Spre;
+  a.y = ctx->ypre;
+  a.C = ctx->C;
+  a.cs = cs;
+  a.hist_len = radix_hist_len(m);
+  a.gram_parts_cap = std::max<int64_t>((int64_t)1 << 28, Wuse * Wuse);
+  std::vector<void*> tmp;
+  bool ok = A(ctx, &a.Ppos, m, tmp) && A(ctx, &a.z, m, tmp) && A(ctx, &a.chain, m * cs, tmp) &&
+            A(ctx, &a.w, m * cs, tmp) && A(ctx, &a.keys, m, tmp) && A(ctx, &a.ktmp, m, tmp) &&
+            A(ctx, &a.vals, m, tmp) && A(ctx, &a.vtmp, m, tmp) && A(ctx, &a.hist, a.hist_len, tmp) &&
+            A(ctx, &a.flag, m, tmp) && A(ctx, &a.rx, m, tmp) && A(ctx, &a.gflag, m, tmp) &&
+            A(ctx, &a.ridx, m + 1, tmp) && A(ctx, &a.rstart, m + 1, tmp) && A(ctx, &a.gidx, m + 1, tmp) &&
+            A(ctx, &a.gstart, m + 1, tmp) && A(ctx, &a.rgroup, m + 1, tmp) && A(ctx, &a.byx, m + 1, tmp) &&
+            A(ctx, &a.xoff, Wmax + 2, tmp) && A(ctx, &a.bsum, plan_scan_scratch(m + 1), tmp) &&
+            A(ctx, &a.lflag, m, tmp) && A(ctx, &a.lnch, m, tmp) && A(ctx, &a.lidx, m + 1, tmp) &&
+            A(ctx, &a.llist, m + 1, tmp) && A(ctx, &a.lchoff, m + 1, tmp) && A(ctx, &a.lchl, m + 1, tmp) &&
+            A(ctx, &a.gparts, a.gram_parts_cap, tmp) && A(ctx, &a.G, Wuse * Wuse, tmp) &&
+            A(ctx, &a.V, Wuse * Wuse, tmp);
+  if (!ok) {
+    dfree_all(ctx, tmp);
+    return fail(ctx, TT_ERR_OOM, "device allocation failed (spectral init)");
+  }
+  std::string msg;
+  int64_t lc = 0;
+  rc = spectral_init_run(ctx->stream, a, &msg, &lc);
+  ctx->launches += lc;
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  dfree_all(ctx, tmp);
+  if (rc) return fail(ctx, rc, msg);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "spectral init");
+  for (auto& c : ctx->core_set) c = 1;
+  ctx->evalValid = false;
+  ctx->tablesC = false;
+  return TT_OK;
+}
+
 int tt_prgd_step(tt_ctx* ctx, double step_size) {
   if (!ctx) return TT_ERR_ARG;
   const int64_t mtot = ctx->allreduce ? ctx->m_global : ctx->m;

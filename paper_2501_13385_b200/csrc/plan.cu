@@ -181,6 +181,11 @@ void scan_i32(cudaStream_t s, const int* in, int64_t len, int64_t* out, long lon
 
 int64_t plan_scan_scratch(int64_t len) { return (len + kSeg - 1) / kSeg + 2; }
 
+void launch_scan_i32(cudaStream_t s, const int* in, int64_t len, int64_t* out, long long* bsum,
+                     int64_t* launches) {
+  scan_i32(s, in, len, out, bsum, launches);
+}
+
 void launch_plan_rows(cudaStream_t s, const int64_t* offs, int64_t nr, int64_t split, int* nv, int* sp,
                       int* np, int64_t* vbase, int64_t* sbase, int64_t* pbase, long long* bsum,
                       int64_t* launches) {

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string>
 #include <vector>
 
 namespace prgd {
@@ -109,6 +110,9 @@ void launch_after_sort_suf(cudaStream_t s, const uint64_t* keys, const uint32_t*
 
 // plan.cu: device construction of the pass work plans (SegPlan)
 int64_t plan_scan_scratch(int64_t len);
+// exclusive scan of int32 into int64 out[0..len] (out[len] = total); bsum: plan_scan_scratch(len)
+void launch_scan_i32(cudaStream_t s, const int* in, int64_t len, int64_t* out, long long* bsum,
+                     int64_t* launches);
 void launch_plan_rows(cudaStream_t s, const int64_t* offs, int64_t nr, int64_t split, int* nv, int* sp,
                       int* np, int64_t* vbase, int64_t* sbase, int64_t* pbase, long long* bsum,
                       int64_t* launches);
@@ -255,6 +259,36 @@ void launch_dense_round(cudaStream_t s, const DenseArgs& a, int64_t* launches);
 // rounding alone (adaptive step: alpha is known only after the D pass)
 void launch_project(cudaStream_t s, const DenseArgs& a, int mode, int64_t* launches);
 void launch_round_only(cudaStream_t s, const DenseArgs& a, int64_t* launches);
+
+// spectral.cu: spectral initialisation T_0 = SVD_r^tt(p^{-1} P_Omega(y)) (Alg. 1 on the sparse tensor)
+struct SpectralArgs {
+  int d, KL;
+  int n[kMaxD];
+  int r[kMaxD + 1];
+  int64_t core_off[kMaxD + 1];
+  int64_t m, NL, nrows;       // nrows = NL * nb_L (virtual prefix rows)
+  double p;
+  const int64_t* offsL;       // [nrows + 1]
+  const int32_t* Spre;        // [m] suffix index per prefix position
+  const double* y;            // [m] observed values, prefix order
+  double* C;                  // output cores
+  int cs;                     // per-sample chain stride (>= max r)
+  int32_t* Ppos;
+  double *z, *chain, *w;
+  uint64_t *keys, *ktmp;
+  uint32_t *vals, *vtmp;
+  int* hist;
+  int64_t hist_len;
+  int *flag, *rx, *gflag;
+  int64_t *ridx, *rstart, *gidx, *gstart, *rgroup, *byx, *xoff;
+  int *lflag, *lnch;                  // long runs: flags, chunk counts
+  int64_t *lidx, *llist, *lchoff, *lchl;
+  long long* bsum;
+  double* gparts;
+  int64_t gram_parts_cap;     // doubles in gparts
+  double *G, *V;              // W_max^2 each
+};
+int spectral_init_run(cudaStream_t s, const SpectralArgs& a, std::string* msg, int64_t* launches);
 
 // adaptive.cu: the adaptive (steepest) step
 void launch_stack_cores(cudaStream_t s, int d, const int* n, const int* r, const int64_t* core_off,

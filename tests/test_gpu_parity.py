@@ -170,6 +170,32 @@ def test_adaptive_step_matches_oracle(pkg, cfg, m, eps_rule):
     ctx.close()
 
 
+# Spectral initialisation at scale: the GPU's sparse TT-SVD of
+# p^{-1} P_Omega(y) (Gram + Jacobi per mode, tt_spectral_init) against the oracle's dense
+# Alg. 1 (numpy SVD of the densified tensor) on shapes of configs 1, 2, 4, 5, 6.
+@pytest.mark.parametrize("cfg,kw", [(1, {}), (2, dict(n=(20, 20, 20, 20), m=40_000)),
+                                    (4, dict(n=(2,) * 14, m=3_000)),
+                                    (5, dict(n=(6,) * 6, r=(1, 4, 4, 4, 4, 4, 1), m=20_000)),
+                                    (6, {})])
+def test_spectral_init_matches_dense_tt_svd(pkg, cfg, kw):
+    pr = synth.make_problem(cfg, **kw)
+    y = pr.observations(oracle.eval_at(pr.truth, pr.idx))
+    ctx = pkg.TTContext(pr.n, pr.r)
+    ctx.set_observations(pr.idx, y)
+    ctx.spectral_init()
+    got = ctx.get_cores()
+    ref = oracle.spectral_init(pr.idx, y, pr.n, pr.r)
+    err = oracle.tt_diff_norm(got, ref)
+    assert err <= 1e-9, err
+    for k in range(pr.d - 1):                     # orthonormal columns (Alg. 1)
+        Lk = got[k].reshape(-1, got[k].shape[2])
+        np.testing.assert_allclose(Lk.T @ Lk, np.eye(Lk.shape[1]), atol=1e-12)
+    ctx.step(1.0)                                 # the init feeds the step
+    ref1 = oracle.prgd_step(got, pr.idx, y, pr.n, pr.r, 1.0)
+    assert oracle.tt_diff_norm(ctx.get_cores(), ref1) <= 1e-11
+    ctx.close()
+
+
 def test_exact_fit_is_noop_and_edge_cases(pkg):
     pr, _, init = problem(1)
     # Integer cores: every chain product is exact in fp64 in any order, so G = 0
