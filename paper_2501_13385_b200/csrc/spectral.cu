@@ -407,8 +407,8 @@ __global__ void __launch_bounds__(kJT) k_sp_jacobi(double* __restrict__ G, doubl
         for (int u = 0; u < kJU; ++u) {
           const int64_t e = e0 + (int64_t)u * kJT;
           on[u] = false;
-          if (e < tot) {
-            const int k = (int)(e / W), j = (int)(e - (int64_t)k * W);
+          if (e < tot) {   // row-major over (j, k): a warp touches one row j of G / V
+            const int j = (int)(e / np), k = (int)(e - (int64_t)j * np);
             on[u] = cs_s[k] != 0.0;
             ip[u] = (int64_t)j * W + pp[k];
             iq[u] = (int64_t)j * W + qq[k];
@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(kJT) k_sp_jacobi(double* __restrict__ G, doubl
 #pragma unroll
         for (int u = 0; u < kJU; ++u)
           if (on[u]) {
-            const int k = (int)((e0 + (int64_t)u * kJT) / W);
+            const int k = (int)((e0 + (int64_t)u * kJT) % np);
             const double c = cs_c[k], sn = cs_s[k];
             G[ip[u]] = c * gp[u] - sn * gq[u];
             G[iq[u]] = sn * gp[u] + c * gq[u];
