@@ -150,26 +150,50 @@ __global__ void k_scan_apply(int* __restrict__ hist, int64_t len, const long lon
     if (base + i < len) hist[base + i] = seg[i];
 }
 
-// Stable scatter: within a tile, warp w owns items [w*512, (w+1)*512) and walks them
-// 32 at a time in order; __match_any_sync ranks equal digits by lane.
-__global__ void k_rs_scatter(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-                             uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
-                             int64_t m, int shift, const int* __restrict__ hist,
-                             int64_t nblocks) {
+// Stable scatter through shared memory: the tile's items are first placed in digit order in
+// shared memory (warp w owns items [w*512, (w+1)*512) and walks them 32 at a time in order;
+// __match_any_sync ranks equal digits by lane), then written out in that order, so consecutive
+// threads write consecutive positions of each digit's output run (coalesced).
+constexpr size_t kRsScatterSmem = (size_t)kRsTile * (sizeof(uint64_t) + sizeof(uint32_t));
+__global__ void __launch_bounds__(kRsThreads) k_rs_scatter(const uint64_t* __restrict__ kin,
+                                                           const uint32_t* __restrict__ vin,
+                                                           uint64_t* __restrict__ kout,
+                                                           uint32_t* __restrict__ vout, int64_t m,
+                                                           int shift, const int* __restrict__ hist,
+                                                           int64_t nblocks) {
+  extern __shared__ uint64_t rs_sk[];                 // [kRsTile] keys, then [kRsTile] values
+  uint32_t* rs_sv = reinterpret_cast<uint32_t*>(rs_sk + kRsTile);
   __shared__ int wcnt[kRsWarps][257];
+  __shared__ int lstart[257], gbase[256];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < kRsWarps * 257; i += blockDim.x) (&wcnt[0][0])[i] = 0;
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kRsTile + (int64_t)w * kRsSub;
+  const int64_t tile0 = (int64_t)blockIdx.x * kRsTile;
+  const int64_t base = tile0 + (int64_t)w * kRsSub;
   for (int step = 0; step < kRsSub / 32; ++step) {
     int64_t t = base + step * 32 + lane;
     if (t < m) atomicAdd(&wcnt[w][(kin[t] >> shift) & 255u], 1);
   }
   __syncthreads();
-  for (int dg = threadIdx.x; dg < 256; dg += blockDim.x) {
-    int run = hist[(int64_t)dg * nblocks + blockIdx.x];
+  // per digit: tile total, then per-warp offsets inside the tile's digit run
+  if (threadIdx.x < 256) {
+    const int dg = threadIdx.x;
+    int tot = 0;
+    for (int w2 = 0; w2 < kRsWarps; ++w2) tot += wcnt[w2][dg];
+    lstart[dg + 1] = tot;
+    gbase[dg] = hist[(int64_t)dg * nblocks + blockIdx.x];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    lstart[0] = 0;
+    for (int dg = 0; dg < 256; ++dg) lstart[dg + 1] += lstart[dg];
+  }
+  __syncthreads();
+  if (threadIdx.x < 256) {
+    const int dg = threadIdx.x;
+    int run = lstart[dg];
     for (int w2 = 0; w2 < kRsWarps; ++w2) {
-      int c = wcnt[w2][dg];
+      const int c = wcnt[w2][dg];
       wcnt[w2][dg] = run;
       run += c;
     }
@@ -186,12 +210,21 @@ __global__ void k_rs_scatter(const uint64_t* __restrict__ kin, const uint32_t* _
     int leader = __ffs(peers) - 1;
     int pos = wcnt[w][dg];
     if (valid) {
-      kout[pos + rank] = key;
-      vout[pos + rank] = val;
+      rs_sk[pos + rank] = key;
+      rs_sv[pos + rank] = val;
     }
     __syncwarp();
     if (lane == leader) wcnt[w][dg] = pos + __popc(peers);
     __syncwarp();
+  }
+  __syncthreads();
+  const int n = (int)(m - tile0 < kRsTile ? m - tile0 : kRsTile);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint64_t key = rs_sk[i];
+    const int dg = (int)((key >> shift) & 255u);
+    const int64_t g = (int64_t)gbase[dg] + (i - lstart[dg]);
+    kout[g] = key;
+    vout[g] = rs_sv[i];
   }
 }
 
@@ -267,6 +300,11 @@ void radix_sort_pairs(cudaStream_t s, uint64_t* keys, uint32_t* vals, uint64_t* 
   uint64_t* ko = keys_tmp;
   uint32_t* vo = vals_tmp;
   if (m > 0) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_rs_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRsScatterSmem);
+      attr = true;
+    }
     int64_t nblocks = (m + kRsTile - 1) / kRsTile;
     (void)hist_len;
     for (int shift = 0; shift < bits; shift += 8) {
@@ -280,8 +318,8 @@ void radix_sort_pairs(cudaStream_t s, uint64_t* keys, uint32_t* vals, uint64_t* 
         k_scan_apply<<<nb, kScanThreads, 0, s>>>(hist, len, bsum);
         *launches += 2;
       }
-      k_rs_scatter<<<(unsigned)nblocks, kRsThreads, 0, s>>>(kin, vin, ko, vo, m, shift, hist,
-                                                            nblocks);
+      k_rs_scatter<<<(unsigned)nblocks, kRsThreads, kRsScatterSmem, s>>>(kin, vin, ko, vo, m, shift,
+                                                                         hist, nblocks);
       *launches += 3;
       uint64_t* tk = kin;
       kin = ko;
