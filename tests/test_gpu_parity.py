@@ -257,3 +257,32 @@ def test_single_sample_and_matrix_case(pkg):
     ref = oracle.prgd_step(cores, idx, y, n, r, 1.0)
     assert oracle.tt_diff_norm(ctx.get_cores(), ref) <= 1e-11
     ctx.close()
+
+
+def test_maximal_rank_and_rule_limits(pkg):
+    # r = 32 = kMaxRank: rank-2r = 64 unfoldings exceed the cluster sweeps' S <= 32 and take
+    # the single-CTA Householder path; the adaptive rule and the spectral init refuse such
+    # ranks with their documented status codes (include/prgd.h).
+    rng = np.random.default_rng(21)
+    n, r = (8, 40, 40, 8), (1, 8, 32, 8, 1)
+    truth = [rng.standard_normal((r[k], n[k], r[k + 1])) / math.sqrt(r[k + 1]) for k in range(4)]
+    N = math.prod(n)
+    lin = rng.choice(N, size=30_000, replace=False)
+    idx = np.stack(np.unravel_index(lin, n), axis=1).astype(np.int32)
+    y = oracle.eval_at(truth, idx)
+    init = [c + 0.05 * rng.standard_normal(c.shape) for c in truth]
+    ctx = pkg.TTContext(n, r)
+    ctx.set_observations(idx, y)
+    ctx.set_cores(init)
+    T = init
+    for _ in range(2):
+        ctx.step(1.0)
+        T = oracle.prgd_step(T, idx, y, n, r, 1.0)
+        assert oracle.tt_diff_norm(ctx.get_cores(), T) <= 1e-11
+    with pytest.raises(pkg.PRGDError) as ei:
+        ctx.set_metric("vee", 0.0, "adaptive")
+    assert ei.value.code == pkg.TT_ERR_RANK
+    with pytest.raises(pkg.PRGDError) as ei:
+        ctx.spectral_init()                       # r_1 n_2 = 320 ok, r_2 n_3 = 1280 > 1024
+    assert ei.value.code == pkg.TT_ERR_ARG
+    ctx.close()
