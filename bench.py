@@ -338,6 +338,10 @@ def main():
     roof = {"bound": "hbm", "kernel": dom_pass, "achieved": round(achieved, 1),
             "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
             "traffic": traffic, "peak_src": pk["src"],
+            # the kernel's measured DRAM traffic (ncu, profiles/traffic.json) over its live time:
+            # the gathers re-read table rows, so this exceeds the algorithmic bytes
+            "dram_gbs": round(traffic / t_dom / 1e9, 1) if traffic and t_dom > 0 else None,
+            "dram_frac": round(traffic / t_dom / 1e9 / pk["hbm_gbs"], 4) if traffic and t_dom > 0 else None,
             "share_of_step": round(per[dom_pass] / tot, 4) if tot else None,
             "group_ms": {k: round(v, 4) for k, v in per.items()},
             "dominant_group": dom}
