@@ -793,104 +793,8 @@ __device__ __noinline__ void col_norms_sorted(const double* X, int rows, int kc,
   __syncthreads();
 }
 
-// Truncation subspace of R (the top-rk left singular vectors of R, X = R^T): one-sided
-// Jacobi on the columns of X restricted to pairs across the current top-rk / bottom
-// groups (groups re-formed by norm before every sweep; bipartite round-robin rounds).
-// Rotations inside a group only change the gauge of the kept (or discarded) subspace,
-// so convergence of the cross pairs is exactly convergence of the truncation.  On
-// return perm[0..rk) lists the kept columns by decreasing norm; V accumulates rotations.
-__device__ bool jacobi_truncation(double* X, int rows, int kc, int rk, double* V, int* sweeps,
-                                  double* nrm, int* perm) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  __shared__ int s_rot;
-  for (int e = tid; e < kc * kc; e += blockDim.x) V[e] = (e / kc == e % kc) ? 1.0 : 0.0;
-  __syncthreads();
-  col_norms_sorted(X, rows, kc, nrm, perm);
-  if (kc <= rk) return true;
-  const int nb = kc - rk;
-  const int npairs = rk < nb ? rk : nb;
-  const int rounds = rk < nb ? nb : rk;
-  const double tol = 2.3e-16 * sqrt((double)(rows > 1 ? rows : 1));
-  const double tol2 = tol * tol;
-  for (int sweep = 0; sweep < 60; ++sweep) {
-    if (tid == 0) {
-      s_rot = 0;
-      if (sweeps) atomicAdd(sweeps, 1);
-    }
-    __syncthreads();
-    for (int round = 0; round < rounds; ++round) {
-      for (int pr = warp; pr < npairs; pr += nw) {
-        int ti, bi;
-        if (rk <= nb) { ti = pr; bi = (pr + round) % nb; }
-        else { bi = pr; ti = (pr + round) % rk; }
-        const int a = perm[ti], b = perm[rk + bi];
-        double* xa = X + (int64_t)a * rows;
-        double* xb = X + (int64_t)b * rows;
-        double ga = 0.0;
-        for (int i = lane; i < rows; i += 32) ga = fma(xa[i], xb[i], ga);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) ga += shx(ga, o);
-        const double al = nrm[a], be = nrm[b];
-        if (ga != 0.0 && ga * ga > tol2 * (al * be)) {
-          const double dlt = be - al;
-          const double sg = (dlt > 0.0 || (dlt == 0.0 && !signbit(dlt))) ? 1.0 : -1.0;
-          const double t = (2.0 * ga * sg) / (fabs(dlt) + sqrt(fma(dlt, dlt, 4.0 * ga * ga)));
-          const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
-          for (int i = lane; i < rows; i += 32) {
-            const double u = xa[i], v = xb[i];
-            xa[i] = c * u - sn * v;
-            xb[i] = sn * u + c * v;
-          }
-          double* va = V + (int64_t)a * kc;
-          double* vb = V + (int64_t)b * kc;
-          for (int i = lane; i < kc; i += 32) {
-            const double u = va[i], v = vb[i];
-            va[i] = c * u - sn * v;
-            vb[i] = sn * u + c * v;
-          }
-          if (lane == 0) {
-            nrm[a] = al - t * ga;
-            nrm[b] = be + t * ga;
-            s_rot = 1;
-          }
-        }
-      }
-      __syncthreads();
-    }
-    const int rot = s_rot;
-    __syncthreads();
-    col_norms_sorted(X, rows, kc, nrm, perm);
-    if (!rot) return true;
-  }
-  return false;
-}
-
 __device__ void blk_copy(double* dst, const double* src, int64_t n) {
   for (int64_t e = threadIdx.x; e < n; e += blockDim.x) dst[e] = src[e];
-}
-
-// out[a', x] = sum_b M[a', b] in[b, x]  (M: ra x rb row-major; in: rb x rest)
-__device__ void blk_mode1(double* out, const double* M, int ra, int rb, const double* in,
-                          int rest) {
-  const int tot = ra * rest;
-  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-    const int a = e / rest, x = e - a * rest;
-    double acc = 0.0;
-    for (int b = 0; b < rb; ++b) acc = fma(M[a * rb + b], in[(int64_t)b * rest + x], acc);
-    out[e] = acc;
-  }
-}
-
-// out[row, c'] = sum_b in[row, b] Mt[b, c']  (Mt: rb x rc row-major, i.e. M^T): lanes
-// vary c' over consecutive words of Mt (conflict-free), in[row, :] is a broadcast.
-__device__ void blk_mode3t(double* out, const double* in, int rows, int rb, const double* Mt, int rc) {
-  const int tot = rows * rc;
-  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-    const int row = e / rc, c = e - row * rc;
-    double acc = 0.0;
-    for (int b = 0; b < rb; ++b) acc = fma(in[(int64_t)row * rb + b], Mt[b * rc + c], acc);
-    out[e] = acc;
-  }
 }
 
 // Row stride of staged matrices: >= n and = 4 (mod 16).  DMMA fragment loads read 4 rows

@@ -109,11 +109,11 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
           xv = a.perm ? a.g[a.perm[s]] : a.g[s];
         }
       }
-      if (MODE == kGSQ) {
+      if constexpr (MODE == kGSQ) {
         if (have && a.g2) a.g2[s] = xv;
         accs = fma(xv, xv, accs);
         continue;
-      }
+      } else {
 #pragma unroll
       for (int st0 = 0; st0 < STEPS; st0 += UNR) {
         double2 b[UNR], b2[MODE == kDPASS ? UNR : 1];
@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
             }
           }
         }
+      }
       }
     }
     const int32_t pslot = a.vrow_part[v];

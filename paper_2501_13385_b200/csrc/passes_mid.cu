@@ -27,7 +27,6 @@ namespace {
 
 constexpr int kMT = 256;          // threads per CTA
 constexpr int kTR = 32;           // rows per tile = 8-lane groups per CTA
-constexpr unsigned kFull = 0xffffffffu;
 
 __host__ __device__ inline int mmald(int w) { return ((w + 15) / 16) * 16 + 4; }
 
