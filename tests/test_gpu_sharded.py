@@ -93,3 +93,52 @@ def test_sharded_two_contexts_match_oracle(cfg, m, steps, rule):
     assert abs(res[0][1] - rref) <= 1e-10 * rref
     for c in ctxs:
         c.close()
+
+
+def _nccl_worker(rank, world, port, out):
+    import os
+    import torch
+    import torch.distributed as dist
+    import paper_2501_13385_b200 as pkg
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world)
+    try:
+        pr = synth.make_problem(2, m=20000)
+        y = pr.observations(oracle.eval_at(pr.truth, pr.idx))
+        res = []
+        for rule in ("theory", "adaptive"):
+            c = pkg.TTContext(pr.n, pr.r)
+            c.set_metric("vee", 0.0, rule)
+            c.set_allreduce(pkg.torch_allreduce(), pr.m)
+            c.set_observations(pr.idx, y)
+            c.set_cores(pr.init)
+            for _ in range(2):
+                c.step(1.0)
+            res.append([x.copy() for x in c.get_cores()])
+            c.close()
+        out["cores"] = res
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_allreduce_callback_world_size_one():
+    # The NCCL plumbing of the sharded mode (torch_allreduce: zero-copy tensor over the
+    # library's buffer, all_reduce on the library's stream) on one GPU with world size 1 (the
+    # sum over one rank is the identity): the iterates must equal the single-process oracle.
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_nccl_worker, args=(1, port, out), nprocs=1, join=True)
+    pr = synth.make_problem(2, m=20000)
+    y = pr.observations(oracle.eval_at(pr.truth, pr.idx))
+    for got, rule in zip(out["cores"], ("theory", "adaptive")):
+        ref = pr.init
+        for _ in range(2):
+            ref = oracle.prgd_step(ref, pr.idx, y, pr.n, pr.r, 1.0, step_rule=rule)
+        assert oracle.tt_diff_norm(got, ref) <= 1e-11, rule
