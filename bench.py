@@ -100,7 +100,7 @@ def algorithmic_bytes(group, m, KL, NL, NR, ld, nvrows_L, nvrows_R):
     if group == "passA_prefix":
         return m * (4 + 8 + 8) + tab(NL) + tab(NR) + NL * 8 + plan(nvrows_L)
     if group == "passA_suffix":
-        return m * (4 + 8) + NR * 8 + plan(nvrows_R)
+        return m * (4 + 8 + 8) + NR * 8 + plan(nvrows_R)      # pos_suf, g gathered, g_suf written
     if group == "passB_prefix":
         return m * (4 + 8) + tab(NR) + tab(NL) + NL * 8 + plan(nvrows_L)
     if group == "passB_suffix":
