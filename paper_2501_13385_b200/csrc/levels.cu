@@ -135,7 +135,7 @@ __device__ void tab_level(const TabLv& L, int cta, int ncta, double* Cs) {
 }
 
 template <int KSM>
-__global__ void __launch_bounds__(kT) k_tab_levels(TabLaunch La, const Scalars* sc) {
+__global__ void __launch_bounds__(kT, KSM <= 4 ? 3 : 2) k_tab_levels(TabLaunch La, const Scalars* sc) {
   if (sc && sc->noop) return;
   extern __shared__ double sm[];
   const int b = blockIdx.x;
@@ -487,7 +487,7 @@ void launch_table_levels(cudaStream_t s, const std::vector<TableLevel>& left,
     }
     La.nlv = n;
     const int64_t tot = tiles[0] + tiles[1];
-    const int64_t budget = (int64_t)sms() * 2;
+    const int64_t budget = (int64_t)sms() * 3;
     La.split[0] = 0;
     for (int q = 0; q < n; ++q) {
       int64_t c = tot <= budget ? tiles[q] : std::max<int64_t>(1, budget * tiles[q] / tot);
