@@ -132,7 +132,7 @@ def test_nccl_allreduce_callback_world_size_one():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()   # no fork from the CUDA-initialised test process
     out = mgr.dict()
     mp.spawn(_nccl_worker, args=(1, port, out), nprocs=1, join=True)
     pr = synth.make_problem(2, m=20000)
