@@ -286,3 +286,61 @@ def test_maximal_rank_and_rule_limits(pkg):
         ctx.spectral_init()                       # r_1 n_2 = 320 ok, r_2 n_3 = 1280 > 1024
     assert ei.value.code == pkg.TT_ERR_ARG
     ctx.close()
+
+
+def test_full_size_config5_properties(pkg):
+    # BASELINE config 5 at full size (3e7 samples, bench.py's launch configuration): A0 bucketing
+    # bit-exact against the oracle's stable order; tt_eval_at on 1e4 sampled indices against the
+    # oracle; then properties that hold at any size over three steps toward a rank-16 truth whose
+    # values are cheap to form exactly (bond-diagonal cores: T(x) = sum_a prod_k c_k[a, x_k],
+    # evaluated here in chunks): finite, left-orthogonal output cores, monotonically decreasing
+    # residual, and the returned iterate's values on sampled indices equal the oracle's
+    # evaluation of the returned cores.
+    pr = synth.make_problem(5)
+    rng = np.random.default_rng(55)
+    KL, NL, NR = pkg.plan(pr.n, pr.r)
+    R = pr.r[1]
+    c = [rng.uniform(0.5, 1.5, size=(R, nk)) for nk in pr.n]
+    y = np.empty(pr.m)
+    for s0 in range(0, pr.m, 1 << 20):
+        blk = pr.idx[s0:s0 + (1 << 20)]
+        acc = np.ones((blk.shape[0], R))
+        for k in range(pr.d):
+            acc *= c[k][:, blk[:, k]].T
+        y[s0:s0 + blk.shape[0]] = acc.sum(axis=1)
+    truth = []
+    for k in range(pr.d):
+        r0, r1 = pr.r[k], pr.r[k + 1]
+        core = np.zeros((r0, pr.n[k], r1))
+        for a in range(R):
+            core[0 if r0 == 1 else a, :, 0 if r1 == 1 else a] = c[k][a]
+        truth.append(core)
+    ctx = pkg.TTContext(pr.n, pr.r)
+    ctx.set_observations(pr.idx, y)
+    o = oracle.stable_order(pr.idx, pr.n, KL)
+    assert np.array_equal(ctx.debug("perm_pre"), o["perm_pre"].astype(np.int32))
+    assert np.array_equal(ctx.debug("perm_suf"), o["perm_suf"].astype(np.int32))
+    assert np.array_equal(ctx.debug("offs_l"), o["offs_L"].astype(np.int64))
+    assert np.array_equal(ctx.debug("offs_r"), o["offs_R"].astype(np.int64))
+    del o
+    q = np.stack([rng.integers(0, nk, size=10_000) for nk in pr.n], axis=1).astype(np.int32)
+    ctx.set_cores(truth)
+    assert ctx.residual_norm() <= 1e-12 * np.linalg.norm(y)     # the values above are T*(Omega)
+    init = [t + 0.05 * rng.standard_normal(t.shape) * np.abs(t).max() for t in truth]
+    ctx.set_cores(init)
+    np.testing.assert_allclose(ctx.eval_at(q), oracle.eval_at(init, q), rtol=0,
+                               atol=1e-12 * np.abs(oracle.eval_at(init, q)).max())
+    res = [ctx.residual_norm()]
+    for _ in range(3):
+        ctx.step(1.0)
+        res.append(ctx.residual_norm())
+        cores = ctx.get_cores()
+        assert all(np.all(np.isfinite(cc)) for cc in cores)
+        for k in range(pr.d - 1):
+            Lk = cores[k].reshape(-1, cores[k].shape[2])
+            np.testing.assert_allclose(Lk.T @ Lk, np.eye(Lk.shape[1]), atol=1e-12)
+        ref = oracle.eval_at(cores, q)
+        np.testing.assert_allclose(ctx.eval_at(q), ref, rtol=0, atol=1e-12 * np.abs(ref).max())
+    assert all(b < a for a, b in zip(res, res[1:])), res
+    assert res[-1] < 0.1 * res[0], res
+    ctx.close()
