@@ -30,6 +30,7 @@ if ROOT not in sys.path:
 import numpy as np  # noqa: E402
 
 METRIC = "PRGD iter/s (observed entries/s = M x iter/s) at d=10, n=16, r=16, |Omega|~3e7, fp64"
+FP64_DMMA_TFS = 37.1   # measured DMMA fp64 peak (tools/fp64_peak.cu), DESIGN.md 8
 UNIT = "iter/s"
 
 
@@ -345,6 +346,19 @@ def main():
             "share_of_step": round(per[dom_pass] / tot, 4) if tot else None,
             "group_ms": {k: round(v, 4) for k, v in per.items()},
             "dominant_group": dom}
+    # FP64 side (SURVEY 8(d) "FP64 util vs peak"): the backward recursions are the path's dense
+    # contraction (A9 as DMMA GEMMs over the table levels); algorithmic flops per level k =
+    # 4 r_k n_k r_{k+1} per parent row (the O and Z products), parents = prod of the other modes
+    # on that side.  Peak: DMMA measured with tools/fp64_peak.cu on this pool.
+    fl = 0.0
+    for k in range(pr.d):
+        parents = math.prod(pr.n[:k]) if k < r["KL"] else math.prod(pr.n[k + 1:])
+        fl += 4.0 * pr.r[k] * pr.n[k] * pr.r[k + 1] * parents
+    t_back = per.get("backward_Y", 0.0) / 1e3
+    fp64 = {"kernel": "backward_Y", "bound": "tensor (DMMA fp64)", "flops": fl,
+            "achieved": round(fl / t_back / 1e12, 2) if t_back > 0 else None, "peak": FP64_DMMA_TFS,
+            "unit": "TFLOP/s", "frac": round(fl / t_back / 1e12 / FP64_DMMA_TFS, 4) if t_back > 0 else None,
+            "peak_src": "tools/fp64_peak.cu (mma.sync m8n8k4 f64, measured on the pool's B200)"}
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
         ms_ = min(args.cpu_sample, m)
@@ -369,6 +383,7 @@ def main():
                                   else "single"},
         "entries_per_s": round(r["m_global"] * args.steps / (r["ms"] / 1e3), 1),
         "roofline": roof,
+        "fp64": fp64,
         "cpu_baseline": cpu,
         "e2e": r.get("e2e"),
         "gpu_launches": int(r["launches"]),
