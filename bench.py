@@ -214,7 +214,11 @@ def run_ours(args, rank, ws, dist):
                clocks=clocks, prof=prof, t_gen=t_gen, t_setobs=t_setobs, res0=res0, res1=res1,
                dense_diag=dense_diag)
     if not args.no_e2e:
-        out["e2e"] = run_e2e(args, pr, y, init, ar, m_global, dist)
+        # three end-to-end repetitions (fresh context each), the median reported: a single
+        # 20-step run is dominated by the one-time upload / bucketing and varies run to run
+        reps = [run_e2e(args, pr, y, init, ar, m_global, dist) for _ in range(3)]
+        reps.sort(key=lambda e: e["value"])
+        out["e2e"] = dict(reps[1], reps=[round(e["value"], 3) for e in reps])
     return out
 
 
