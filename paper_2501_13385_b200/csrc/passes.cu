@@ -113,10 +113,64 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
         if (have && a.g2) a.g2[s] = xv;
         accs = fma(xv, xv, accs);
         continue;
+      } else if constexpr (MODE == kSDDMM || MODE == kDPASS) {
+        // partial dot products of the chunk's STEPS samples of this lane group, then a
+        // transpose-reduction over the group's LPS lanes (LPS - 1 shuffles for LPS samples
+        // instead of log2(LPS) per sample): afterwards lane `sub` holds the dot product of
+        // sample t = sub * G + grp, which it finishes and stores (coalesced over the warp)
+        double pd[STEPS];
+#pragma unroll
+        for (int st0 = 0; st0 < STEPS; st0 += UNR) {
+          double2 b[UNR], b2[MODE == kDPASS ? UNR : 1];
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) {
+            const int t = (st0 + u) * G + grp;
+            const int cidx = __shfl_sync(kFull, colv, t & 31);
+            const double* cp = a.coltab + (int64_t)cidx * ld + 2 * sub;
+            b[u] = make_double2(0.0, 0.0);
+            if (t < nc) b[u] = ld2(cp);
+            if constexpr (MODE == kDPASS) {
+              b2[u] = make_double2(0.0, 0.0);
+              if (t < nc) b2[u] = ld2(a.coltab2 + (int64_t)cidx * ld + 2 * sub);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) {
+            double part = fma(rv.x, b[u].x, rv.y * b[u].y);
+            if constexpr (MODE == kDPASS) {
+              part = fma(rv2.x, b2[u].x, part);
+              part = fma(rv2.y, b2[u].y, part);
+            }
+            pd[st0 + u] = part;
+          }
+        }
+#pragma unroll
+        for (int o = LPS / 2; o > 0; o >>= 1) {
+          const bool up = (sub & o) != 0;
+#pragma unroll
+          for (int j = 0; j < o; ++j) {
+            const double send = up ? pd[j] : pd[j + o];
+            const double keep = up ? pd[j + o] : pd[j];
+            pd[j] = keep + __shfl_xor_sync(kFull, send, o);
+          }
+        }
+        const int t = sub * G + grp;
+        if constexpr (MODE == kSDDMM) {
+          const double yv = __shfl_sync(kFull, xv, t & 31);
+          const int p2 = a.g2 ? __shfl_sync(kFull, p2v, t & 31) : 0;
+          if (t < nc) {
+            const double gv = pd[0] - yv;
+            a.g[beg + c0 + t] = gv;
+            if (a.g2) a.g2[p2] = gv;
+            accs = fma(gv, gv, accs);
+          }
+        } else {
+          if (t < nc) accs = fma(pd[0], pd[0], accs);
+        }
       } else {
 #pragma unroll
       for (int st0 = 0; st0 < STEPS; st0 += UNR) {
-        double2 b[UNR], b2[MODE == kDPASS ? UNR : 1];
+        double2 b[UNR];
         double xs[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
@@ -125,40 +179,13 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
           xs[u] = __shfl_sync(kFull, xv, t & 31);
           b[u] = make_double2(0.0, 0.0);
           if (t < nc) b[u] = ld2(a.coltab + (int64_t)cidx * ld + 2 * sub);
-          if constexpr (MODE == kDPASS) {
-            b2[u] = make_double2(0.0, 0.0);
-            if (t < nc) b2[u] = ld2(a.coltab2 + (int64_t)cidx * ld + 2 * sub);
-          }
         }
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
           const int t = (st0 + u) * G + grp;
-          if (MODE == kSDDMM) {
-            double part = fma(rv.x, b[u].x, rv.y * b[u].y);
-#pragma unroll
-            for (int o = LPS / 2; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
-            const int p2 = a.g2 ? __shfl_sync(kFull, p2v, t & 31) : 0;
-            if (t < nc) {
-              const double gv = part - xs[u];
-              if (sub == 0) {
-                a.g[beg + c0 + t] = gv;
-                if (a.g2) a.g2[p2] = gv;
-                accs = fma(gv, gv, accs);
-              }
-            }
-          } else if constexpr (MODE == kDPASS) {
-            // D(x_s) = rowtab.coltab + rowtab2.coltab2 (tangent vector at the sample)
-            double part = fma(rv.x, b[u].x, rv.y * b[u].y);
-            part = fma(rv2.x, b2[u].x, part);
-            part = fma(rv2.y, b2[u].y, part);
-#pragma unroll
-            for (int o = LPS / 2; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
-            if (t < nc && sub == 0) accs = fma(part, part, accs);
-          } else {
-            if (t < nc) {
-              accv.x = fma(xs[u], b[u].x, accv.x);
-              accv.y = fma(xs[u], b[u].y, accv.y);
-            }
+          if (t < nc) {
+            accv.x = fma(xs[u], b[u].x, accv.x);
+            accv.y = fma(xs[u], b[u].y, accv.y);
           }
         }
       }
@@ -174,7 +201,7 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
       }
     } else if (MODE == kSDDMM || MODE == kDPASS) {
 #pragma unroll
-      for (int o = LPS; o < 32; o <<= 1) accs += __shfl_xor_sync(kFull, accs, o);
+      for (int o = 1; o < 32; o <<= 1) accs += __shfl_xor_sync(kFull, accs, o);   // every lane holds samples
       if (lane == 0) {
         if (pslot < 0) a.out[row] = accs;
         else a.part[pslot] = accs;
