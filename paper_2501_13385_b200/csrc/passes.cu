@@ -81,11 +81,11 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
   const int64_t wl = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (wl >= a.nwarps) return;
   const int64_t warp = wl + a.warp_off;
-  const int ld = a.ld;
+  constexpr int ld = 2 * LPS;          // table row stride (the launcher picks LPS = a.ld / 2)
   const int64_t v0 = a.warp_vbegin[warp], v1 = a.warp_vbegin[warp + 1];
   for (int64_t v = v0; v < v1; ++v) {
     const int32_t row = a.vrow_row[v];
-    const int64_t trow = row % a.nrow_real;
+    const int64_t trow = row < a.nrow_real ? row : row % a.nrow_real;   // gather blocks only
     const int64_t beg = a.vrow_begin[v];
     const int cnt = a.vrow_cnt[v];
     double2 rv = make_double2(0.0, 0.0), rv2 = make_double2(0.0, 0.0);
