@@ -53,10 +53,11 @@ __device__ __forceinline__ double2 ld2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
 
-// Minimum resident CTAs per SM (register cap): measured on B200 at config 5, the SDDMM pass
-// is fastest at 4 (64 registers, no spills), the SpMM passes at 6 (40 registers).
+// Minimum resident CTAs per SM (register cap), measured on B200 at config 5: the SDDMM pass
+// is fastest at 4 (64 registers; 5 spills and is 10 % slower), the SpMM passes at 5
+// (48 registers; 6 and 4 are 3 % / 0.5 % slower).
 #ifndef PRGD_SEG_OCC_SPMM
-#define PRGD_SEG_OCC_SPMM 6
+#define PRGD_SEG_OCC_SPMM 5
 #endif
 #ifndef PRGD_SEG_OCC_SDDMM
 #define PRGD_SEG_OCC_SDDMM 4
