@@ -909,16 +909,15 @@ int make_plan(tt_ctx* ctx, const int64_t* offs_dev, int64_t nrow, int nblk, int 
   pl->npart = tot[2];
   const int64_t nvr = pl->nvrows;
   auto& OL = ctx->obs_allocs;
-  if (!(A(ctx, &pl->vrow_row, nvr, OL) && A(ctx, &pl->vrow_begin, nvr, OL) && A(ctx, &pl->vrow_cnt, nvr, OL) &&
-        A(ctx, &pl->vrow_part, nvr, OL) && A(ctx, &pl->warp_vbegin, nvr + 1, OL) &&
+  if (!(A(ctx, &pl->vrow, nvr, OL) && A(ctx, &pl->warp_vbegin, nvr + 1, OL) &&
         A(ctx, &pl->split_row, pl->nsplit, OL) && A(ctx, &pl->split_first, pl->nsplit + 1, OL) &&
         A(ctx, &pl->part, std::max<int64_t>(pl->npart, 1) * ld, OL) && A(ctx, &cost, nvr, tmp) &&
         A(ctx, &C, nvr + 1, tmp) && A(ctx, &flag, nvr, tmp) && A(ctx, &wid, nvr + 1, tmp))) {
     cleanup();
     return fail(ctx, TT_ERR_OOM, "device allocation failed (plan)");
   }
-  launch_plan_fill(s, offs_dev, nr, nrow, nblk, kSplit, vbase, sbase, pbase, nvr, pl->vrow_row,
-                   pl->vrow_begin, pl->vrow_cnt, pl->vrow_part, pl->split_row, pl->split_first,
+  launch_plan_fill(s, offs_dev, nr, nrow, nblk, kSplit, vbase, sbase, pbase, nvr, pl->vrow,
+                   pl->split_row, pl->split_first,
                    kVrowCost, kWarpCost, cost, C, flag, wid, bsum, blk, &lc);
   launch_plan_warps(s, flag, wid, nvr, pl->warp_vbegin, &lc);
   std::vector<int64_t> hb(3 * (nblk + 1));

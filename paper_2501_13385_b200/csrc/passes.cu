@@ -28,10 +28,7 @@ struct SegDev {
   int64_t warp_off;       // first plan warp of this launch
   int64_t nrow_real;      // table rows: virtual row v -> table row v % nrow_real
   int accum;              // SpMM: add into out (gather blocks after the first)
-  const int32_t* vrow_row;
-  const int64_t* vrow_begin;
-  const int32_t* vrow_cnt;
-  const int32_t* vrow_part;
+  const int4* vrow;       // {row, count, first sample, partial slot} per virtual row
   const int64_t* warp_vbegin;
   double* part;
   int ld;
@@ -85,10 +82,11 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
   constexpr int ld = 2 * LPS;          // table row stride (the launcher picks LPS = a.ld / 2)
   const int64_t v0 = a.warp_vbegin[warp], v1 = a.warp_vbegin[warp + 1];
   for (int64_t v = v0; v < v1; ++v) {
-    const int32_t row = a.vrow_row[v];
+    const int4 vr = a.vrow[v];
+    const int32_t row = vr.x;
     const int64_t trow = row < a.nrow_real ? row : row % a.nrow_real;   // gather blocks only
-    const int64_t beg = a.vrow_begin[v];
-    const int cnt = a.vrow_cnt[v];
+    const int64_t beg = vr.z;
+    const int cnt = vr.y;
     double2 rv = make_double2(0.0, 0.0), rv2 = make_double2(0.0, 0.0);
     if (MODE == kSDDMM || MODE == kDPASS) rv = ld2(a.rowtab + trow * ld + 2 * sub);
     if (MODE == kDPASS) rv2 = ld2(a.rowtab2 + trow * ld + 2 * sub);
@@ -192,7 +190,7 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
       }
       }
     }
-    const int32_t pslot = a.vrow_part[v];
+    const int32_t pslot = vr.w;
     if (MODE == kGSQ) {
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) accs += __shfl_xor_sync(kFull, accs, o);
@@ -493,10 +491,7 @@ void launch_seg(cudaStream_t s, const SegArgs& a, const Scalars* sc, int64_t* la
   dv.warp_off = 0;
   dv.nrow_real = p.nrow_real > 0 ? p.nrow_real : p.nrows;
   dv.accum = 0;
-  dv.vrow_row = p.vrow_row;
-  dv.vrow_begin = p.vrow_begin;
-  dv.vrow_cnt = p.vrow_cnt;
-  dv.vrow_part = p.vrow_part;
+  dv.vrow = p.vrow;
   dv.warp_vbegin = p.warp_vbegin;
   dv.part = p.part;
   dv.ld = a.ld;

@@ -98,9 +98,8 @@ __global__ void k_pscan_apply(const int* __restrict__ in, int64_t len, const lon
 // fill the virtual rows of every row and the split-row table; cost per virtual row
 __global__ void k_plan_fill(const int64_t* __restrict__ offs, int64_t nr, int64_t split,
                             const int64_t* __restrict__ vbase, const int64_t* __restrict__ sbase,
-                            const int64_t* __restrict__ pbase, int32_t* __restrict__ vrow_row,
-                            int64_t* __restrict__ vrow_begin, int32_t* __restrict__ vrow_cnt,
-                            int32_t* __restrict__ vrow_part, int32_t* __restrict__ split_row,
+                            const int64_t* __restrict__ pbase, int4* __restrict__ vrow,
+                            int32_t* __restrict__ split_row,
                             int64_t* __restrict__ split_first, int* __restrict__ cost, int vcost) {
   const int64_t P = blockIdx.x * (int64_t)kPT + threadIdx.x;
   if (P == 0) split_first[sbase[nr]] = pbase[nr];
@@ -108,10 +107,7 @@ __global__ void k_plan_fill(const int64_t* __restrict__ offs, int64_t nr, int64_
   const int64_t beg = offs[P], cnt = offs[P + 1] - beg;
   const int64_t v0 = vbase[P];
   if (cnt <= split) {
-    vrow_row[v0] = (int32_t)P;
-    vrow_begin[v0] = beg;
-    vrow_cnt[v0] = (int32_t)cnt;
-    vrow_part[v0] = -1;
+    vrow[v0] = make_int4((int)P, (int)cnt, (int)beg, -1);
     cost[v0] = (int)cnt + vcost;
     return;
   }
@@ -122,22 +118,19 @@ __global__ void k_plan_fill(const int64_t* __restrict__ offs, int64_t nr, int64_
   for (int64_t t = 0; t < nv; ++t) {
     const int64_t o = t * split;
     const int c = (int)(cnt - o < split ? cnt - o : split);
-    vrow_row[v0 + t] = (int32_t)P;
-    vrow_begin[v0 + t] = beg + o;
-    vrow_cnt[v0 + t] = c;
-    vrow_part[v0 + t] = (int32_t)(p0 + t);
+    vrow[v0 + t] = make_int4((int)P, c, (int)(beg + o), (int)(p0 + t));
     cost[v0 + t] = c + vcost;
   }
 }
 
 // warp-start flags: first virtual row of a gather block, or the block-relative running cost
 // crosses a multiple of wcost
-__global__ void k_plan_flags(const int64_t* __restrict__ C, const int32_t* __restrict__ vrow_row,
+__global__ void k_plan_flags(const int64_t* __restrict__ C, const int4* __restrict__ vrow,
                              int64_t nvrows, int64_t nrow, const int64_t* __restrict__ vbase,
                              int64_t wcost, int* __restrict__ flag) {
   const int64_t v = blockIdx.x * (int64_t)kPT + threadIdx.x;
   if (v >= nvrows) return;
-  const int64_t b = vrow_row[v] / nrow;
+  const int64_t b = vrow[v].x / nrow;
   const int64_t v0 = vbase[b * nrow];
   int f = v == v0;
   if (!f) {
@@ -200,17 +193,15 @@ void launch_plan_rows(cudaStream_t s, const int64_t* offs, int64_t nr, int64_t s
 
 void launch_plan_fill(cudaStream_t s, const int64_t* offs, int64_t nr, int64_t nrow, int nblk,
                       int64_t split, const int64_t* vbase, const int64_t* sbase, const int64_t* pbase,
-                      int64_t nvrows, int32_t* vrow_row, int64_t* vrow_begin, int32_t* vrow_cnt,
-                      int32_t* vrow_part, int32_t* split_row, int64_t* split_first, int vcost,
+                      int64_t nvrows, int4* vrow, int32_t* split_row, int64_t* split_first, int vcost,
                       int64_t wcost, int* cost, int64_t* C, int* flag, int64_t* wid,
                       long long* bsum, int64_t* blk_out, int64_t* launches) {
-  k_plan_fill<<<blocks_for(nr > 0 ? nr : 1), kPT, 0, s>>>(offs, nr, split, vbase, sbase, pbase, vrow_row,
-                                                          vrow_begin, vrow_cnt, vrow_part, split_row,
-                                                          split_first, cost, vcost);
+  k_plan_fill<<<blocks_for(nr > 0 ? nr : 1), kPT, 0, s>>>(offs, nr, split, vbase, sbase, pbase, vrow,
+                                                          split_row, split_first, cost, vcost);
   ++*launches;
   scan_i32(s, cost, nvrows, C, bsum, launches);
   if (nvrows > 0) {
-    k_plan_flags<<<blocks_for(nvrows), kPT, 0, s>>>(C, vrow_row, nvrows, nrow, vbase, wcost, flag);
+    k_plan_flags<<<blocks_for(nvrows), kPT, 0, s>>>(C, vrow, nvrows, nrow, vbase, wcost, flag);
     ++*launches;
   }
   scan_i32(s, flag, nvrows, wid, bsum, launches);

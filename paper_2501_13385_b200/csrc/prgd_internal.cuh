@@ -53,10 +53,8 @@ struct SegPlan {
   int64_t nwarps = 0;
   int64_t nsplit = 0;       // rows split over several vrows
   int64_t npart = 0;        // partial slots
-  int32_t* vrow_row = nullptr;
-  int64_t* vrow_begin = nullptr;
-  int32_t* vrow_cnt = nullptr;
-  int32_t* vrow_part = nullptr;    // -1: whole row, else partial slot
+  int4* vrow = nullptr;            // per virtual row {table row (virtual), sample count, first
+                                   // sample (m < 2^31), partial slot or -1}: one 16-byte load
   int64_t* warp_vbegin = nullptr;  // [nwarps+1]
   int32_t* split_row = nullptr;    // [nsplit]
   int64_t* split_first = nullptr;  // [nsplit+1] partial slot ranges
@@ -118,8 +116,7 @@ void launch_plan_rows(cudaStream_t s, const int64_t* offs, int64_t nr, int64_t s
                       int64_t* launches);
 void launch_plan_fill(cudaStream_t s, const int64_t* offs, int64_t nr, int64_t nrow, int nblk,
                       int64_t split, const int64_t* vbase, const int64_t* sbase, const int64_t* pbase,
-                      int64_t nvrows, int32_t* vrow_row, int64_t* vrow_begin, int32_t* vrow_cnt,
-                      int32_t* vrow_part, int32_t* split_row, int64_t* split_first, int vcost,
+                      int64_t nvrows, int4* vrow, int32_t* split_row, int64_t* split_first, int vcost,
                       int64_t wcost, int* cost, int64_t* C, int* flag, int64_t* wid,
                       long long* bsum, int64_t* blk_out, int64_t* launches);
 void launch_plan_warps(cudaStream_t s, const int* flag, const int64_t* wid, int64_t nvrows,
