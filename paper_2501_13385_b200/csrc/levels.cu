@@ -76,7 +76,7 @@ struct TabLaunch {
 // blocks J = w, w+8, ...; A fragments are loaded straight from global per tile, each 8x8
 // output tile leaves as double2 streaming stores.
 template <int KSM>
-__device__ void tab_level(const TabLv& L, int cta, int ncta, double* Cs) {
+__device__ void tab_level(const TabLv L, int cta, int ncta, double* Cs) {   // by value: fields in registers
   const int K = L.in ? (L.left ? L.r0 : L.r1) : 1;
   const int KS = (K + 3) >> 2;
   const int W = L.nk * L.ld_out;
@@ -99,6 +99,8 @@ __device__ void tab_level(const TabLv& L, int cta, int ncta, double* Cs) {
   const int64_t ntiles = (L.nparent + kFwdRows - 1) / kFwdRows;
   for (int64_t tile = cta; tile < ntiles; tile += ncta) {
     const int64_t p0 = tile * kFwdRows;
+    // fragments beyond K are zero (the staged Cs rows k >= K are zero too), so the DMMA loop
+    // runs unpredicated over KSM k-steps
     double af[4][KSM];
 #pragma unroll
     for (int I = 0; I < 4; ++I) {
@@ -107,7 +109,7 @@ __device__ void tab_level(const TabLv& L, int cta, int ncta, double* Cs) {
       for (int ks = 0; ks < KSM; ++ks) {
         const int k = 4 * ks + tq;
         double v = 0.0;
-        if (ks < KS && k < K && p < L.nparent) v = L.in ? __ldg(L.in + p * L.ld_in + k) : 1.0;
+        if (k < K && p < L.nparent) v = L.in ? __ldg(L.in + p * L.ld_in + k) : 1.0;
         af[I][ks] = v;
       }
     }
@@ -121,8 +123,7 @@ __device__ void tab_level(const TabLv& L, int cta, int ncta, double* Cs) {
       for (int I = 0; I < 4; ++I) {
         double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-        for (int ks = 0; ks < KSM; ++ks)
-          if (ks < KS) dmma_l(d0, d1, af[I][ks], bf[ks]);
+        for (int ks = 0; ks < KSM; ++ks) dmma_l(d0, d1, af[I][ks], bf[ks]);
         const int64_t p = p0 + I * 8 + gid;
         if (p < L.nparent) {
           const double f = L.rowscale ? __ldg(L.rowscale + p * L.nk + j) : 1.0;
