@@ -97,8 +97,17 @@ __device__ void tab_level(const TabLv L, int cta, int ncta, double* Cs) {   // b
   const int gid = lane >> 2, tq = lane & 3;
   const int nJ = W >> 3;
   const int64_t ntiles = (L.nparent + kFwdRows - 1) / kFwdRows;
+  double* Fs = Cs + (int64_t)4 * KS * ldc;            // child-row scales of the tile
   for (int64_t tile = cta; tile < ntiles; tile += ncta) {
     const int64_t p0 = tile * kFwdRows;
+    if (L.rowscale) {                                   // stage the tile's psi once (coalesced)
+      __syncthreads();
+      for (int t = threadIdx.x; t < kFwdRows * L.nk; t += blockDim.x) {
+        const int64_t e = p0 * L.nk + t;
+        Fs[t] = e < L.nparent * L.nk ? __ldg(L.rowscale + e) : 0.0;
+      }
+      __syncthreads();
+    }
     // fragments beyond K are zero (the staged Cs rows k >= K are zero too), so the DMMA loop
     // runs unpredicated over KSM k-steps
     double af[4][KSM];
@@ -126,7 +135,7 @@ __device__ void tab_level(const TabLv L, int cta, int ncta, double* Cs) {   // b
         for (int ks = 0; ks < KSM; ++ks) dmma_l(d0, d1, af[I][ks], bf[ks]);
         const int64_t p = p0 + I * 8 + gid;
         if (p < L.nparent) {
-          const double f = L.rowscale ? __ldg(L.rowscale + p * L.nk + j) : 1.0;
+          const double f = L.rowscale ? Fs[(I * 8 + gid) * L.nk + j] : 1.0;
           __stcs(reinterpret_cast<double2*>(L.out + p * W + q), make_double2(d0 * f, d1 * f));
         }
       }
@@ -170,7 +179,7 @@ struct BackLaunch {
 // 4-row k-step it loads NVB A- and <= 8 B-fragments and issues NVB x 8 independent DMMAs.
 // The next tile's X / V rows land by cp.async while the current tile computes.
 template <int NVB>
-__device__ void back_level(const BackLv& L, int cta, int ncta, double* sm, bool direct) {
+__device__ void back_level(const BackLv L, int cta, int ncta, double* sm, bool direct) {   // by value: fields in registers
   const int W = L.nk * L.wrow;
   const int ldx = mma_ld(W);
   const int olen8 = L.O ? max((L.olen + 7) & ~7, (L.ldO + 7) & ~7) : 0;
@@ -373,7 +382,8 @@ constexpr int kMaxBackCtas = 160;
 
 size_t tab_smem(const TabLv& L) {
   const int K = L.in ? (L.left ? L.r0 : L.r1) : 1;
-  return (size_t)(4 * ((K + 3) >> 2)) * mma_ld(L.nk * L.ld_out) * sizeof(double);
+  return ((size_t)(4 * ((K + 3) >> 2)) * mma_ld(L.nk * L.ld_out) + (L.rowscale ? kFwdRows * L.nk : 0)) *
+         sizeof(double);
 }
 
 size_t back_smem(const BackLv& L) {
