@@ -29,6 +29,7 @@ namespace {
 
 constexpr int kNW = kDenseThreads / 32;
 constexpr int kMaxCols = 2 * kMaxRank;   // 64
+constexpr int kProjThreads = 1024;       // k_project: one CTA per core, latency-bound phases
 
 __device__ __forceinline__ double shx(double v, int o) { return __shfl_xor_sync(0xffffffffu, v, o); }
 
@@ -935,7 +936,7 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_orth(DenseArgs a) {
 }
 
 // One CTA per core k: projection (A10), unweighting (A11), assembly of B_k (A13).
-__global__ void __launch_bounds__(kDenseThreads) k_project(DenseArgs a) {
+__global__ void __launch_bounds__(kProjThreads) k_project(DenseArgs a) {
   extern __shared__ double smraw[];
   Scalars* sc = a.sc;
   if (sc->noop) return;
@@ -1234,7 +1235,7 @@ void launch_dense_orth(cudaStream_t s, const DenseArgs& a, int64_t* launches) {
 
 void launch_dense_round(cudaStream_t s, const DenseArgs& a, int64_t* launches) {
   const size_t bytes = (size_t)a.smem_doubles * sizeof(double);
-  k_project<<<a.d, kDenseThreads, bytes, s>>>(a);
+  k_project<<<a.d, kProjThreads, bytes, s>>>(a);
   if (!(a.clw && launch_round_cs(s, a, bytes))) k_dense_round<<<1, kDenseThreads, bytes, s>>>(a);
   *launches += 2;
 }
@@ -1242,7 +1243,7 @@ void launch_dense_round(cudaStream_t s, const DenseArgs& a, int64_t* launches) {
 void launch_project(cudaStream_t s, const DenseArgs& a, int mode, int64_t* launches) {
   DenseArgs b = a;
   b.proj_mode = mode;
-  k_project<<<b.d, kDenseThreads, (size_t)b.smem_doubles * sizeof(double), s>>>(b);
+  k_project<<<b.d, kProjThreads, (size_t)b.smem_doubles * sizeof(double), s>>>(b);
   ++*launches;
 }
 
