@@ -84,7 +84,8 @@ enum { TT_STEP_THEORY = 0, TT_STEP_RAW = 1, TT_STEP_ADAPTIVE = 2 };
  * r[k] <= min(prod_{i<k} n_i, prod_{i>=k} n_i), r[k] <= r[k-1] n[k-1],
  * r[k-1] <= n[k-1] r[k] (TT_ERR_RANK otherwise).  Build limits
  * (TT_ERR_UNSUPPORTED): r[k] <= 32, and some prefix split K with
- * prod(n[0..K-1]) and prod(n[K..d-1]) both <= 2^30 (see tt_plan).
+ * prod(n[0..K-1]) and prod(n[K..d-1]) both <= 2^30 (see tt_plan), with the split-level
+ * tables below 2^31 doubles (max(N_L, N_R) * pad(r_K) < 2^31; 32-bit table offsets).
  * Cores start at zero; observations unset.  *out receives the context. */
 PRGD_API int tt_create(int d, const int64_t* n, const int64_t* r, tt_ctx** out);
 

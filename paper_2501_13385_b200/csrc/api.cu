@@ -136,6 +136,14 @@ int validate_and_plan(int d, const int64_t* n, const int64_t* r, Plan* pl, std::
     *msg = "no prefix/suffix split with both table sizes <= 2^30 rows";
     return TT_ERR_UNSUPPORTED;
   }
+  {   // the pass kernels index the gathered split-level table with 32-bit offsets
+    int pr = 2;
+    while (pr < r[best]) pr <<= 1;
+    if (bestv * pr >= ((int64_t)1 << 31)) {
+      *msg = "split-level tables above 2^31 doubles (16 GB) are not supported";
+      return TT_ERR_UNSUPPORTED;
+    }
+  }
   pl->KL = best;
   pl->NL = bNL;
   pl->NR = bNR;

@@ -123,15 +123,13 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
           double2 b[UNR], b2[MODE == kDPASS ? UNR : 1];
 #pragma unroll
           for (int u = 0; u < UNR; ++u) {
+            // lanes past the chunk hold colv = 0: their loads read table row 0 (valid) and
+            // their dot products are never finished (t >= nc below), so no predicate is needed
             const int t = (st0 + u) * G + grp;
             const int cidx = __shfl_sync(kFull, colv, t & 31);
-            const double* cp = a.coltab + (int64_t)cidx * ld + 2 * sub;
-            b[u] = make_double2(0.0, 0.0);
-            if (t < nc) b[u] = ld2(cp);
-            if constexpr (MODE == kDPASS) {
-              b2[u] = make_double2(0.0, 0.0);
-              if (t < nc) b2[u] = ld2(a.coltab2 + (int64_t)cidx * ld + 2 * sub);
-            }
+            const int off = cidx * ld + 2 * sub;   // < 2^31: table size checked by the planner
+            b[u] = ld2(a.coltab + off);
+            if constexpr (MODE == kDPASS) b2[u] = ld2(a.coltab2 + off);
           }
 #pragma unroll
           for (int u = 0; u < UNR; ++u) {
