@@ -171,19 +171,17 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
         double xs[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
+          // lanes past the chunk hold colv = 0 and xv = 0: they read table row 0 and add
+          // 0 x row (finite tables), so no predicate is needed
           const int t = (st0 + u) * G + grp;
           const int cidx = __shfl_sync(kFull, colv, t & 31);
           xs[u] = __shfl_sync(kFull, xv, t & 31);
-          b[u] = make_double2(0.0, 0.0);
-          if (t < nc) b[u] = ld2(a.coltab + (int64_t)cidx * ld + 2 * sub);
+          b[u] = ld2(a.coltab + (cidx * ld + 2 * sub));   // < 2^31 (planner)
         }
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
-          const int t = (st0 + u) * G + grp;
-          if (t < nc) {
-            accv.x = fma(xs[u], b[u].x, accv.x);
-            accv.y = fma(xs[u], b[u].y, accv.y);
-          }
+          accv.x = fma(xs[u], b[u].x, accv.x);
+          accv.y = fma(xs[u], b[u].y, accv.y);
         }
       }
       }
