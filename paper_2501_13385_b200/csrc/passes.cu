@@ -68,8 +68,10 @@ struct SegOcc {
                                                              : (MODE == kSPMM ? PRGD_SEG_OCC_SPMM : 8);
 };
 
-template <int LPS, int MODE>
+// LPS lanes per sample, each holding V double2 of the row (ld = 2 LPS V)
+template <int LPS, int MODE, int V = 1>
 __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Scalars* sc) {
+  static_assert(V == 1 || MODE == kSDDMM || MODE == kDPASS, "vector lanes: SDDMM / DPASS only");
   if (sc && sc->noop) return;
   constexpr int G = 32 / LPS;        // samples per warp step
   constexpr int STEPS = 32 / G;      // steps per 32-sample chunk (= LPS)
@@ -79,7 +81,7 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
   const int64_t wl = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (wl >= a.nwarps) return;
   const int64_t warp = wl + a.warp_off;
-  constexpr int ld = 2 * LPS;          // table row stride (the launcher picks LPS = a.ld / 2)
+  constexpr int ld = 2 * LPS * V;      // table row stride (the launcher picks LPS V = a.ld / 2)
   const int64_t v0 = a.warp_vbegin[warp], v1 = a.warp_vbegin[warp + 1];
   for (int64_t v = v0; v < v1; ++v) {
     const int4 vr = a.vrow[v];
@@ -87,9 +89,13 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
     const int64_t trow = row < a.nrow_real ? row : row % a.nrow_real;   // gather blocks only
     const int64_t beg = vr.z;
     const int cnt = vr.y;
-    double2 rv = make_double2(0.0, 0.0), rv2 = make_double2(0.0, 0.0);
-    if (MODE == kSDDMM || MODE == kDPASS) rv = ld2(a.rowtab + trow * ld + 2 * sub);
-    if (MODE == kDPASS) rv2 = ld2(a.rowtab2 + trow * ld + 2 * sub);
+    double2 rv[V], rv2[V];
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      rv[q] = rv2[q] = make_double2(0.0, 0.0);
+      if (MODE == kSDDMM || MODE == kDPASS) rv[q] = ld2(a.rowtab + trow * ld + 2 * (V * sub + q));
+      if (MODE == kDPASS) rv2[q] = ld2(a.rowtab2 + trow * ld + 2 * (V * sub + q));
+    }
     double accs = 0.0;
     double2 accv = make_double2(0.0, 0.0);
     for (int c0 = 0; c0 < cnt; c0 += 32) {
@@ -120,23 +126,28 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
         double pd[STEPS];
 #pragma unroll
         for (int st0 = 0; st0 < STEPS; st0 += UNR) {
-          double2 b[UNR], b2[MODE == kDPASS ? UNR : 1];
+          double2 b[UNR][V], b2[MODE == kDPASS ? UNR : 1][V];
 #pragma unroll
           for (int u = 0; u < UNR; ++u) {
             // lanes past the chunk hold colv = 0: their loads read table row 0 (valid) and
             // their dot products are never finished (t >= nc below), so no predicate is needed
             const int t = (st0 + u) * G + grp;
             const int cidx = __shfl_sync(kFull, colv, t & 31);
-            const int off = cidx * ld + 2 * sub;   // < 2^31: table size checked by the planner
-            b[u] = ld2(a.coltab + off);
-            if constexpr (MODE == kDPASS) b2[u] = ld2(a.coltab2 + off);
+            const int off = cidx * ld + 2 * V * sub;   // < 2^31: table size checked by the planner
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+              b[u][q] = ld2(a.coltab + off + 2 * q);
+              if constexpr (MODE == kDPASS) b2[u][q] = ld2(a.coltab2 + off + 2 * q);
+            }
           }
 #pragma unroll
           for (int u = 0; u < UNR; ++u) {
-            double part = fma(rv.x, b[u].x, rv.y * b[u].y);
+            double part = fma(rv[0].x, b[u][0].x, rv[0].y * b[u][0].y);
+#pragma unroll
+            for (int q = 1; q < V; ++q) part = fma(rv[q].y, b[u][q].y, fma(rv[q].x, b[u][q].x, part));
             if constexpr (MODE == kDPASS) {
-              part = fma(rv2.x, b2[u].x, part);
-              part = fma(rv2.y, b2[u].y, part);
+#pragma unroll
+              for (int q = 0; q < V; ++q) part = fma(rv2[q].y, b2[u][q].y, fma(rv2[q].x, b2[u][q].x, part));
             }
             pd[st0 + u] = part;
           }
@@ -471,6 +482,12 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 template <int LPS>
 void seg_dispatch_mode(cudaStream_t s, int mode, const SegDev& dv, unsigned grid,
                        const Scalars* sc) {
+  // SDDMM / DPASS: from 16-wide rows on, 4 columns per lane (half the lanes per sample, half the
+  // transpose-reduction and index shuffles per sample)
+  if constexpr (LPS >= 8) {
+    if (mode == kSDDMM) { k_seg<LPS / 2, kSDDMM, 2><<<grid, 256, 0, s>>>(dv, sc); return; }
+    if (mode == kDPASS) { k_seg<LPS / 2, kDPASS, 2><<<grid, 256, 0, s>>>(dv, sc); return; }
+  }
   if (mode == kSDDMM) k_seg<LPS, kSDDMM><<<grid, 256, 0, s>>>(dv, sc);
   else if (mode == kDPASS) k_seg<LPS, kDPASS><<<grid, 256, 0, s>>>(dv, sc);
   else if (mode == kGSQ) k_seg<1, kGSQ><<<grid, 256, 0, s>>>(dv, sc);
