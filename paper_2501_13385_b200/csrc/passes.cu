@@ -71,7 +71,7 @@ struct SegOcc {
 // LPS lanes per sample, each holding V double2 of the row (ld = 2 LPS V)
 template <int LPS, int MODE, int V = 1>
 __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Scalars* sc) {
-  static_assert(V == 1 || MODE == kSDDMM || MODE == kDPASS, "vector lanes: SDDMM / DPASS only");
+  static_assert(V == 1 || MODE != kGSQ, "vector lanes: not for the scalar GSQ pass");
   if (sc && sc->noop) return;
   constexpr int G = 32 / LPS;        // samples per warp step
   constexpr int STEPS = 32 / G;      // steps per 32-sample chunk (= LPS)
@@ -97,7 +97,9 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
       if (MODE == kDPASS) rv2[q] = ld2(a.rowtab2 + trow * ld + 2 * (V * sub + q));
     }
     double accs = 0.0;
-    double2 accv = make_double2(0.0, 0.0);
+    double2 accv[V];
+#pragma unroll
+    for (int q = 0; q < V; ++q) accv[q] = make_double2(0.0, 0.0);
     for (int c0 = 0; c0 < cnt; c0 += 32) {
       const int nc = cnt - c0 < 32 ? cnt - c0 : 32;
       const int64_t s = beg + c0 + lane;
@@ -178,7 +180,7 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
       } else {
 #pragma unroll
       for (int st0 = 0; st0 < STEPS; st0 += UNR) {
-        double2 b[UNR];
+        double2 b[UNR][V];
         double xs[UNR];
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
@@ -187,13 +189,17 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
           const int t = (st0 + u) * G + grp;
           const int cidx = __shfl_sync(kFull, colv, t & 31);
           xs[u] = __shfl_sync(kFull, xv, t & 31);
-          b[u] = ld2(a.coltab + (cidx * ld + 2 * sub));   // < 2^31 (planner)
+          const int off = cidx * ld + 2 * V * sub;   // < 2^31 (planner)
+#pragma unroll
+          for (int q = 0; q < V; ++q) b[u][q] = ld2(a.coltab + off + 2 * q);
         }
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-          accv.x = fma(xs[u], b[u].x, accv.x);
-          accv.y = fma(xs[u], b[u].y, accv.y);
-        }
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            accv[q].x = fma(xs[u], b[u][q].x, accv[q].x);
+            accv[q].y = fma(xs[u], b[u][q].y, accv[q].y);
+          }
       }
       }
     }
@@ -214,26 +220,32 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
       }
     } else {
 #pragma unroll
-      for (int o = LPS; o < 32; o <<= 1) {
-        accv.x += __shfl_xor_sync(kFull, accv.x, o);
-        accv.y += __shfl_xor_sync(kFull, accv.y, o);
-      }
+      for (int o = LPS; o < 32; o <<= 1)
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          accv[q].x += __shfl_xor_sync(kFull, accv[q].x, o);
+          accv[q].y += __shfl_xor_sync(kFull, accv[q].y, o);
+        }
       if (grp == 0) {
         double* dst;
         if (pslot < 0) {
           const double f = a.rowscale ? a.rowscale[trow] : 1.0;
-          accv.x *= f;
-          accv.y *= f;
-          dst = a.out + trow * ld + 2 * sub;
-          if (a.accum) {
-            const double2 o = *reinterpret_cast<const double2*>(dst);
-            accv.x += o.x;
-            accv.y += o.y;
+          dst = a.out + trow * ld + 2 * V * sub;
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            accv[q].x *= f;
+            accv[q].y *= f;
+            if (a.accum) {
+              const double2 o = *reinterpret_cast<const double2*>(dst + 2 * q);
+              accv[q].x += o.x;
+              accv[q].y += o.y;
+            }
           }
         } else {
-          dst = a.part + (int64_t)pslot * ld + 2 * sub;
+          dst = a.part + (int64_t)pslot * ld + 2 * V * sub;
         }
-        *reinterpret_cast<double2*>(dst) = accv;
+#pragma unroll
+        for (int q = 0; q < V; ++q) *reinterpret_cast<double2*>(dst + 2 * q) = accv[q];
       }
     }
   }
@@ -491,7 +503,7 @@ void seg_dispatch_mode(cudaStream_t s, int mode, const SegDev& dv, unsigned grid
   if (mode == kSDDMM) k_seg<LPS, kSDDMM><<<grid, 256, 0, s>>>(dv, sc);
   else if (mode == kDPASS) k_seg<LPS, kDPASS><<<grid, 256, 0, s>>>(dv, sc);
   else if (mode == kGSQ) k_seg<1, kGSQ><<<grid, 256, 0, s>>>(dv, sc);
-  else k_seg<LPS, kSPMM><<<grid, 256, 0, s>>>(dv, sc);
+  else k_seg<LPS, kSPMM><<<grid, 256, 0, s>>>(dv, sc);   // (V = 2 measured slower for SpMM)
 }
 
 }  // namespace
