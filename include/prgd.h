@@ -93,7 +93,9 @@ PRGD_API int tt_create(int d, const int64_t* n, const int64_t* r, tt_ctx** out);
 PRGD_API int tt_destroy(tt_ctx* ctx);
 
 /* Use `stream` (a cudaStream_t, e.g. PyTorch's current stream) for all work.
- * NULL restores the library's own stream. */
+ * NULL restores the library's own stream.  Several contexts may share one stream:
+ * each captures its step graphs on a private stream and only launches them on this
+ * one.  tt_set_observations also uses a private side stream for the value upload. */
 PRGD_API int tt_set_stream(tt_ctx* ctx, void* stream);
 
 /* Route device allocations through alloc(bytes, user) / free(ptr, user) (e.g.
