@@ -744,7 +744,8 @@ void enqueue_update(tt_ctx* ctx, int64_t* lc, int part = 0) {
         launch_Y(s, true, t.V, t.ldV, t.X, t.wrow, t.ngroups, t.r0, t.nk, t.r1, t.Y, ctx->Ypart,
                  ctx->Ypart_cap, ctx->sc, lc);
         if (t.O)
-          launch_E_down(s, t.X, t.wrow, t.core, t.r0, t.nk, t.r1, t.O, t.ldO, t.ngroups, ctx->sc, lc);
+          launch_E_down(s, t.X, t.wrow, t.core, t.r0, t.nk, t.r1, t.O, t.ldO, t.ngroups, ctx->Ypart,
+                        ctx->Ypart_cap, ctx->sc, lc);
       }
       for (const BackwardLevel& t : BR) {
         if (back_fused_ok(t.r0, t.nk, t.r1)) {
@@ -755,7 +756,8 @@ void enqueue_update(tt_ctx* ctx, int64_t* lc, int part = 0) {
         launch_Y(s, false, t.V, t.ldV, t.X, t.wrow, t.ngroups, t.r0, t.nk, t.r1, t.Y, ctx->Ypart,
                  ctx->Ypart_cap, ctx->sc, lc);
         if (t.O)
-          launch_F_up(s, t.X, t.wrow, t.core, t.r0, t.nk, t.r1, t.O, t.ldO, t.ngroups, ctx->sc, lc);
+          launch_F_up(s, t.X, t.wrow, t.core, t.r0, t.nk, t.r1, t.O, t.ldO, t.ngroups, ctx->Ypart,
+                      ctx->Ypart_cap, ctx->sc, lc);
       }
     }
   }

@@ -29,7 +29,7 @@ namespace {
 
 constexpr int kNW = kDenseThreads / 32;
 constexpr int kMaxCols = 2 * kMaxRank;   // 64
-constexpr int kProjThreads = 1024;       // k_project: one CTA per core, latency-bound phases
+constexpr int kProjThreads = 512;        // k_project: one CTA per core, latency-bound phases
 
 __device__ __forceinline__ double shx(double v, int o) { return __shfl_xor_sync(0xffffffffu, v, o); }
 
@@ -935,6 +935,36 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_orth(DenseArgs a) {
   }
 }
 
+// z = (L L^T)^{-1} y for one row (r1 <= R): forward then back substitution in registers.
+template <int R>
+__device__ __forceinline__ void proj_solve_row(const double* y, double* z, const double* Ls, int r1) {
+  double zv[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) zv[i] = i < r1 ? y[i] : 0.0;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    if (i < r1) {
+      double sacc = zv[i];
+#pragma unroll
+      for (int c = 0; c < i; ++c) sacc = fma(-Ls[i * r1 + c], zv[c], sacc);
+      zv[i] = sacc / Ls[i * r1 + i];
+    }
+  }
+#pragma unroll
+  for (int i = R - 1; i >= 0; --i) {
+    if (i < r1) {
+      double sacc = zv[i];
+#pragma unroll
+      for (int c = i + 1; c < R; ++c)
+        if (c < r1) sacc = fma(-Ls[c * r1 + i], zv[c], sacc);
+      zv[i] = sacc / Ls[i * r1 + i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+    if (i < r1) z[i] = zv[i];
+}
+
 // One CTA per core k: projection (A10), unweighting (A11), assembly of B_k (A13).
 __global__ void __launch_bounds__(kProjThreads) k_project(DenseArgs a) {
   extern __shared__ double smraw[];
@@ -957,7 +987,7 @@ __global__ void __launch_bounds__(kProjThreads) k_project(DenseArgs a) {
     double* W = Ls + r1 * r1;                 // r1 x r1
     double* Z = W + r1 * r1;                  // m x ld (staged) or Ah
     const int ld = r1 | 1;                    // odd: row-per-thread substitutions below
-    const bool stage = (int64_t)m * ld * 2 + 2 * r1 * r1 <= a.smem_doubles;
+    const bool stage = (int64_t)m * ld * 2 + 2 * r1 * r1 + kProjThreads <= a.smem_doubles;
     double* Us = stage ? Z + (int64_t)m * ld : nullptr;
     const int zld = stage ? ld : r1;
     if (!stage) Z = Ah;
@@ -976,29 +1006,33 @@ __global__ void __launch_bounds__(kProjThreads) k_project(DenseArgs a) {
       }
       __syncthreads();
     }
+    // per row, in registers (the same operation order as a textbook forward / back solve)
     for (int row = threadIdx.x; row < m; row += blockDim.x) {
       const double* y = stage ? Z + (int64_t)row * zld : Y + (int64_t)row * r1;
       double* z = Z + (int64_t)row * zld;
-      for (int i = 0; i < r1; ++i) {
-        double s = y[i];
-        for (int c = 0; c < i; ++c) s = fma(-Ls[i * r1 + c], z[c], s);
-        z[i] = s / Ls[i * r1 + i];
-      }
-      for (int i = r1 - 1; i >= 0; --i) {
-        double s = z[i];
-        for (int c = i + 1; c < r1; ++c) s = fma(-Ls[c * r1 + i], z[c], s);
-        z[i] = s / Ls[i * r1 + i];
-      }
+      if (r1 <= 16) proj_solve_row<16>(y, z, Ls, r1);
+      else proj_solve_row<kMaxRank>(y, z, Ls, r1);
     }
     __syncthreads();
-    // W = L(U_k)^T Z  (r1 x r1)
+    // W = L(U_k)^T Z  (r1 x r1): thread groups take interleaved rows, partials summed in
+    // group order (fixed)
     const double* Uv = stage ? Us : U;
     const int uld = stage ? ld : r1;
-    for (int e = threadIdx.x; e < r1 * r1; e += blockDim.x) {
-      const int aa = e / r1, bb = e - aa * r1;
+    const int rr = r1 * r1;
+    const int ngrp = (int)blockDim.x / rr > 0 ? (int)blockDim.x / rr : 1;
+    double* Wp = smraw + 2 * rr + (stage ? 2 * (int64_t)m * ld : 0);   // ngrp x rr partials
+    for (int e = threadIdx.x; e < ngrp * rr; e += blockDim.x) {
+      const int gi = e / rr, el = e - gi * rr;
+      const int aa = el / r1, bb = el - aa * r1;
       double acc = 0.0;
-      for (int row = 0; row < m; ++row)
+      for (int row = gi; row < m; row += ngrp)
         acc = fma(Uv[(int64_t)row * uld + aa], Z[(int64_t)row * zld + bb], acc);
+      Wp[e] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < rr; e += blockDim.x) {
+      double acc = 0.0;
+      for (int gi = 0; gi < ngrp; ++gi) acc += Wp[gi * rr + e];
       W[e] = acc;
     }
     __syncthreads();

@@ -129,12 +129,14 @@ void launch_table_left(cudaStream_t s, const double* in, int ld_in, const double
 void launch_table_right(cudaStream_t s, const double* in, int ld_in, const double* core, int r0,
                         int nk, int r1, double* out, int ld_out, int64_t rows_out,
                         const double* rowscale, const Scalars* sc, int64_t* launches);
+// scratch (>= a few x rows_out x ld_out doubles, or 0): slice-split partials for levels with
+// few output rows
 void launch_E_down(cudaStream_t s, const double* Ein, int ld_in, const double* core, int r0,
-                   int nk, int r1, double* Eout, int ld_out, int64_t rows_out,
-                   const Scalars* sc, int64_t* launches);
+                   int nk, int r1, double* Eout, int ld_out, int64_t rows_out, double* scratch,
+                   int64_t scratch_cap, const Scalars* sc, int64_t* launches);
 void launch_F_up(cudaStream_t s, const double* Fin, int ld_in, const double* core, int r0, int nk,
-                 int r1, double* Fout, int ld_out, int64_t rows_out, const Scalars* sc,
-                 int64_t* launches);
+                 int r1, double* Fout, int ld_out, int64_t rows_out, double* scratch,
+                 int64_t scratch_cap, const Scalars* sc, int64_t* launches);
 // Y_k[i,j,c] = sum_p A[p,i] E[p*nk+j, c]   (left)   or
 // Y_k[i,j,c] = sum_q F[j+nk*q, i] B[q, c]  (right); split-K with deterministic reduce.
 void launch_Y(cudaStream_t s, bool left, const double* A, int ldA, const double* E, int ldE,

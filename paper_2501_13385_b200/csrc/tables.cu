@@ -94,9 +94,12 @@ __global__ void __launch_bounds__(kTabThreads) k_table_right(
 
 // E_k[p, i] = sum_{j,c} U_k(i, j, c) E_{k+1}[p n_k + j, c]; the core is staged
 // transposed ([j][c][i]) once per block (in chunks of slices) for kRecRows rows.
+// (grid.y > 1: block y takes the slices j in [y nk / grid.y, (y+1) nk / grid.y) and writes a
+// partial output to part[y], summed in y order by k_jsplit_reduce)
 __global__ void __launch_bounds__(kTabThreads) k_E_down(
     const double* __restrict__ Ein, int ld_in, const double* __restrict__ core, int r0, int nk,
-    int r1, double* __restrict__ Eout, int ld_out, int64_t rows, int jchunk, const Scalars* sc) {
+    int r1, double* __restrict__ Eout, int ld_out, int64_t rows, int jchunk, double* __restrict__ part,
+    const Scalars* sc) {
   if (sc && sc->noop) return;
   extern __shared__ double sm[];
   const int lanes = ld_out, per = blockDim.x / lanes;
@@ -106,8 +109,9 @@ __global__ void __launch_bounds__(kTabThreads) k_E_down(
   const int nloc = (kRecRows + per - 1) / per;
   for (int t = 0; t < nloc; ++t) acc[t] = 0.0;
   const int psz = r1 * r0;
-  for (int j0 = 0; j0 < nk; j0 += jchunk) {
-    const int jn = nk - j0 < jchunk ? nk - j0 : jchunk;
+  const int jbeg = (int)((int64_t)blockIdx.y * nk / gridDim.y), jend = (int)((int64_t)(blockIdx.y + 1) * nk / gridDim.y);
+  for (int j0 = jbeg; j0 < jend; j0 += jchunk) {
+    const int jn = jend - j0 < jchunk ? jend - j0 : jchunk;
     __syncthreads();
     for (int t = threadIdx.x; t < jn * psz; t += blockDim.x) {
       const int jj = t / psz, rem = t - jj * psz;
@@ -133,14 +137,16 @@ __global__ void __launch_bounds__(kTabThreads) k_E_down(
     for (int t = 0; t < nloc; ++t) {
       const int64_t p = p0 + pl + (int64_t)t * per;
       if (p >= rows || p >= p0 + kRecRows) break;
-      Eout[p * ld_out + i] = i < r0 ? acc[t] : 0.0;
+      double* dst = gridDim.y > 1 ? part + (int64_t)blockIdx.y * rows * ld_out : Eout;
+      dst[p * ld_out + i] = i < r0 ? acc[t] : 0.0;
     }
 }
 
 // F_{k+1}[q, c] = sum_{j,i} F_k[j + n_k q, i] U_k(i, j, c); core staged as [j][i][c].
 __global__ void __launch_bounds__(kTabThreads) k_F_up(
     const double* __restrict__ Fin, int ld_in, const double* __restrict__ core, int r0, int nk,
-    int r1, double* __restrict__ Fout, int ld_out, int64_t rows, int jchunk, const Scalars* sc) {
+    int r1, double* __restrict__ Fout, int ld_out, int64_t rows, int jchunk, double* __restrict__ part,
+    const Scalars* sc) {
   if (sc && sc->noop) return;
   extern __shared__ double sm[];
   const int lanes = ld_out, per = blockDim.x / lanes;
@@ -150,8 +156,9 @@ __global__ void __launch_bounds__(kTabThreads) k_F_up(
   const int nloc = (kRecRows + per - 1) / per;
   for (int t = 0; t < nloc; ++t) acc[t] = 0.0;
   const int psz = r0 * r1;
-  for (int j0 = 0; j0 < nk; j0 += jchunk) {
-    const int jn = nk - j0 < jchunk ? nk - j0 : jchunk;
+  const int jbeg = (int)((int64_t)blockIdx.y * nk / gridDim.y), jend = (int)((int64_t)(blockIdx.y + 1) * nk / gridDim.y);
+  for (int j0 = jbeg; j0 < jend; j0 += jchunk) {
+    const int jn = jend - j0 < jchunk ? jend - j0 : jchunk;
     __syncthreads();
     for (int t = threadIdx.x; t < jn * psz; t += blockDim.x) {
       const int jj = t / psz, rem = t - jj * psz;
@@ -177,7 +184,8 @@ __global__ void __launch_bounds__(kTabThreads) k_F_up(
     for (int t = 0; t < nloc; ++t) {
       const int64_t q = q0 + ql + (int64_t)t * per;
       if (q >= rows || q >= q0 + kRecRows) break;
-      Fout[q * ld_out + c] = c < r1 ? acc[t] : 0.0;
+      double* dst = gridDim.y > 1 ? part + (int64_t)blockIdx.y * rows * ld_out : Fout;
+      dst[q * ld_out + c] = c < r1 ? acc[t] : 0.0;
     }
 }
 
@@ -371,24 +379,56 @@ static int rec_jchunk(int r0, int nk, int r1) {
   return jc;
 }
 
+namespace {
+__global__ void k_jsplit_reduce(const double* __restrict__ part, int nsplit, int64_t n, double* __restrict__ out,
+                                const Scalars* sc) {
+  if (sc && sc->noop) return;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double acc = 0.0;
+  for (int y = 0; y < nsplit; ++y) acc += part[(int64_t)y * n + e];
+  out[e] = acc;
+}
+
+// slice splits for levels with few output rows (enough CTAs for the GPU), bounded by scratch
+int rec_jsplit(int64_t rows_out, int nk, int jc, int ld_out, int64_t scratch_cap) {
+  const int64_t rb = (rows_out + kRecRows - 1) / kRecRows;
+  int64_t js = rb >= 148 ? 1 : (296 + rb - 1) / rb;
+  js = std::min<int64_t>(js, (nk + jc - 1) / jc);
+  if (scratch_cap > 0) js = std::min<int64_t>(js, scratch_cap / std::max<int64_t>(1, rows_out * ld_out));
+  else js = 1;
+  return (int)std::max<int64_t>(1, js);
+}
+}  // namespace
+
 void launch_E_down(cudaStream_t s, const double* Ein, int ld_in, const double* core, int r0,
-                   int nk, int r1, double* Eout, int ld_out, int64_t rows_out,
-                   const Scalars* sc, int64_t* launches) {
+                   int nk, int r1, double* Eout, int ld_out, int64_t rows_out, double* scratch,
+                   int64_t scratch_cap, const Scalars* sc, int64_t* launches) {
   const int jc = rec_jchunk(r0, nk, r1);
   const size_t smem = (size_t)jc * r0 * r1 * sizeof(double);
-  k_E_down<<<blocks_for(rows_out, kRecRows), kTabThreads, smem, s>>>(Ein, ld_in, core, r0, nk, r1,
-                                                                     Eout, ld_out, rows_out, jc, sc);
+  const int js = rec_jsplit(rows_out, nk, jc, ld_out, scratch_cap);
+  dim3 grid(blocks_for(rows_out, kRecRows), js);
+  k_E_down<<<grid, kTabThreads, smem, s>>>(Ein, ld_in, core, r0, nk, r1, Eout, ld_out, rows_out, jc, scratch, sc);
   ++*launches;
+  if (js > 1) {
+    k_jsplit_reduce<<<blocks_for(rows_out * ld_out, 256), 256, 0, s>>>(scratch, js, rows_out * ld_out, Eout, sc);
+    ++*launches;
+  }
 }
 
 void launch_F_up(cudaStream_t s, const double* Fin, int ld_in, const double* core, int r0, int nk,
-                 int r1, double* Fout, int ld_out, int64_t rows_out, const Scalars* sc,
-                 int64_t* launches) {
+                 int r1, double* Fout, int ld_out, int64_t rows_out, double* scratch,
+                 int64_t scratch_cap, const Scalars* sc, int64_t* launches) {
   const int jc = rec_jchunk(r0, nk, r1);
   const size_t smem = (size_t)jc * r0 * r1 * sizeof(double);
-  k_F_up<<<blocks_for(rows_out, kRecRows), kTabThreads, smem, s>>>(Fin, ld_in, core, r0, nk, r1,
-                                                                   Fout, ld_out, rows_out, jc, sc);
+  const int js = rec_jsplit(rows_out, nk, jc, ld_out, scratch_cap);
+  dim3 grid(blocks_for(rows_out, kRecRows), js);
+  k_F_up<<<grid, kTabThreads, smem, s>>>(Fin, ld_in, core, r0, nk, r1, Fout, ld_out, rows_out, jc, scratch, sc);
   ++*launches;
+  if (js > 1) {
+    k_jsplit_reduce<<<blocks_for(rows_out * ld_out, 256), 256, 0, s>>>(scratch, js, rows_out * ld_out, Fout, sc);
+    ++*launches;
+  }
 }
 
 int64_t Y_partial_need(int64_t nsum, int r0, int nk, int r1) {
