@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     from concurrent.futures import ThreadPoolExecutor
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    cflags = [f for f in FLAGS if f != "-shared"]
+    cflags = [f for f in FLAGS if f != "-shared"] + os.environ.get("PRGD_EXTRA_NVCC", "").split()
     inc = ["-I", os.path.join(ROOT, "include")]
 
     def compile_one(src):
