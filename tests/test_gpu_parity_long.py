@@ -1,0 +1,51 @@
+"""Long GPU parity against stored oracle iterates (tests/golden, written by
+tools/make_golden.py from synth + oracle only): the configurations BASELINE.json's north star
+names at their full sizes, through the C-ABI, in bench.py's launch configuration.
+
+Tolerances (BASELINE.json north star): relative Frobenius error of the iterate (gauge-free,
+block-TT QR norm) <= 1e-11 after one step from the identical state and <= 1e-8 after 50
+iterations; intermediate saved iterates <= 1e-8; residual norms <= 1e-8 relative."""
+import numpy as np
+import pytest
+
+import oracle
+from tests import _golden as G
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2501_13385_b200 as p
+    p.load()
+    return p
+
+
+@pytest.mark.parametrize("case", ["cfg3_full_50steps", "cfg4_full_50steps", "cfg5_4e6_50steps",
+                                  "cfg5_full_1step", "cfg5_full_50steps"])
+def test_golden_iterates(pkg, case):
+    cfg, m, step, steps, keep = G.CASES[case]
+    gold = G.load(case)                     # a missing file fails the test (no skip)
+    pr = G.problem(cfg, m)
+    assert G.input_sha(pr) == gold["sha"], "stale golden file: synth inputs changed"
+    y = G.observations(pr)
+    assert pr.m == gold["m"]
+    assert abs(float(np.sum(y)) - gold["ysum"]) <= 1e-10 * np.sqrt(gold["ysq"] * pr.m)
+    assert abs(float(np.dot(y, y)) - gold["ysq"]) <= 1e-12 * gold["ysq"]
+    ctx = pkg.TTContext(pr.n, pr.r)
+    ctx.set_observations(pr.idx, y)
+    ctx.set_cores(pr.init)
+    res0 = ctx.residual_norm()
+    assert abs(res0 - gold["res"][0]) <= 1e-11 * gold["res"][0]
+    errs = {}
+    for it in range(1, gold["steps"] + 1):
+        ctx.step(step)
+        if it < len(gold["res"]):
+            r = ctx.residual_norm()
+            assert abs(r - gold["res"][it]) <= 1e-8 * gold["res"][it], (it, r, gold["res"][it])
+        if it in gold["iterates"]:
+            err = oracle.tt_diff_norm(ctx.get_cores(), gold["iterates"][it])
+            errs[it] = err
+            assert err <= (1e-11 if it == 1 else 1e-8), (it, err)
+    ctx.close()
+    print(f"{case}: relative errors {errs}")
