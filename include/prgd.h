@@ -73,7 +73,7 @@ typedef struct tt_ctx tt_ctx;
  *                  (eq. `PRGD stepsize`; with TT_EPS_NONE RGD's
  *                  ||P_T G||^2 / ||P_Omega P_T G||^2).  Costs one more pass
  *                  over Omega per step (the tangent vector evaluated at every sample);
- *                  alpha_l = 0 if that vanishes.  Needs 2 r_k <= 32. */
+ *                  alpha_l = 0 if that vanishes. */
 enum { TT_EPS_VEE = 0, TT_EPS_FIXED = 1, TT_EPS_NONE = 2 };
 enum { TT_STEP_THEORY = 0, TT_STEP_RAW = 1, TT_STEP_ADAPTIVE = 2 };
 
@@ -104,14 +104,31 @@ PRGD_API int tt_set_stream(tt_ctx* ctx, void* stream);
 PRGD_API int tt_set_allocator(tt_ctx* ctx, void* (*alloc)(size_t bytes, void* user),
                      void (*release)(void* ptr, void* user), void* user);
 
+/* Path over Omega.  Both compute the same iteration; they differ in how the
+ * left / right parts T^{<=k-1}, T^{>=k+1} of every sample are formed:
+ *   TT_PATH_TABLES  memoised prefix / suffix tables in HBM (one split K_L), passes over Omega
+ *                   as sampled dense-dense / sparse-dense products (tables needed: see tt_create)
+ *   TT_PATH_CHAINS  per-sample chains of r x r slice products ("fast recursive computations",
+ *                   PAPER.md:146), interfaces materialised per sample (2 sum_k r_k doubles each),
+ *                   per-mode buckets (A0) and a segmented contraction per slice (DMMA where a
+ *                   piece holds >= 32 samples, rank-1 updates otherwise)
+ *   TT_PATH_AUTO    tables when they fit, else chains (default)
+ * Must be called before any core or observation is set (TT_ERR_STATE); TT_PATH_TABLES on a
+ * shape whose tables do not fit returns TT_ERR_UNSUPPORTED.  tt_get_path reports the path in
+ * use (resolved from AUTO). */
+enum { TT_PATH_AUTO = 0, TT_PATH_TABLES = 1, TT_PATH_CHAINS = 2 };
+PRGD_API int tt_set_path(tt_ctx* ctx, int path);
+PRGD_API int tt_get_path(tt_ctx* ctx, int* path);
+
 /* ------------------------------------------------------------------ data */
 
 /* Set the observed set Omega: h_idx[m][d] sample-major int32
  * multi-indices (0-based), h_vals[m] the observed values y_s.  Omega is a set:
  * duplicate multi-indices are the caller's error (not detected).  Validates every
  * index (TT_ERR_INDEX), copies to the device and builds the one-time bucketing
- * (A0: stable LSD counting sorts into prefix and suffix order).  m = 0 is
- * allowed (empty Omega).  m must be < 2^31.  Sets p = m / prod(n) (reading R3). */
+ * (A0: stable LSD counting sorts -- into prefix and suffix order on the table path, by x_k
+ * for every mode k on the chain path).  m = 0 is allowed (empty Omega).  m must be < 2^31.
+ * Sets p = m / prod(n) (reading R3). */
 PRGD_API int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals, int64_t m);
 
 /* Copy core k (0 <= k < d) in/out, [r[k]][n[k]][r[k+1]] C-order float64.
@@ -123,7 +140,9 @@ PRGD_API int tt_get_core(tt_ctx* ctx, int k, double* h_core_out);
 
 /* Metric / step rules, see the enums above.  eps is used by TT_EPS_FIXED only
  * (must be > 0 then).  Defaults: TT_EPS_VEE, TT_STEP_THEORY.  TT_STEP_ADAPTIVE allocates
- * its buffers here (TT_ERR_OOM; TT_ERR_RANK if some 2 r_k > 32). */
+ * its buffers here (TT_ERR_OOM).  The denominator ||P_Omega D||^2 is evaluated through the
+ * tables when 2 r_k <= 32 on the table path, else by per-sample chains of the rank-2r tangent
+ * TT (the multi-indices of Omega stay on the device for this). */
 PRGD_API int tt_set_metric(tt_ctx* ctx, int eps_rule, double eps, int step_rule);
 
 /* Spectral initialisation at scale: set every core to
@@ -133,8 +152,8 @@ PRGD_API int tt_set_metric(tt_ctx* ctx, int eps_rule, double eps, int step_rule)
  * Gram of the projected unfolding, accumulated over the samples grouped by (x_{k+1..d}, x_k)
  * (DESIGN.md §2).  Gram-based, so the kept subspace is accurate to ~u ||G|| / eigen-gap.
  * Needs observations (TT_ERR_STATE otherwise, and in sharded mode), prod(n) < 2^62 and
- * r_{k-1} n_k <= 1024 for k < d (TT_ERR_ARG).  Synchronous.  Output cores 0..d-2 have
- * orthonormal columns L(T_k). */
+ * r_{k-1} n_k <= 1024 for k < d (TT_ERR_ARG), and the table path (TT_ERR_STATE on the chain
+ * path).  Synchronous.  Output cores 0..d-2 have orthonormal columns L(T_k). */
 PRGD_API int tt_spectral_init(tt_ctx* ctx);
 
 /* ------------------------------------------------------------------ the hot path */
@@ -185,25 +204,11 @@ PRGD_API int tt_set_allreduce(tt_ctx* ctx, tt_allreduce_fn fn, void* user, int64
 /* ------------------------------------------------------------------ introspection */
 
 /* Host-only planning (no device needed): validates (d, n, r) like tt_create and
- * returns the prefix/suffix split K_L (1..d-1) used by the bucketing and the
- * dense partial-product tables: N_L = prod(n[0..K_L-1]), N_R = prod(n[K_L..d-1]).
+ * returns the prefix/suffix split K_L (1..d-1) used by the table path's bucketing and
+ * partial-product tables: N_L = prod(n[0..K_L-1]), N_R = prod(n[K_L..d-1]).  For shapes
+ * whose tables do not fit (TT_PATH_AUTO resolves to the chain path) K_L = 0, N_L = N_R = 0.
  * Any output pointer may be NULL. */
 PRGD_API int tt_plan(int d, const int64_t* n, const int64_t* r, int* K_L, int64_t* N_L, int64_t* N_R);
-
-/* Host-only: the layout of the two bucketing orders (A0).
- *  nb_L / nb_R  gather blocks: the prefix order groups samples by the virtual row
- *               VP = floor(S nb_L / N_R) N_L + P, the suffix order by
- *               VS = floor(P nb_R / N_L) N_R + S; TT_DBG_OFFS_L / _R then have
- *               nb_L N_L + 1 / nb_R N_R + 1 entries.  Default 1 (blocking measured slower
- *               on B200); PRGD_GATHER_BLOCKS (a power of two) overrides.
- *  middle       1 when the passes re-associate through the middle cores K_L-1, K_L (0-based)
- *               (DESIGN.md §2): within a prefix row samples are then ordered by
- *               (x_{K_L}, S div n_{K_L}), within a suffix row by (x_{K_L-1}, P div n_{K_L-1}).
- *               Chosen from the shapes (both sides >= 65536 rows, middle n r <= 512, r <= 32);
- *               PRGD_MIDDLE=0/1 overrides.
- * Any output pointer may be NULL.  Validation and errors as tt_plan. */
-PRGD_API int tt_plan_layout(int d, const int64_t* n, const int64_t* r, int* nb_L, int* nb_R,
-                            int* middle);
 
 /* Counters: launches = kernels this context launched since creation (graph nodes
  * counted per replay); steps = tt_prgd_step calls. */
@@ -228,10 +233,10 @@ PRGD_API const char* tt_profile_name(int group);
  * what = TT_DBG_* below, k = mode where relevant, cap = capacity in elements.
  * Returns the element count in *count.  Synchronises. */
 enum {
-  TT_DBG_PERM_PRE = 1,   /* int32[m]   sample ids in prefix order            (A0) */
-  TT_DBG_OFFS_L = 2,     /* int64[nb_L N_L+1] prefix virtual-row offsets     (A0) */
-  TT_DBG_PERM_SUF = 3,   /* int32[m]   sample ids in suffix order            (A0) */
-  TT_DBG_OFFS_R = 4,     /* int64[nb_R N_R+1] suffix virtual-row offsets     (A0) */
+  TT_DBG_PERM_PRE = 1,   /* int32[m]   sample ids in prefix order (table path)  (A0) */
+  TT_DBG_OFFS_L = 2,     /* int64[N_L+1] prefix bucket offsets (table path)     (A0) */
+  TT_DBG_PERM_SUF = 3,   /* int32[m]   sample ids in suffix order (table path)  (A0) */
+  TT_DBG_OFFS_R = 4,     /* int64[N_R+1] suffix bucket offsets (table path)     (A0) */
   TT_DBG_RESID = 5,      /* double[m]  g_s in ORIGINAL sample order          (A2) */
   TT_DBG_H = 6,          /* double[n_k] h_{k,j} of the last pass A           (A3) */
   TT_DBG_PHI = 7,        /* double[n_k] phi_{k,j} of the last step           (A3) */
@@ -240,7 +245,9 @@ enum {
   TT_DBG_U = 9,          /* double[core k] U_k of the last step              (A5) */
   TT_DBG_P = 10,         /* double[r_k+1 ^2] P_{k+1} (right Gram) of last step (A6) */
   TT_DBG_Y = 11,         /* double[core k] Y_k of the last step              (A9) */
-  TT_DBG_AHAT = 12       /* double[core k] Ahat_k of the last step           (A10) */
+  TT_DBG_AHAT = 12,      /* double[core k] Ahat_k of the last step           (A10) */
+  TT_DBG_PERM_MODE = 13, /* int32[m]   sample ids bucketed by x_k (chain path) (A0) */
+  TT_DBG_OFFS_MODE = 14  /* int64[n_k+1] mode-k bucket offsets (chain path)    (A0) */
 };
 PRGD_API int tt_debug_get(tt_ctx* ctx, int what, int k, void* h_out, int64_t cap, int64_t* count);
 

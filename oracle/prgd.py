@@ -450,18 +450,12 @@ def split_point(n: Sequence[int]) -> int:
     return best
 
 
-def stable_order(idx, n, K_L, nb_L=1, nb_R=1, middle=False):
-    """A0 as built here: samples bucketed by prefix index
-    P(s) = mixed radix of (x_1..x_{K_L}) (x_1 most significant) and by suffix index
-    S(s) = mixed radix of (x_{K_L+1}..x_d) (x_d most significant), grouped first by the
-    gather block of the other index: virtual rows VP = floor(S nb_L / N_R) N_L + P and
-    VS = floor(P nb_R / N_L) N_R + S (nb = 1: plain P / S buckets).
-    Prefix order = stable argsort of key VP*2^bS + S; suffix order = stable argsort of
-    VS*2^bP + P.  With `middle`, the in-row keys put the middle digits first:
-    S -> (S mod n_{K_L+1}) N_R/n_{K_L+1} + S div n_{K_L+1} (x_{K_L+1} most significant) and
-    P -> (P mod n_{K_L}) N_L/n_{K_L} + P div n_{K_L} (x_{K_L} most significant), 1-based mode
-    numbers as in the paper.  Returns dict(perm_pre, offs_L, perm_suf, offs_R, P, S) with
-    offsets over the nb_L N_L (nb_R N_R) virtual rows."""
+def stable_order(idx, n, K_L):
+    """A0 on the table path: samples bucketed by the prefix index
+    P(s) = mixed radix of (x_1..x_{K_L}) (x_1 most significant) and by the suffix index
+    S(s) = mixed radix of (x_{K_L+1}..x_d) (x_d most significant).  Prefix order = stable
+    argsort of the key P*2^bS + S (i.e. by (P, S)); suffix order = stable argsort of
+    S*2^bP + P.  Returns dict(perm_pre, offs_L, perm_suf, offs_R, P, S)."""
     idx = np.asarray(idx, dtype=np.int64)
     d = len(n)
     P = np.zeros(idx.shape[0], dtype=np.int64)
@@ -472,25 +466,18 @@ def stable_order(idx, n, K_L, nb_L=1, nb_R=1, middle=False):
         S = S * n[k] + idx[:, k]
     NL, NR = math.prod(n[:K_L]), math.prod(n[K_L:])
     bP, bS = max(1, int(NL - 1).bit_length()), max(1, int(NR - 1).bit_length())
-    VP = (S * nb_L // NR) * NL + P
-    VS = (P * nb_R // NL) * NR + S
-    Sk, Pk = S, P
-    if middle:
-        nR, nL = n[K_L], n[K_L - 1]
-        Sk = (S % nR) * (NR // nR) + S // nR
-        Pk = (P % nL) * (NL // nL) + P // nL
-    kpre = (VP << bS) | Sk
-    ksuf = (VS << bP) | Pk
-    perm_pre = np.argsort(kpre, kind="stable")
-    perm_suf = np.argsort(ksuf, kind="stable")
-    offs_L = np.concatenate([[0], np.cumsum(np.bincount(VP, minlength=NL * nb_L))])
-    offs_R = np.concatenate([[0], np.cumsum(np.bincount(VS, minlength=NR * nb_R))])
+    perm_pre = np.argsort((P << bS) | S, kind="stable")
+    perm_suf = np.argsort((S << bP) | P, kind="stable")
+    offs_L = np.concatenate([[0], np.cumsum(np.bincount(P, minlength=NL))])
+    offs_R = np.concatenate([[0], np.cumsum(np.bincount(S, minlength=NR))])
     return dict(perm_pre=perm_pre, offs_L=offs_L, perm_suf=perm_suf, offs_R=offs_R, P=P, S=S)
 
 
 def stable_buckets(idx, n):
-    """Per-mode buckets: perm_k = stable argsort of x_{:,k},
-    offs_k = exclusive cumulative counts."""
+    """A0 per-mode buckets (the chain path): for each mode k, perm_k = the
+    stable argsort of x_{:,k} (bucket j = the samples with x_{s,k} = j, the rows of the mode-k
+    unfolding M_k(G) that PAPER.md:163 sums over, in ascending s), offs_k = exclusive
+    cumulative bucket counts (n_k + 1 entries)."""
     out = []
     for k in range(len(n)):
         perm = np.argsort(idx[:, k], kind="stable")

@@ -27,7 +27,8 @@ STATUS_NAMES = {0: "TT_OK", -1: "TT_ERR_ARG", -2: "TT_ERR_RANK", -3: "TT_ERR_IND
 EPS_RULES = {"vee": 0, "fixed": 1, "none": 2}
 STEP_RULES = {"theory": 0, "raw": 1, "adaptive": 2}
 DBG = {"perm_pre": 1, "offs_l": 2, "perm_suf": 3, "offs_r": 4, "resid": 5, "h": 6, "phi": 7,
-       "eps": 8, "u": 9, "p": 10, "y": 11, "ahat": 12}
+       "eps": 8, "u": 9, "p": 10, "y": 11, "ahat": 12, "perm_mode": 13, "offs_mode": 14}
+PATHS = {"auto": 0, "tables": 1, "chains": 2}
 
 
 class PRGDError(RuntimeError):
@@ -76,8 +77,8 @@ def load() -> ctypes.CDLL:
         "tt_last_error": (ctypes.c_char_p, [P]),
         "tt_plan": (ctypes.c_int, [ctypes.c_int, i64p, i64p, ctypes.POINTER(ctypes.c_int),
                                    i64p, i64p]),
-        "tt_plan_layout": (ctypes.c_int, [ctypes.c_int, i64p, i64p, ctypes.POINTER(ctypes.c_int),
-                                          ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
+        "tt_set_path": (ctypes.c_int, [P, ctypes.c_int]),
+        "tt_get_path": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_int)]),
         "tt_spectral_init": (ctypes.c_int, [P]),
         "tt_set_allreduce": (ctypes.c_int, [P, ALLREDUCE_FN, P, ctypes.c_int64]),
         "tt_get_stats": (ctypes.c_int, [P, ctypes.POINTER(_Stats)]),
@@ -110,22 +111,6 @@ def plan(n: Sequence[int], r: Sequence[int]):
     return kl.value, nl.value, nr.value
 
 
-def plan_layout(n: Sequence[int], r: Sequence[int]):
-    """Host-only bucketing layout (tt_plan_layout): returns (nb_L, nb_R, middle)."""
-    lib = load()
-    bl, br, mid = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
-    rc = lib.tt_plan_layout(len(n), _i64(n), _i64(r), ctypes.byref(bl), ctypes.byref(br),
-                            ctypes.byref(mid))
-    if rc != TT_OK:
-        raise PRGDError(rc, "tt_plan_layout")
-    return bl.value, br.value, bool(mid.value)
-
-
-def plan_blocks(n: Sequence[int], r: Sequence[int]):
-    """(nb_L, nb_R) of plan_layout."""
-    return plan_layout(n, r)[:2]
-
-
 def _ptr(a: np.ndarray) -> int:
     return a.ctypes.data
 
@@ -142,19 +127,30 @@ class TTContext:
     allocated on) are reused by the next context instead of fresh cudaMalloc calls; pass
     stream= to give a context its own stream."""
 
-    def __init__(self, n: Sequence[int], r: Sequence[int], use_torch: bool = True, stream=None):
+    def __init__(self, n: Sequence[int], r: Sequence[int], use_torch: bool = True, stream=None,
+                 path: str = "auto"):
         self.lib = load()
         self.n = tuple(int(v) for v in n)
         self.r = tuple(int(v) for v in r)
         self.d = len(self.n)
+        self.m = 0
         self._h = ctypes.c_void_p()
         rc = self.lib.tt_create(self.d, _i64(self.n), _i64(self.r), ctypes.byref(self._h))
         if rc != TT_OK:
             raise PRGDError(rc, "tt_create")
         self.stream = None
         self._keep = []
+        if path != "auto":
+            self._check(self.lib.tt_set_path(self._h, PATHS[path]), "tt_set_path")
         if use_torch:
             self._attach_torch(stream)
+
+    @property
+    def path(self) -> str:
+        """The path over Omega in use (tt_get_path): "tables" or "chains"."""
+        v = ctypes.c_int()
+        self._check(self.lib.tt_get_path(self._h, ctypes.byref(v)), "tt_get_path")
+        return {1: "tables", 2: "chains"}[v.value]
 
     # -- plumbing: PyTorch device memory and stream
     def _attach_torch(self, stream=None):
@@ -223,8 +219,10 @@ class TTContext:
         m = vals.shape[0]
         if m and idx.shape != (m, self.d):
             raise ValueError("idx must be [m, d]")
+        self.m = 0
         self._check(self.lib.tt_set_observations(self._h, _ptr(idx), _ptr(vals), m),
                     "tt_set_observations")
+        self.m = int(m)
 
     def set_core(self, k: int, core: np.ndarray):
         core = np.ascontiguousarray(core, dtype=np.float64)
@@ -290,7 +288,7 @@ class TTContext:
     def debug(self, what: str, k: int = 0) -> np.ndarray:
         """Read back internal device state (tt_debug_get; tests only)."""
         code = DBG[what]
-        dt = np.int32 if code in (1, 3) else (np.int64 if code in (2, 4) else np.float64)
+        dt = np.int32 if code in (1, 3, 13) else (np.int64 if code in (2, 4, 14) else np.float64)
         out = np.empty(max(self._debug_size(code, k), 4), dtype=dt)
         cnt = ctypes.c_int64()
         self._check(self.lib.tt_debug_get(self._h, code, k, _ptr(out), out.shape[0],
@@ -298,12 +296,13 @@ class TTContext:
         return out[:cnt.value]
 
     def _debug_size(self, code, k):
-        if code in (1, 3, 5):
-            return self._m_query()
+        if code in (1, 3, 5, 13):
+            return self.m
         if code in (2, 4):
             kl, nl, nr = plan(self.n, self.r)
-            bl, br = plan_blocks(self.n, self.r)
-            return (nl * bl if code == 2 else nr * br) + 1
+            return (nl if code == 2 else nr) + 1
+        if code == 14:
+            return self.n[k] + 1
         if code in (6, 7):
             return self.n[k]
         if code == 8:
@@ -313,16 +312,6 @@ class TTContext:
         if code == 10:
             return self.r[k + 1] ** 2
         return 0
-
-    def _m_query(self):
-        kl, nl, nr = plan(self.n, self.r)
-        bl, br = plan_blocks(self.n, self.r)
-        offs = np.empty(nl * bl + 1, dtype=np.int64)
-        cnt = ctypes.c_int64()
-        rc = self.lib.tt_debug_get(self._h, 2, 0, _ptr(offs), offs.shape[0], ctypes.byref(cnt))
-        if rc != TT_OK or cnt.value == 0:
-            return 0
-        return int(offs[-1])
 
 
 def torch_allreduce(group=None):

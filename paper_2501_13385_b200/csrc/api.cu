@@ -40,52 +40,14 @@ int64_t sat_mul(int64_t a, int64_t b) {
 }
 
 struct Plan {
-  int KL = 0;
+  int KL = 0;             // table path: prefix/suffix split (0 on the chain path)
   int64_t NL = 0, NR = 0;
-  int nbL = 1, nbR = 1;   // gather blocks of the prefix / suffix orders (A0)
-  bool mid = false;       // middle-split passes: rows re-associated through
-                          // the cores K_L-1 and K_L, gathers from the level K_L-1 / K_L+1 tables
+  bool chain = false;     // per-sample chain path (chains.cu) instead of the tables
 };
 
-// Middle-split passes apply when both middle cores are small (n r <= 512 with ranks <= 32),
-// K_L >= 2 and d - K_L >= 2 (the gathered tables are the levels K_L-1 and K_L+1), and both
-// sides have >= 65536 rows (a CTA tile is 32 rows handled by one 8-lane group each).
-// PRGD_MIDDLE=0/1 overrides (experiments; shape conditions still apply).
-bool middle_ok(int d, const int64_t* n, const int64_t* r, int KL, int64_t NL, int64_t NR) {
-  if (KL < 2 || d - KL < 2) return false;
-  for (int k = KL - 1; k <= KL + 1; ++k)
-    if (r[k] > 32) return false;
-  auto pad = [](int64_t v) { int64_t p = 2; while (p < v) p <<= 1; return p; };
-  // 8-lane sample groups (2 fp64 per lane) and <= 113 KB of shared memory per CTA
-  if (pad(r[KL - 1]) > 16 || pad(r[KL]) > 16 || pad(r[KL + 1]) > 16) return false;
-  if (n[KL] * pad(r[KL + 1]) > 256 || n[KL - 1] * pad(r[KL - 1]) > 256) return false;
-  if (n[KL] * pad(r[KL + 1]) % 8 != 0 || n[KL - 1] * pad(r[KL - 1]) % 8 != 0) return false;
-  // Off by default: measured on B200 at config 5 the middle-split kernels cut DRAM traffic
-  // ~5x (L2 hit rate 82-86%) but are latency-bound on the per-row chains (pass A 2.3-3.8 ms,
-  // pass B 1.5-2.7 ms vs 1.1 / 0.86 ms for the gather passes; profiles/r01_middle_split.md).
-  const char* env = getenv("PRGD_MIDDLE");
-  if (env && *env) return atoi(env) != 0 && NL >= 32 && NR >= 32;
-  (void)NL;
-  (void)NR;
-  return false;
-}
-
-// Number of column blocks for a bucketing side whose gathered table has `rows` rows of
-// `ld` doubles.  Measured on B200 at config 5 (profiles/r01_gather_blocks.md): 2, 4, 8 blocks
-// made every pass slower (1.06 -> 1.52 / 2.57 / 4.67 ms for pass A), i.e. the passes are bound
-// by per-row work, not by gather misses, so the default is 1; PRGD_GATHER_BLOCKS overrides.
-int gather_blocks(int64_t rows, int ld) {
-  const char* env = getenv("PRGD_GATHER_BLOCKS");
-  if (env && *env) {
-    int v = atoi(env);
-    if (v >= 1 && v <= 64 && (v & (v - 1)) == 0) return v;
-  }
-  (void)rows;
-  (void)ld;
-  return 1;
-}
-
-int validate_and_plan(int d, const int64_t* n, const int64_t* r, Plan* pl, std::string* msg) {
+// path: TT_PATH_AUTO (tables when they fit, else chains), TT_PATH_TABLES, TT_PATH_CHAINS.
+int validate_and_plan(int d, const int64_t* n, const int64_t* r, Plan* pl, std::string* msg,
+                      int path = TT_PATH_AUTO) {
   if (d < 2 || d > kMaxD || !n || !r) {
     *msg = "need 2 <= d <= 64 and non-null n, r";
     return TT_ERR_ARG;
@@ -132,27 +94,25 @@ int validate_and_plan(int d, const int64_t* n, const int64_t* r, Plan* pl, std::
       bNR = NR;
     }
   }
-  if (bestv > ((int64_t)1 << 30)) {
-    *msg = "no prefix/suffix split with both table sizes <= 2^30 rows";
-    return TT_ERR_UNSUPPORTED;
-  }
-  {   // the pass kernels index the gathered split-level table with 32-bit offsets
+  bool tables_fit = bestv <= ((int64_t)1 << 30);
+  if (tables_fit) {   // the pass kernels index the gathered split-level table with 32-bit offsets
     int pr = 2;
     while (pr < r[best]) pr <<= 1;
-    if (bestv * pr >= ((int64_t)1 << 31)) {
-      *msg = "split-level tables above 2^31 doubles (16 GB) are not supported";
-      return TT_ERR_UNSUPPORTED;
-    }
+    tables_fit = bestv * pr < ((int64_t)1 << 31);
+  }
+  if (path == TT_PATH_TABLES && !tables_fit) {
+    *msg = "table path: no prefix/suffix split with both table sizes <= 2^30 rows and split-level "
+           "tables below 2^31 doubles";
+    return TT_ERR_UNSUPPORTED;
+  }
+  *pl = Plan();
+  if (path == TT_PATH_CHAINS || !tables_fit) {
+    pl->chain = true;
+    return TT_OK;
   }
   pl->KL = best;
   pl->NL = bNL;
   pl->NR = bNR;
-  int rk = 2;
-  while (rk < r[best]) rk <<= 1;
-  pl->nbL = gather_blocks(bNR, rk);   // prefix order gathers right-table rows
-  pl->nbR = gather_blocks(bNL, rk);   // suffix order gathers left-table rows
-  pl->mid = middle_ok(d, n, r, best, bNL, bNR);
-  if (pl->mid) pl->nbL = pl->nbR = 1;
   return TT_OK;
 }
 
@@ -188,11 +148,22 @@ struct tt_ctx {
   std::vector<double*> LT, EL, RT, FR;
   double *HL = nullptr, *HR = nullptr, *psiL = nullptr, *psiR = nullptr, *Ypart = nullptr;
   double* margp = nullptr;      // marginal chunk partials, 32 * sum(n)
-  double *psiL1 = nullptr, *psiR1 = nullptr;   // middle-split weights (N_L/n_{KL-1}, N_R/n_KL)
-  double *TL1 = nullptr, *TR1 = nullptr;       // U tables of levels KL-1 / KL+1 scaled by psiL1 / psiR1
   double* g_suf = nullptr;      // residual in suffix order (written by pass A)
   int32_t* pre2suf = nullptr;   // suffix position of prefix position t
   int64_t Ypart_cap = 0;
+
+  int path_req = TT_PATH_AUTO;  // tt_set_path
+  // observed multi-indices, int32 [m][d] (the ABI layout), kept on the device: the chain path
+  // reads them every pass; the table path uses them for the adaptive denominator when 2r > 32
+  int32_t* idx_dev = nullptr;
+  // chain path (chains.cu): values / residual / preconditioned residual in the original sample
+  // order, interfaces IL_k / IR_k [k][s][r_k], per-mode buckets and their pieces
+  double *yobs = nullptr, *ghat = nullptr, *IL = nullptr, *IR = nullptr;
+  ChainPieces pcs;
+  ChainTT ctt{};
+  double* dval = nullptr;       // adaptive step by chains: D(x_s)^2
+  double* Dblk = nullptr;       // adaptive step by chains: block cores of the tangent vector
+  ChainTT dtt{};
 
   bool obs_set = false;
   int64_t m = 0;
@@ -349,6 +320,33 @@ int ensure_base(tt_ctx* ctx) {
             A(ctx, &ctx->work, ctx->work_len, L) && A(ctx, &ctx->clw, ctx->clw_len, L) &&
             A(ctx, &ctx->sc, 1, L);
   if (!ok) return fail(ctx, TT_ERR_OOM, "device allocation failed (base buffers)");
+  // chain-path view of the cores (and of the rank-2r block cores for the adaptive step)
+  ctx->ctt = ChainTT{};
+  ctx->ctt.d = d;
+  ctx->dtt = ChainTT{};
+  ctx->dtt.d = d;
+  for (int k = 0; k <= d; ++k) {
+    ctx->ctt.r[k] = (int)ctx->r[k];
+    ctx->ctt.off[k] = ctx->core_off[k];
+    ctx->ctt.phi_off[k] = ctx->phi_off[k];
+    ctx->dtt.r[k] = (k == 0 || k == d) ? 1 : 2 * (int)ctx->r[k];
+    ctx->dtt.off[k] = ctx->b_off[k];
+    ctx->dtt.phi_off[k] = ctx->phi_off[k];
+  }
+  for (int k = 0; k < d; ++k) ctx->ctt.n[k] = ctx->dtt.n[k] = (int)ctx->n[k];
+  if (ctx->plan.chain) {
+    if (cudaMallocHost(&ctx->sc_host, sizeof(Scalars)) != cudaSuccess)
+      return fail(ctx, TT_ERR_OOM, "pinned allocation failed");
+    std::memset(ctx->sc_host, 0, sizeof(Scalars));
+    CK(cudaMemcpyAsync(ctx->n_dev, ctx->n_i.data(), d * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemsetAsync(ctx->C, 0, ctx->core_off[d] * sizeof(double), ctx->stream));
+    CK(cudaMemsetAsync(ctx->sc, 0, sizeof(Scalars), ctx->stream));
+    CK(cudaMemsetAsync(ctx->h, 0, ctx->phi_off[d] * sizeof(double), ctx->stream));
+    dense_init();
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->base_ready = true;
+    return TT_OK;
+  }
   // tables
   ctx->LT.assign(KL + 1, nullptr);
   ctx->EL.assign(KL + 1, nullptr);
@@ -364,14 +362,9 @@ int ensure_base(tt_ctx* ctx) {
     if (!A(ctx, &ctx->RT[k], sz, L) || !A(ctx, &ctx->FR[k], sz, L))
       return fail(ctx, TT_ERR_OOM, "device allocation failed (right tables)");
   }
-  if (!A(ctx, &ctx->HL, ctx->plan.NL * ctx->plan.nbL, L) ||
-      !A(ctx, &ctx->HR, ctx->plan.NR * ctx->plan.nbR, L) ||
+  if (!A(ctx, &ctx->HL, ctx->plan.NL, L) || !A(ctx, &ctx->HR, ctx->plan.NR, L) ||
       !A(ctx, &ctx->psiL, ctx->plan.NL, L) || !A(ctx, &ctx->psiR, ctx->plan.NR, L) ||
-      !A(ctx, &ctx->margp, 32 * ctx->phi_off[d], L) ||
-      (ctx->plan.mid && (!A(ctx, &ctx->psiL1, ctx->plan.NL / ctx->n[KL - 1], L) ||
-                         !A(ctx, &ctx->psiR1, ctx->plan.NR / ctx->n[KL], L) ||
-                         !A(ctx, &ctx->TL1, ctx->NLk[KL - 1] * ctx->ldr[KL - 1], L) ||
-                         !A(ctx, &ctx->TR1, ctx->NRk[KL + 1] * ctx->ldr[KL + 1], L))))
+      !A(ctx, &ctx->margp, 32 * ctx->phi_off[d], L))
     return fail(ctx, TT_ERR_OOM, "device allocation failed (H / psi)");
   int64_t ycap = 1;
   for (int k = 0; k < d; ++k) {
@@ -393,7 +386,6 @@ int ensure_base(tt_ctx* ctx) {
   dense_init();
   tables_init();
   levels_init();
-  passes_mid_init();
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->base_ready = true;
   return TT_OK;
@@ -428,15 +420,27 @@ DenseArgs dense_args(tt_ctx* ctx) {
   return a;
 }
 
+// The adaptive denominator runs by chains on the chain path and when some 2 r_k exceeds the
+// table kernels' rank limit.
+bool adapt_by_chains(const tt_ctx* ctx) {
+  if (ctx->plan.chain) return true;
+  for (int k = 0; k <= ctx->d; ++k)
+    if (2 * ctx->r[k] > kMaxRank) return true;
+  return false;
+}
+
 // Buffers of the adaptive step (allocated once, before any graph capture).
 int ensure_adaptive(tt_ctx* ctx) {
   int rc = ensure_base(ctx);
   if (rc) return rc;
-  if (ctx->Dcore) return TT_OK;
+  if (ctx->Dcore || ctx->Dblk) return TT_OK;
   const int d = ctx->d, KL = ctx->plan.KL;
-  if (ctx->plan.mid) return fail(ctx, TT_ERR_STATE, "adaptive step not available with the middle-split passes");
-  for (int k = 0; k <= d; ++k)
-    if (2 * ctx->r[k] > kMaxRank) return fail(ctx, TT_ERR_RANK, "adaptive step needs 2 r_k <= 32");
+  if (adapt_by_chains(ctx)) {   // D evaluated by per-sample chains of the rank-2r tangent TT
+    if (!A(ctx, &ctx->Dblk, ctx->b_off[d], ctx->base_allocs) ||
+        !A(ctx, &ctx->dpart, adapt_vsum_parts(), ctx->base_allocs))
+      return fail(ctx, TT_ERR_OOM, "device allocation failed (adaptive step)");
+    return TT_OK;
+  }
   int64_t lenL = 1, lenR = 1;
   for (int k = 1; k < KL; ++k) lenL = std::max<int64_t>(lenL, ctx->NLk[k] * pad_rank(2 * (int)ctx->r[k]));
   for (int k = KL; k + 1 < d; ++k)
@@ -455,31 +459,28 @@ void grp(tt_ctx* ctx, int id, bool begin) {
 }
 
 // ------------------------------------------------------------------ enqueue pieces
-// Tables of the left / right parts.  With the middle-split passes the
-// step needs the left levels up to K_L (C) / K_L - 1 (U) and the right levels down to
-// K_L + 1, unscaled; `full` builds every level (queries of tt_eval_at use level K_L).
-void enqueue_tables(tt_ctx* ctx, bool useU, int64_t* lc, bool full = false) {
+// Tables of the left / right parts: left levels 1..K_L, right levels
+// d-1..K_L (the U tables scaled by psi at the split level).
+void enqueue_tables(tt_ctx* ctx, bool useU, int64_t* lc) {
   const int d = ctx->d, KL = ctx->plan.KL;
   cudaStream_t s = ctx->stream;
   const double* cores = useU ? ctx->U : ctx->C;
   const Scalars* sc = useU ? ctx->sc : nullptr;
-  const bool mid = ctx->plan.mid && !full;
-  const int lmax = mid && useU ? KL - 1 : KL;    // last left level built
-  const int rmin = mid ? KL + 1 : KL;            // last right level built
+  const int lmax = KL, rmin = KL;
   std::vector<TableLevel> L, R;
   bool ok = true;
   // left levels 1..lmax (A_{k+1} from A_k and core k), right levels d-1..rmin
   for (int k = 0; k < lmax; ++k) {
     TableLevel t{true, k == 0 ? nullptr : ctx->LT[k], ctx->ldr[k], cores + ctx->core_off[k],
                  (int)ctx->r[k], (int)ctx->n[k], (int)ctx->r[k + 1], ctx->LT[k + 1], ctx->ldr[k + 1],
-                 ctx->NLk[k + 1], (useU && !mid && k + 1 == KL) ? ctx->psiL : nullptr};
+                 ctx->NLk[k + 1], (useU && k + 1 == KL) ? ctx->psiL : nullptr};
     ok = ok && level_tab_ok(t.r0, t.nk, t.r1, t.ld_out);
     L.push_back(t);
   }
   for (int k = d - 1; k >= rmin; --k) {
     TableLevel t{false, k == d - 1 ? nullptr : ctx->RT[k + 1], ctx->ldr[k + 1],
                  cores + ctx->core_off[k], (int)ctx->r[k], (int)ctx->n[k], (int)ctx->r[k + 1],
-                 ctx->RT[k], ctx->ldr[k], ctx->NRk[k], (useU && !mid && k == KL) ? ctx->psiR : nullptr};
+                 ctx->RT[k], ctx->ldr[k], ctx->NRk[k], (useU && k == KL) ? ctx->psiR : nullptr};
     ok = ok && level_tab_ok(t.r0, t.nk, t.r1, t.ld_out);
     R.push_back(t);
   }
@@ -498,17 +499,24 @@ void enqueue_tables(tt_ctx* ctx, bool useU, int64_t* lc, bool full = false) {
 void enqueue_evaluate(tt_ctx* ctx, int64_t* lc, bool with_sumsq = true) {
   const int d = ctx->d, KL = ctx->plan.KL;
   cudaStream_t s = ctx->stream;
+  if (ctx->plan.chain) {   // pass A by per-sample chains (A1-A2), h by bucket pieces (A3)
+    if (ctx->obs_set && (ctx->m > 0 || ctx->allreduce)) {
+      grp(ctx, 1, true);
+      launch_chain_eval(s, 1, ctx->idx_dev, ctx->m, ctx->ctt, ctx->C, ctx->yobs, ctx->g, nullptr, nullptr, lc);
+      grp(ctx, 1, false);
+      grp(ctx, 3, true);
+      launch_chain_h(s, ctx->pcs, ctx->ctt, ctx->m, ctx->g, ctx->h, lc);
+      if (with_sumsq) launch_gather_sq_sum(s, ctx->h, ctx->n_i[0], ctx->sc, lc);
+      grp(ctx, 3, false);
+    }
+    return;
+  }
   grp(ctx, 0, true);
   enqueue_tables(ctx, false, lc);
   grp(ctx, 0, false);
   if (ctx->obs_set && (ctx->m > 0 || ctx->allreduce)) {
     grp(ctx, 1, true);
-    if (ctx->plan.mid) {
-      launch_mid_passA(s, ctx->offsL, ctx->Spre, ctx->ypre, ctx->g, ctx->HL, ctx->LT[KL],
-                       ctx->ldr[KL], ctx->C + ctx->core_off[KL], (int)ctx->r[KL], (int)ctx->n[KL],
-                       (int)ctx->r[KL + 1], ctx->RT[KL + 1], ctx->ldr[KL + 1], ctx->plan.NL,
-                       ctx->plan.NR / ctx->n[KL], nullptr, lc);
-    } else {
+    {
       SegArgs a{};
       a.plan = &ctx->planL;
       a.mode = kSDDMM;
@@ -534,9 +542,9 @@ void enqueue_evaluate(tt_ctx* ctx, int64_t* lc, bool with_sumsq = true) {
     launch_seg(s, b, nullptr, lc);
     grp(ctx, 2, false);
     grp(ctx, 3, true);
-    launch_marginals(s, ctx->HL, ctx->plan.NL * ctx->plan.nbL, KL, ctx->n_i.data(), true, ctx->h,
+    launch_marginals(s, ctx->HL, ctx->plan.NL, KL, ctx->n_i.data(), true, ctx->h,
                      ctx->margp, lc);
-    launch_marginals(s, ctx->HR, ctx->plan.NR * ctx->plan.nbR, d - KL, ctx->n_i.data() + KL, false,
+    launch_marginals(s, ctx->HR, ctx->plan.NR, d - KL, ctx->n_i.data() + KL, false,
                      ctx->h + ctx->phi_off[KL], ctx->margp + 32 * ctx->phi_off[KL], lc);
     if (with_sumsq) launch_gather_sq_sum(s, ctx->h, ctx->n_i[0], ctx->sc, lc);
     grp(ctx, 3, false);
@@ -555,6 +563,19 @@ void enqueue_adaptive_front(tt_ctx* ctx, int64_t* lc) {
   DenseArgs da = dense_args(ctx);
   grp(ctx, 11, true);
   launch_project(s, da, 1, lc);
+  if (adapt_by_chains(ctx)) {
+    // D = sum_k [Ttil_1..A_k..Ttil_d] as a rank-2r block TT, evaluated by per-sample chains
+    launch_tangent_cores(s, ctx->U, ctx->Ahat, ctx->phi, ctx->ctt, ctx->dtt, ctx->Dblk, ctx->sc, lc);
+    if (ctx->m > 0) {
+      launch_chain_eval(s, 2, ctx->idx_dev, ctx->m, ctx->dtt, ctx->Dblk, nullptr, ctx->dval, ctx->sc,
+                        nullptr, lc);
+      launch_adapt_den(s, ctx->dval, ctx->m, ctx->dpart, ctx->sc, lc);
+    } else {
+      cudaMemsetAsync(&ctx->sc->adapt_den, 0, sizeof(double), s);
+    }
+    grp(ctx, 11, false);
+    return;
+  }
   std::vector<int> ni(d), ri(d + 1);
   for (int k = 0; k < d; ++k) ni[k] = (int)ctx->n[k];
   for (int k = 0; k <= d; ++k) ri[k] = (int)ctx->r[k];
@@ -614,7 +635,7 @@ void enqueue_adaptive_front(tt_ctx* ctx, int64_t* lc) {
     a.coltab2 = ctx->FR[KL];    // RD (psi_R scaled)
     a.out = ctx->HL;
     launch_seg(s, a, ctx->sc, lc);
-    launch_adapt_den(s, ctx->HL, ctx->plan.NL * ctx->plan.nbL, ctx->dpart, ctx->sc, lc);
+    launch_adapt_den(s, ctx->HL, ctx->plan.NL, ctx->dpart, ctx->sc, lc);
   } else {
     cudaMemsetAsync(&ctx->sc->adapt_den, 0, sizeof(double), s);
   }
@@ -655,39 +676,28 @@ void enqueue_update(tt_ctx* ctx, int64_t* lc, int part = 0) {
   grp(ctx, 4, true);
   launch_weights(s, ctx->h, d, ctx->n_i.data(), ctx->phi_off[d], ctx->eps_rule, ctx->eps_fixed,
                  ctx->step_rule, ctx->phi, ctx->sc, lc);
-  launch_psi(s, ctx->phi, ctx->phi_off.data(), KL, d, ctx->n_i.data(), ctx->plan.NL,
-             ctx->plan.NR, ctx->psiL, ctx->psiR, ctx->psiL1, ctx->psiR1, ctx->sc, lc);
+  if (!ctx->plan.chain)
+    launch_psi(s, ctx->phi, ctx->phi_off.data(), KL, d, ctx->n_i.data(), ctx->plan.NL,
+               ctx->plan.NR, ctx->psiL, ctx->psiR, ctx->sc, lc);
   grp(ctx, 4, false);
   DenseArgs da = dense_args(ctx);
   grp(ctx, 5, true);
   launch_dense_orth(s, da, lc);
   grp(ctx, 5, false);
+  if (ctx->plan.chain) {   // pass B by per-sample chains (A7-A8), segmented contraction (A9)
+    grp(ctx, 7, true);
+    launch_chain_iface(s, ctx->idx_dev, ctx->m, ctx->ctt, ctx->U, ctx->phi, ctx->g, ctx->ghat, ctx->IL,
+                       ctx->IR, ctx->sc, lc);
+    grp(ctx, 7, false);
+    grp(ctx, 9, true);
+    launch_chain_contract(s, ctx->pcs, ctx->ctt, ctx->m, ctx->ghat, ctx->IL, ctx->IR, ctx->Y, ctx->sc, lc);
+    grp(ctx, 9, false);
+  } else {
   grp(ctx, 6, true);
   enqueue_tables(ctx, true, lc);
   grp(ctx, 6, false);
   grp(ctx, 7, true);
-  if (ctx->plan.mid) {
-    launch_scale_rows(s, ctx->RT[KL + 1], ctx->psiR1, ctx->NRk[KL + 1], ctx->ldr[KL + 1], ctx->TR1,
-                      ctx->sc, lc);
-    launch_scale_rows(s, ctx->LT[KL - 1], ctx->psiL1, ctx->NLk[KL - 1], ctx->ldr[KL - 1], ctx->TL1,
-                      ctx->sc, lc);
-    // E_KL[P] = psi_L[P] sum_j U_KL(:, j, :) Z[P][j], Z from the right U-table level KL+1
-    launch_mid_passB(s, true, ctx->offsL, ctx->Spre, ctx->g, ctx->TR1, (int)ctx->r[KL + 1],
-                     ctx->ldr[KL + 1], ctx->psiR1, ctx->phi + ctx->phi_off[KL], ctx->psiL,
-                     ctx->U + ctx->core_off[KL], (int)ctx->r[KL], (int)ctx->n[KL], (int)ctx->r[KL + 1],
-                     ctx->EL[KL], (int)ctx->r[KL], ctx->ldr[KL], ctx->plan.NL,
-                     ctx->plan.NR / ctx->n[KL], ctx->sc, lc);
-    grp(ctx, 7, false);
-    grp(ctx, 8, true);
-    // F_KL[S] = psi_R[S] sum_i Z'[S][i] U_{KL-1}(:, i, :), Z' from the left U-table level KL-1
-    launch_mid_passB(s, false, ctx->offsR, ctx->Psuf, ctx->g_suf, ctx->TL1,
-                     (int)ctx->r[KL - 1], ctx->ldr[KL - 1], ctx->psiL1,
-                     ctx->phi + ctx->phi_off[KL - 1], ctx->psiR, ctx->U + ctx->core_off[KL - 1],
-                     (int)ctx->r[KL - 1], (int)ctx->n[KL - 1], (int)ctx->r[KL], ctx->FR[KL],
-                     (int)ctx->r[KL], ctx->ldr[KL], ctx->plan.NR, ctx->plan.NL / ctx->n[KL - 1],
-                     ctx->sc, lc);
-    grp(ctx, 8, false);
-  } else {
+  {
   SegArgs a{};
   a.plan = &ctx->planL;
   a.mode = kSPMM;
@@ -762,6 +772,7 @@ void enqueue_update(tt_ctx* ctx, int64_t* lc, int part = 0) {
     }
   }
   grp(ctx, 9, false);
+  }   // table path
   if (part == 1) return;
   if (adaptive) {
     enqueue_adaptive_front(ctx, lc);
@@ -941,6 +952,113 @@ int make_plan(tt_ctx* ctx, const int64_t* offs_dev, int64_t nrow, int nblk, int 
   return TT_OK;
 }
 
+void apply_plan(tt_ctx* ctx, const Plan& pl) {
+  ctx->plan = pl;
+  ctx->NLk.assign(pl.KL + 1, 1);
+  ctx->NRk.assign(ctx->d + 1, 1);
+  if (pl.chain) return;
+  for (int k = 1; k <= pl.KL; ++k) ctx->NLk[k] = ctx->NLk[k - 1] * ctx->n[k - 1];
+  for (int k = ctx->d - 1; k >= pl.KL; --k) ctx->NRk[k] = ctx->NRk[k + 1] * ctx->n[k];
+}
+
+// Observations on the chain path: the multi-indices stay in the ABI layout,
+// the values in the original order; A0 builds the per-mode buckets (stable radix sort of the
+// sample ids by x_k, k = 0..d-1) and cuts them into pieces of <= P samples.
+int set_obs_chain(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals, int64_t m) {
+  const int d = ctx->d;
+  auto& OL = ctx->obs_allocs;
+  std::vector<void*> tmp;
+  auto cleanup = [&]() { dfree_all(ctx, tmp); };
+  ChainPieces& pc = ctx->pcs;
+  pc = ChainPieces();
+  int rmax = 1;
+  for (int k = 0; k <= d; ++k) rmax = std::max<int>(rmax, (int)ctx->r[k]);
+  pc.nbuckets = ctx->phi_off[d];
+  pc.stride = 1;
+  for (int k = 0; k < d; ++k) pc.stride = std::max<int>(pc.stride, (int)(ctx->r[k] * ctx->r[k + 1]));
+  pc.P = chain_piece_size(m, d, rmax);
+  int64_t iface = 0;                                  // interface doubles, m r_k for k = 1..d-1
+  ctx->ctt.m = m;
+  ctx->ctt.il_off[0] = ctx->ctt.il_off[1] = 0;
+  for (int k = 1; k < d; ++k) {
+    ctx->ctt.il_off[k] = iface;
+    iface += m * ctx->r[k];
+  }
+  ctx->ctt.il_off[d] = iface;
+  ctx->dtt.m = m;
+  uint64_t *keys = nullptr, *ktmp = nullptr;
+  uint32_t *vals = nullptr, *vtmp = nullptr;
+  int* hist = nullptr;
+  int* np = nullptr;
+  long long* bsum = nullptr;
+  const int64_t hl = radix_hist_len(m);
+  const int64_t noffs = pc.nbuckets + d;
+  bool ok = A(ctx, &ctx->idx_dev, m * d, OL) && A(ctx, &ctx->yobs, m, OL) && A(ctx, &ctx->g, m, OL) &&
+            A(ctx, &ctx->ghat, m, OL) && A(ctx, &ctx->IL, iface, OL) && A(ctx, &ctx->IR, iface, OL) &&
+            A(ctx, &pc.perm, (int64_t)d * m, OL) && A(ctx, &pc.offs, noffs, OL) &&
+            A(ctx, &pc.pbase, pc.nbuckets + 1, OL) && (!adapt_by_chains(ctx) || A(ctx, &ctx->dval, m, OL)) &&
+            A(ctx, &keys, m, tmp) && A(ctx, &ktmp, m, tmp) && A(ctx, &vals, m, tmp) &&
+            A(ctx, &vtmp, m, tmp) && A(ctx, &hist, hl, tmp) && A(ctx, &np, pc.nbuckets, tmp) &&
+            A(ctx, &bsum, plan_scan_scratch(pc.nbuckets), tmp);
+  if (!ok) {
+    cleanup();
+    dfree_all(ctx, OL);
+    return fail(ctx, TT_ERR_OOM, "device allocation failed (observations, chain path)");
+  }
+  cudaStream_t s = ctx->stream;
+  int64_t lc = 0;
+  CK(cudaMemsetAsync(&ctx->sc->index_err, 0, sizeof(int), s));
+  if (m > 0) {
+    CK(cudaMemcpyAsync(ctx->idx_dev, h_idx, (size_t)m * d * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->yobs, h_vals, (size_t)m * sizeof(double), cudaMemcpyHostToDevice, s));
+    for (int k = 0; k < d; ++k) {
+      int bits = 1;
+      while (((int64_t)1 << bits) < ctx->n[k]) ++bits;
+      launch_mode_keys(s, ctx->idx_dev, m, d, k, (int)ctx->n[k], keys, vals, &ctx->sc->index_err, &lc);
+      uint64_t* ko;
+      uint32_t* vo;
+      radix_sort_pairs(s, keys, vals, ktmp, vtmp, m, bits, hist, hl, &ko, &vo, &lc);
+      launch_mode_after_sort(s, ko, vo, m, ctx->n[k], pc.perm + (int64_t)k * m,
+                             pc.offs + ctx->phi_off[k] + k, &lc);
+    }
+  } else {
+    CK(cudaMemsetAsync(pc.offs, 0, noffs * sizeof(int64_t), s));
+  }
+  launch_piece_count(s, pc.offs, ctx->ctt, pc.nbuckets, pc.P, np, &lc);
+  launch_scan_i32(s, np, pc.nbuckets, pc.pbase, bsum, &lc);
+  CK(cudaMemcpyAsync(&pc.npieces, pc.pbase + pc.nbuckets, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (ctx->sc_host->index_err) {
+    cleanup();
+    dfree_all(ctx, OL);
+    return fail(ctx, TT_ERR_INDEX, "an observed index is outside [0, n_k)");
+  }
+  if (!A(ctx, &pc.pieces, std::max<int64_t>(pc.npieces, 1), OL) ||
+      !A(ctx, &pc.part, std::max<int64_t>(pc.npieces, 1) * pc.stride, OL)) {
+    cleanup();
+    dfree_all(ctx, OL);
+    return fail(ctx, TT_ERR_OOM, "device allocation failed (bucket pieces)");
+  }
+  launch_piece_fill(s, pc.offs, pc.pbase, pc.nbuckets, ctx->ctt, pc.P, pc.pieces, &lc);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(ctx, e, "bucketing kernels (chain path)");
+  }
+  CK(cudaStreamSynchronize(s));
+  cleanup();
+  ctx->launches += lc;
+  ctx->m = m;
+  double nstar = 1.0;
+  for (int k = 0; k < d; ++k) nstar *= (double)ctx->n[k];
+  ctx->p = (double)(ctx->allreduce ? ctx->m_global : m) / nstar;
+  CK(cudaMemcpyAsync(&ctx->sc->p, &ctx->p, sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  ctx->obs_set = true;
+  return TT_OK;
+}
+
 bool all_cores_set(tt_ctx* ctx) {
   for (char c : ctx->core_set)
     if (!c) return false;
@@ -963,6 +1081,26 @@ int tt_plan(int d, const int64_t* n, const int64_t* r, int* K_L, int64_t* N_L, i
   return TT_OK;
 }
 
+int tt_set_path(tt_ctx* ctx, int path) {
+  if (!ctx) return TT_ERR_ARG;
+  if (path < TT_PATH_AUTO || path > TT_PATH_CHAINS) return fail(ctx, TT_ERR_ARG, "unknown path");
+  if (ctx->base_ready || ctx->obs_set)
+    return fail(ctx, TT_ERR_STATE, "tt_set_path must precede any core or observation");
+  Plan pl;
+  std::string msg;
+  int rc = validate_and_plan(ctx->d, ctx->n.data(), ctx->r.data(), &pl, &msg, path);
+  if (rc != TT_OK) return fail(ctx, rc, msg);
+  ctx->path_req = path;
+  apply_plan(ctx, pl);
+  return TT_OK;
+}
+
+int tt_get_path(tt_ctx* ctx, int* path) {
+  if (!ctx || !path) return TT_ERR_ARG;
+  *path = ctx->plan.chain ? TT_PATH_CHAINS : TT_PATH_TABLES;
+  return TT_OK;
+}
+
 int tt_set_allreduce(tt_ctx* ctx, tt_allreduce_fn fn, void* user, int64_t m_global) {
   if (!ctx) return TT_ERR_ARG;
   if (fn && m_global < 0) return fail(ctx, TT_ERR_ARG, "m_global must be >= 0");
@@ -972,17 +1110,6 @@ int tt_set_allreduce(tt_ctx* ctx, tt_allreduce_fn fn, void* user, int64_t m_glob
   ctx->m_global = fn ? m_global : -1;
   drop_graphs(ctx);
   ctx->evalValid = false;
-  return TT_OK;
-}
-
-int tt_plan_layout(int d, const int64_t* n, const int64_t* r, int* nb_L, int* nb_R, int* middle) {
-  Plan pl;
-  std::string msg;
-  int rc = validate_and_plan(d, n, r, &pl, &msg);
-  if (rc != TT_OK) return rc;
-  if (nb_L) *nb_L = pl.nbL;
-  if (nb_R) *nb_R = pl.nbR;
-  if (middle) *middle = pl.mid ? 1 : 0;
   return TT_OK;
 }
 
@@ -1011,11 +1138,7 @@ int tt_create(int d, const int64_t* n, const int64_t* r, tt_ctx** out) {
   for (int k = 0; k < d; ++k) ctx->n_i[k] = (int)n[k];
   ctx->ldr.resize(d + 1);
   for (int k = 0; k <= d; ++k) ctx->ldr[k] = pad_rank((int)r[k]);
-  ctx->plan = pl;
-  ctx->NLk.assign(pl.KL + 1, 1);
-  for (int k = 1; k <= pl.KL; ++k) ctx->NLk[k] = ctx->NLk[k - 1] * n[k - 1];
-  ctx->NRk.assign(d + 1, 1);
-  for (int k = d - 1; k >= pl.KL; --k) ctx->NRk[k] = ctx->NRk[k + 1] * n[k];
+  apply_plan(ctx, pl);
   ctx->core_set.assign(d, 0);
   if (cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete ctx;
@@ -1122,10 +1245,11 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
   ctx->obs_set = false;
   ctx->evalValid = false;
   ctx->m = 0;
+  ctx->idx_dev = nullptr;
+  if (ctx->plan.chain) return set_obs_chain(ctx, h_idx, h_vals, m);
   const int d = ctx->d, KL = ctx->plan.KL;
   const int64_t NL = ctx->plan.NL, NR = ctx->plan.NR;
-  const int nbL = ctx->plan.nbL, nbR = ctx->plan.nbR;
-  const int64_t NLv = NL * nbL, NRv = NR * nbR;   // virtual rows (gather block, row)
+  const int64_t NLv = NL, NRv = NR;
   auto& OL = ctx->obs_allocs;
   std::vector<void*> tmp;
   int32_t* idx_dev = nullptr;
@@ -1135,14 +1259,16 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
   int32_t* inv = nullptr;
   int* hist = nullptr;
   const int64_t hl = radix_hist_len(m);
-  bool ok = A(ctx, &idx_dev, m * d, tmp) && A(ctx, &y_orig, m, tmp) && A(ctx, &kpre, m, tmp) &&
+  bool ok = A(ctx, &idx_dev, m * d, OL) && A(ctx, &y_orig, m, tmp) && A(ctx, &kpre, m, tmp) &&
             A(ctx, &ksuf, m, tmp) && A(ctx, &ktmp, m, tmp) && A(ctx, &vals, m, tmp) &&
             A(ctx, &vals2, m, tmp) && A(ctx, &vtmp, m, tmp) && A(ctx, &inv, m, tmp) &&
             A(ctx, &hist, hl, tmp) && A(ctx, &ctx->Spre, m + 8, OL) && A(ctx, &ctx->ypre, m + 8, OL) &&
             A(ctx, &ctx->g, m + 8, OL) && A(ctx, &ctx->sid_pre, m, OL) && A(ctx, &ctx->pos_suf, m, OL) &&
             A(ctx, &ctx->Psuf, m + 8, OL) && A(ctx, &ctx->sid_suf, m, OL) &&
             A(ctx, &ctx->g_suf, m + 8, OL) && A(ctx, &ctx->pre2suf, m, OL) &&
-            A(ctx, &ctx->offsL, NLv + 1 + 40, OL) && A(ctx, &ctx->offsR, NRv + 1 + 40, OL);
+            A(ctx, &ctx->offsL, NLv + 1 + 40, OL) && A(ctx, &ctx->offsR, NRv + 1 + 40, OL) &&
+            (!adapt_by_chains(ctx) || A(ctx, &ctx->dval, m, OL));
+  ctx->idx_dev = idx_dev;
   auto cleanup = [&]() { dfree_all(ctx, tmp); };
   if (!ok) {
     cleanup();
@@ -1155,11 +1281,6 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
   while (((int64_t)1 << bitsS) < NR) ++bitsS;
   while (((int64_t)1 << bitsVP) < NLv) ++bitsVP;
   while (((int64_t)1 << bitsVS) < NRv) ++bitsVS;
-  if (ctx->plan.mid) {   // in-row keys (digit << shift) | rest (sort.cu) need shift + digit bits
-    auto bits = [](int64_t v) { int b = 0; while (((int64_t)1 << b) < v) ++b; return b; };
-    bitsS = std::max(bitsS, bits(NR / ctx->n[KL]) + bits(ctx->n[KL]));
-    bitsP = std::max(bitsP, bits(NL / ctx->n[KL - 1]) + bits(ctx->n[KL - 1]));
-  }
   cudaStream_t s = ctx->stream;
   int64_t lc = 0;
   if (m > 0) {
@@ -1176,9 +1297,7 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
     CK(cudaMemcpyAsync(y_orig, h_vals, (size_t)m * sizeof(double), cudaMemcpyHostToDevice, ctx->side));
     CK(cudaEventRecord(ctx->ev_side[1], ctx->side));
     CK(cudaMemsetAsync(&ctx->sc->index_err, 0, sizeof(int), s));
-    launch_make_keys(s, idx_dev, m, d, ctx->n_dev, KL, bitsP, bitsS, NL, NR, nbL, nbR,
-                     ctx->plan.mid ? (int)ctx->n[KL - 1] : 1, ctx->plan.mid ? (int)ctx->n[KL] : 1,
-                     kpre, ksuf, vals, ctx->sc, &lc);
+    launch_make_keys(s, idx_dev, m, d, ctx->n_dev, KL, bitsP, bitsS, kpre, ksuf, vals, ctx->sc, &lc);
     CK(cudaMemcpyAsync(vals2, vals, (size_t)m * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(Scalars), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -1212,9 +1331,9 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
   }
   cleanup();
   ptm.mark("free_tmp");
-  if ((rc = make_plan(ctx, ctx->offsL, NL, nbL, ctx->ldr[KL], m, &ctx->planL))) return rc;
+  if ((rc = make_plan(ctx, ctx->offsL, NL, 1, ctx->ldr[KL], m, &ctx->planL))) return rc;
   ptm.mark("plan_L");
-  if ((rc = make_plan(ctx, ctx->offsR, NR, nbR, ctx->ldr[KL], m, &ctx->planR))) return rc;
+  if ((rc = make_plan(ctx, ctx->offsR, NR, 1, ctx->ldr[KL], m, &ctx->planR))) return rc;
   ptm.mark("plan_R");
   ctx->m = m;
   double nstar = 1.0;
@@ -1230,7 +1349,7 @@ int tt_spectral_init(tt_ctx* ctx) {
   if (!ctx) return TT_ERR_ARG;
   if (!ctx->obs_set || ctx->m <= 0) return fail(ctx, TT_ERR_STATE, "spectral init needs a nonempty Omega");
   if (ctx->allreduce) return fail(ctx, TT_ERR_STATE, "spectral init is single-rank (sharded mode set)");
-  if (ctx->plan.mid) return fail(ctx, TT_ERR_STATE, "spectral init not available with the middle-split layout");
+  if (ctx->plan.chain) return fail(ctx, TT_ERR_STATE, "spectral init needs the table path (TT_PATH_TABLES)");
   const int d = ctx->d;
   long double nstar = 1;
   int Wmax = 1, cs = 1;
@@ -1260,7 +1379,7 @@ int tt_spectral_init(tt_ctx* ctx) {
   }
   a.m = m;
   a.NL = ctx->plan.NL;
-  a.nrows = ctx->plan.NL * ctx->plan.nbL;
+  a.nrows = ctx->plan.NL;
   a.p = ctx->p;
   a.offsL = ctx->offsL;
   a.Spre = ctx->Spre;
@@ -1325,7 +1444,7 @@ int tt_prgd_step(tt_ctx* ctx, double step_size) {
     ++ctx->prof_steps;
   }
   ctx->evalValid = true;
-  ctx->tablesC = !ctx->plan.mid;
+  ctx->tablesC = !ctx->plan.chain;
   ++ctx->steps;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(ctx, e, "step");
@@ -1340,8 +1459,8 @@ int tt_eval_at(tt_ctx* ctx, const int32_t* h_idx, int64_t count, double* h_out) 
   int rc = ensure_base(ctx);
   if (rc) return rc;
   int64_t lc = 0;
-  if (!ctx->tablesC) {
-    enqueue_tables(ctx, false, &lc, true);
+  if (!ctx->plan.chain && !ctx->tablesC) {
+    enqueue_tables(ctx, false, &lc);
     ctx->tablesC = true;
   }
   std::vector<void*> tmp;
@@ -1355,8 +1474,11 @@ int tt_eval_at(tt_ctx* ctx, const int32_t* h_idx, int64_t count, double* h_out) 
   CK(cudaMemsetAsync(&ctx->sc->index_err, 0, sizeof(int), s));
   CK(cudaMemcpyAsync(qidx, h_idx, (size_t)count * ctx->d * sizeof(int32_t), cudaMemcpyHostToDevice, s));
   const int KL = ctx->plan.KL;
-  launch_eval_queries(s, qidx, count, ctx->d, ctx->n_i.data(), KL, ctx->LT[KL], ctx->RT[KL],
-                      ctx->ldr[KL], (int)ctx->r[KL], qout, ctx->sc, &lc);
+  if (ctx->plan.chain)
+    launch_chain_eval(s, 0, qidx, count, ctx->ctt, ctx->C, nullptr, qout, nullptr, &ctx->sc->index_err, &lc);
+  else
+    launch_eval_queries(s, qidx, count, ctx->d, ctx->n_i.data(), KL, ctx->LT[KL], ctx->RT[KL],
+                        ctx->ldr[KL], (int)ctx->r[KL], qout, ctx->sc, &lc);
   ctx->launches += lc;
   CK(cudaMemcpyAsync(h_out, qout, (size_t)count * sizeof(double), cudaMemcpyDeviceToHost, s));
   rc = read_scalars(ctx);
@@ -1376,7 +1498,7 @@ int tt_residual_norm(tt_ctx* ctx, double* out) {
   if (!ctx->evalValid) {
     if ((rc = run_evaluate(ctx))) return rc;
     ctx->evalValid = true;
-    ctx->tablesC = !ctx->plan.mid;
+    ctx->tablesC = !ctx->plan.chain;
   }
   if ((rc = read_scalars(ctx))) return rc;
   *out = std::sqrt(ctx->sc_host->sumsq);
@@ -1444,10 +1566,34 @@ int tt_debug_get(tt_ctx* ctx, int what, int k, void* h_out, int64_t cap, int64_t
   int64_t cnt = 0;
   size_t esz = sizeof(double);
   switch (what) {
+    case TT_DBG_PERM_PRE:
+    case TT_DBG_PERM_SUF:
+    case TT_DBG_OFFS_L:
+    case TT_DBG_OFFS_R:
+      if (ctx->plan.chain) return fail(ctx, TT_ERR_STATE, "prefix / suffix buckets exist on the table path");
+      break;
+    default:
+      break;
+  }
+  switch (what) {
     case TT_DBG_PERM_PRE: src = ctx->sid_pre; cnt = ctx->m; esz = 4; break;
     case TT_DBG_PERM_SUF: src = ctx->sid_suf; cnt = ctx->m; esz = 4; break;
-    case TT_DBG_OFFS_L: src = ctx->offsL; cnt = ctx->obs_set ? ctx->plan.NL * ctx->plan.nbL + 1 : 0; esz = 8; break;
-    case TT_DBG_OFFS_R: src = ctx->offsR; cnt = ctx->obs_set ? ctx->plan.NR * ctx->plan.nbR + 1 : 0; esz = 8; break;
+    case TT_DBG_OFFS_L: src = ctx->offsL; cnt = ctx->obs_set ? ctx->plan.NL + 1 : 0; esz = 8; break;
+    case TT_DBG_OFFS_R: src = ctx->offsR; cnt = ctx->obs_set ? ctx->plan.NR + 1 : 0; esz = 8; break;
+    case TT_DBG_PERM_MODE:
+    case TT_DBG_OFFS_MODE:
+      if (!need_k()) return fail(ctx, TT_ERR_ARG, "bad k");
+      if (!ctx->plan.chain) return fail(ctx, TT_ERR_STATE, "per-mode buckets exist on the chain path");
+      if (what == TT_DBG_PERM_MODE) {
+        src = ctx->pcs.perm + (int64_t)k * ctx->m;
+        cnt = ctx->obs_set ? ctx->m : 0;
+        esz = 4;
+      } else {
+        src = ctx->pcs.offs + ctx->phi_off[k] + k;
+        cnt = ctx->obs_set ? ctx->n[k] + 1 : 0;
+        esz = 8;
+      }
+      break;
     case TT_DBG_H:
     case TT_DBG_PHI:
       if (!need_k()) return fail(ctx, TT_ERR_ARG, "bad k");
@@ -1488,10 +1634,17 @@ int tt_debug_get(tt_ctx* ctx, int what, int k, void* h_out, int64_t cap, int64_t
       if (!ctx->evalValid && ctx->m > 0) {
         if ((rc = run_evaluate(ctx))) return rc;
         ctx->evalValid = true;
-        ctx->tablesC = !ctx->plan.mid;
+        ctx->tablesC = !ctx->plan.chain;
       }
       std::vector<double> gp(ctx->m);
       std::vector<int32_t> sp(ctx->m);
+      if (ctx->plan.chain) {   // original sample order already
+        if (ctx->m > 0)
+          CK(cudaMemcpyAsync(h_out, ctx->g, ctx->m * sizeof(double), cudaMemcpyDeviceToHost, s));
+        if ((rc = read_scalars(ctx))) return rc;
+        *count = ctx->m;
+        return TT_OK;
+      }
       if (ctx->m > 0) {
         CK(cudaMemcpyAsync(gp.data(), ctx->g, ctx->m * sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(sp.data(), ctx->sid_pre, ctx->m * sizeof(int32_t), cudaMemcpyDeviceToHost, s));

@@ -1,15 +1,17 @@
 // dense.cu — the small dense work of one PRGD iteration.
 //
-//   k_dense_orth   (1 CTA)  A4 That = W^{1/2} T (Prop. 3.1),
-//                  A5 left-orthogonal U by a Householder QR sweep,
-//                  A6 right Grams P_k = That^{>=k+1} That^{>=k+1 T} and their Cholesky
-//                  factors.
+//   k_orth_cs      (one 8-CTA thread-block cluster, round_cs.inc) A4 That = W^{1/2} T
+//                  (Prop. 3.1), A5 left-orthogonal U by distributed
+//                  CholeskyQR, A6 right Grams P_k = That^{>=k+1}
+//                  That^{>=k+1 T} and their Cholesky factors.
 //   k_project      (d CTAs, one per core, independent) A10 closed-form projection
 //                  (PAPER.md:356-360), A11 unweighting and A13 the
 //                  rank-2r cores B_k of W_l = T_l - alpha grad.
-//   k_dense_round  (1 CTA)  A14 TT-rounding = Alg. 1 on W_l:
-//                  right-to-left Householder QR, then left-to-right QR + one-sided
-//                  Jacobi SVD keeping the top r_k left singular vectors.
+//   k_round_cs     (one 8-CTA cluster, round_cs.inc) A14 TT-rounding = Alg. 1 on W_l
+//                  (PAPER.md:114-131): right-to-left CholeskyQR, then left-to-right
+//                  CholeskyQR + truncation of the small R factor by one-sided Jacobi.
+//   k_dense_orth / k_dense_round (1 CTA, Householder below) are the fallbacks for bonds the
+//                  cluster kernels do not take (2 r > 32) and for rank-deficient unfoldings.
 //
 // Householder QR (LAPACK dgeqr2 / dorg2r conventions: beta = -sign(alpha)||x||,
 // tau = (beta - alpha)/beta, v_j = 1, tau = 0 for a zero sub-column) with rows owned

@@ -381,39 +381,9 @@ struct PsiArgs {
 };
 
 __global__ void k_psi(const double* __restrict__ phi, PsiArgs pa, double* __restrict__ psiL,
-                      double* __restrict__ psiR, double* __restrict__ psiL1,
-                      double* __restrict__ psiR1, const Scalars* sc) {
+                      double* __restrict__ psiR, const Scalars* sc) {
   if (sc && sc->noop) return;
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  // middle-split weights: psiL1[P'] = prod_{k < KL-1} phi^{-1}, psiR1[S'] = prod_{k > KL} phi^{-1}
-  const int64_t NL1 = psiL1 ? pa.NL / pa.n[pa.KL - 1] : 0;
-  const int64_t NR1 = psiR1 ? pa.NR / pa.n[pa.KL] : 0;
-  if (e >= pa.NL + pa.NR) {
-    int64_t f = e - pa.NL - pa.NR;
-    if (f < NL1) {
-      int64_t P = f;
-      double v = 1.0;
-      for (int k = pa.KL - 2; k >= 0; --k) {
-        int64_t q = P / pa.n[k];
-        int xk = (int)(P - q * pa.n[k]);
-        P = q;
-        v /= phi[pa.phi_off[k] + xk];
-      }
-      psiL1[f] = v;
-    } else if (f < NL1 + NR1) {
-      int64_t S = f - NL1;
-      const int64_t S0 = S;
-      double v = 1.0;
-      for (int k = pa.KL + 1; k < pa.d; ++k) {
-        int64_t q = S / pa.n[k];
-        int xk = (int)(S - q * pa.n[k]);
-        S = q;
-        v /= phi[pa.phi_off[k] + xk];
-      }
-      psiR1[S0] = v;
-    }
-    return;
-  }
   if (e < pa.NL) {
     int64_t P = e;
     double v = 1.0;
@@ -602,7 +572,7 @@ void launch_weights(cudaStream_t s, const double* h, int d, const int* n_host, i
 
 void launch_psi(cudaStream_t s, const double* phi, const int64_t* phi_off_host, int KL, int d,
                 const int* n_host, int64_t NL, int64_t NR, double* psiL, double* psiR,
-                double* psiL1, double* psiR1, const Scalars* sc, int64_t* launches) {
+                const Scalars* sc, int64_t* launches) {
   PsiArgs pa;
   pa.d = d;
   pa.KL = KL;
@@ -612,8 +582,7 @@ void launch_psi(cudaStream_t s, const double* phi, const int64_t* phi_off_host, 
   }
   pa.NL = NL;
   pa.NR = NR;
-  const int64_t extra = (psiL1 ? NL / n_host[KL - 1] : 0) + (psiR1 ? NR / n_host[KL] : 0);
-  k_psi<<<blocks_for(NL + NR + extra, 256), 256, 0, s>>>(phi, pa, psiL, psiR, psiL1, psiR1, sc);
+  k_psi<<<blocks_for(NL + NR, 256), 256, 0, s>>>(phi, pa, psiL, psiR, sc);
   ++*launches;
 }
 

@@ -90,8 +90,7 @@ struct DenseArgs {
 // ------------------------------------------------------------------ kernels (launchers)
 // sort.cu
 void launch_make_keys(cudaStream_t s, const int32_t* idx, int64_t m, int d, const int* n_dev,
-                      int KL, int bitsP, int bitsS, int64_t NL, int64_t NR, int nbL, int nbR,
-                      int nsubL, int nsubR, uint64_t* kpre, uint64_t* ksuf, uint32_t* vals,
+                      int KL, int bitsP, int bitsS, uint64_t* kpre, uint64_t* ksuf, uint32_t* vals,
                       Scalars* sc, int64_t* launches);
 void radix_sort_pairs(cudaStream_t s, uint64_t* keys, uint32_t* vals, uint64_t* keys_tmp,
                       uint32_t* vals_tmp, int64_t m, int bits, int* hist_buf, int64_t hist_len,
@@ -152,19 +151,6 @@ void launch_back_level(cudaStream_t s, bool left, const double* X, int ldX, cons
                        int64_t ngroups, double* Y, double* partial, int64_t partial_cap,
                        const Scalars* sc, int64_t* launches);  // shared-memory attributes (call once, outside capture)
 
-// DMMA table / backward kernels (tables.cu), used when tab_mma_ok / back_mma_ok hold.
-bool tab_mma_ok(int r0, int nk, int r1, int ld_out);
-void launch_tab_mma(cudaStream_t s, bool left, const double* in, int ld_in, const double* core,
-                    int r0, int nk, int r1, double* out, int ld_out, int64_t rows_out,
-                    const double* rowscale, const Scalars* sc, int64_t* launches);
-bool back_mma_ok(int r0, int nk, int r1, int wrow);
-int64_t back_mma_partial_need(int64_t ngroups, int r0, int nk, int r1, int wrow);
-void launch_back_mma(cudaStream_t s, bool left, const double* X, int wrow, const double* V, int ldV,
-                     const double* core, int r0, int nk, int r1, double* O, int ldO,
-                     int64_t ngroups, double* Y, double* partial, int64_t partial_cap,
-                     const Scalars* sc, int64_t* launches);
-void tables_mma_init();
-
 // levels.cu: table levels / backward recursions on DMMA with few launches.
 struct TableLevel {        // out (flat [rows_out / nk][nk * ld_out]) from in x core
   bool left;
@@ -200,20 +186,6 @@ void launch_backward_levels(cudaStream_t s, const std::vector<BackwardLevel>& le
                             const Scalars* sc, int64_t* lc);
 void levels_init();
 
-// passes_mid.cu: passes re-associated through the middle cores (plan.mid).
-void launch_mid_passA(cudaStream_t s, const int64_t* offs, const int32_t* key, const double* y,
-                      double* g, double* H, const double* A, int lda, const double* core, int rK,
-                      int nK, int rK1, const double* Bt, int ldb, int64_t N, int64_t N1,
-                      const Scalars* sc, int64_t* launches);
-void launch_mid_passB(cudaStream_t s, bool left, const int64_t* offs, const int32_t* key,
-                      const double* x, const double* T, int rt, int ldt, const double* wr,
-                      const double* phij, const double* rowscale, const double* core, int r0,
-                      int nmid, int r1, double* out, int rout, int ldo, int64_t N, int64_t N1,
-                      const Scalars* sc, int64_t* launches);
-void launch_scale_rows(cudaStream_t s, const double* in, const double* f, int64_t rows, int ld,
-                       double* out, const Scalars* sc, int64_t* launches);
-void passes_mid_init();
-
 // passes.cu
 enum SegMode { kSDDMM = 0, kGSQ = 1, kSPMM = 2, kDPASS = 3 };
 struct SegArgs {
@@ -241,10 +213,9 @@ void launch_marginals(cudaStream_t s, const double* H, int64_t N, int nmodes, co
 void launch_weights(cudaStream_t s, const double* h, int d, const int* n_host, int64_t nsum,
                     int eps_rule, double eps_fixed, int step_rule, double* phi, Scalars* sc,
                     int64_t* launches);
-// psiL1 / psiR1 (middle-split weights over N_L / n_{KL-1} and N_R / n_KL rows) may be null.
 void launch_psi(cudaStream_t s, const double* phi, const int64_t* phi_off_host, int KL, int d,
                 const int* n_host, int64_t NL, int64_t NR, double* psiL, double* psiR,
-                double* psiL1, double* psiR1, const Scalars* sc, int64_t* launches);
+                const Scalars* sc, int64_t* launches);
 void launch_eval_queries(cudaStream_t s, const int32_t* idx, int64_t count, int d, const int* n_host,
                          int KL, const double* tabL, const double* tabR, int ld, int rb,
                          double* out, Scalars* sc, int64_t* launches);
@@ -265,7 +236,7 @@ struct SpectralArgs {
   int n[kMaxD];
   int r[kMaxD + 1];
   int64_t core_off[kMaxD + 1];
-  int64_t m, NL, nrows;       // nrows = NL * nb_L (virtual prefix rows)
+  int64_t m, NL, nrows;       // nrows = NL (prefix buckets)
   double p;
   const int64_t* offsL;       // [nrows + 1]
   const int32_t* Spre;        // [m] suffix index per prefix position
@@ -288,6 +259,52 @@ struct SpectralArgs {
   double *G, *V;              // W_max^2 each
 };
 int spectral_init_run(cudaStream_t s, const SpectralArgs& a, std::string* msg, int64_t* launches);
+
+// chains.cu: the per-sample chain path.
+struct ChainTT {             // a TT read by the chain kernels; cores in the ABI layout [r][n][r']
+  int d;
+  int64_t m;                 // samples (interface buffers)
+  int n[kMaxD];
+  int r[kMaxD + 1];
+  int64_t off[kMaxD + 1];      // core offsets
+  int64_t phi_off[kMaxD + 1];  // offsets of the per-mode slice arrays (phi, h; bucket index base)
+  int64_t il_off[kMaxD + 1];   // offsets of the interface arrays IL_k / IR_k (k = 1..d-1), m r_k each
+};
+struct ChainPieces {         // the per-mode buckets (A0) cut into pieces of <= P samples
+  int32_t* perm = nullptr;   // [d][m] sample ids, bucket-sorted per mode (stable)
+  int64_t* offs = nullptr;   // per-mode offsets concatenated: mode k at phi_off[k] + k, n_k + 1 each
+  int4* pieces = nullptr;    // {bucket e, mode k, t0, t1}
+  int64_t npieces = 0;
+  int64_t* pbase = nullptr;  // [nbuckets + 1] first piece of each bucket
+  int64_t nbuckets = 0;      // sum n_k
+  double* part = nullptr;    // [npieces * stride] piece partial sums
+  int stride = 1;            // max r_k r_{k+1}
+  int P = 256;
+};
+int chain_piece_size(int64_t m, int d, int rmax);
+// mode 0: out = T(x); 1: out = T(x) - y (pass A); 2: out = T(x)^2 (adaptive denominator, noop-aware)
+void launch_chain_eval(cudaStream_t s, int mode, const int32_t* idx, int64_t m, const ChainTT& tt,
+                       const double* cores, const double* y, double* out, const Scalars* sc,
+                       int* index_err, int64_t* launches);
+void launch_chain_iface(cudaStream_t s, const int32_t* idx, int64_t m, const ChainTT& tt, const double* U,
+                        const double* phi, const double* g, double* ghat, double* IL, double* IR,
+                        const Scalars* sc, int64_t* launches);
+void launch_chain_h(cudaStream_t s, const ChainPieces& pc, const ChainTT& tt, int64_t m, const double* g,
+                    double* h, int64_t* launches);
+void launch_chain_contract(cudaStream_t s, const ChainPieces& pc, const ChainTT& tt, int64_t m,
+                           const double* ghat, const double* IL, const double* IR, double* Y,
+                           const Scalars* sc, int64_t* launches);
+void launch_mode_keys(cudaStream_t s, const int32_t* idx, int64_t m, int d, int k, int nk, uint64_t* keys,
+                      uint32_t* vals, int* index_err, int64_t* launches);
+void launch_mode_after_sort(cudaStream_t s, const uint64_t* keys, const uint32_t* vals, int64_t m, int64_t nk,
+                            int32_t* perm, int64_t* offs, int64_t* launches);
+void launch_piece_count(cudaStream_t s, const int64_t* offs_cat, const ChainTT& tt, int64_t nb, int P,
+                        int* np, int64_t* launches);
+void launch_piece_fill(cudaStream_t s, const int64_t* offs_cat, const int64_t* pbase, int64_t nb,
+                       const ChainTT& tt, int P, int4* pieces, int64_t* launches);
+void launch_tangent_cores(cudaStream_t s, const double* U, const double* Ahat, const double* phi,
+                          const ChainTT& tt, const ChainTT& bt, double* out, const Scalars* sc,
+                          int64_t* launches);
 
 // adaptive.cu: the adaptive (steepest) step
 void launch_stack_cores(cudaStream_t s, int d, const int* n, const int* r, const int64_t* core_off,

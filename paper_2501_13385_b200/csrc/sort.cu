@@ -2,12 +2,10 @@
 //
 // Each sample s gets a prefix index P(s) (mixed radix of x_0..x_{KL-1}, x_0 most
 // significant) and a suffix index S(s) (mixed radix of x_KL..x_{d-1}, x_{d-1} most
-// significant).  The prefix order groups samples by the virtual row
-// VP = floor(S nbL / N_R) N_L + P (gather block of S first, so that a pass over it gathers
-// right-table rows from one L2-resident block at a time), the suffix order by
-// VS = floor(P nbR / N_L) N_R + S.  Prefix order = stable sort by key (VP << bitsS) | S,
-// suffix order = stable sort by (VS << bitsP) | P: an LSD radix sort whose passes are stable
-// counting sorts of 8-bit digits (histogram -> exclusive scan -> stable scatter).
+// significant).  Prefix order = stable sort by key (P << bitsS) | S, suffix order = stable
+// sort by (S << bitsP) | P: an LSD radix sort whose passes are stable counting sorts of 8-bit
+// digits (histogram -> exclusive scan -> stable scatter).  The chain path sorts by x_k alone
+// for every mode (chains.cu), the per-mode buckets of SURVEY §8(a) A0.
 // The result is unique (stable sorts are), so it is compared bit-exactly with the
 // oracle's numpy argsort(kind="stable") on the same keys.
 #include "prgd_internal.cuh"
@@ -21,8 +19,7 @@ constexpr int kRsSub = 512;                     // items per warp per tile
 constexpr int kRsTile = kRsSub * kRsWarps;      // 4096 items per block
 
 __global__ void k_make_keys(const int32_t* __restrict__ idx, int64_t m, int d,
-                            const int* __restrict__ n, int KL, int bitsP, int bitsS, int64_t NL,
-                            int64_t NR, int nbL, int nbR, int nsubL, int nsubR,
+                            const int* __restrict__ n, int KL, int bitsP, int bitsS,
                             uint64_t* __restrict__ kpre,
                             uint64_t* __restrict__ ksuf, uint32_t* __restrict__ vals, Scalars* sc) {
   int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -45,29 +42,8 @@ __global__ void k_make_keys(const int32_t* __restrict__ idx, int64_t m, int d,
     P = 0;
     S = 0;
   }
-  // virtual rows: gather block of the other side's index first (A0)
-  const uint64_t VP = (S * (uint64_t)nbL / (uint64_t)NR) * (uint64_t)NL + P;
-  const uint64_t VS = (P * (uint64_t)nbR / (uint64_t)NL) * (uint64_t)NR + S;
-  // middle-split order inside a row (sub != 0): the suffix index as (j = x_KL, S' = S / n_KL)
-  // with j most significant, the prefix index as (i = x_{KL-1}, P' = P / n_{KL-1}), so that
-  // the samples of a row form contiguous runs of equal middle digit (passes).
-  // stored as (digit << shift) | rest with 2^shift >= the rest's range: same order as
-  // digit * range + rest, decoded with a shift and a mask
-  uint64_t Sk = S, Pk = P;
-  if (nsubR > 1) {
-    const uint64_t rr = NR / (uint64_t)nsubR;
-    int sh = 0;
-    while ((1ull << sh) < rr) ++sh;
-    Sk = ((S % (uint64_t)nsubR) << sh) | (S / (uint64_t)nsubR);
-  }
-  if (nsubL > 1) {
-    const uint64_t rr = NL / (uint64_t)nsubL;
-    int sh = 0;
-    while ((1ull << sh) < rr) ++sh;
-    Pk = ((P % (uint64_t)nsubL) << sh) | (P / (uint64_t)nsubL);
-  }
-  kpre[s] = (VP << bitsS) | Sk;
-  ksuf[s] = (VS << bitsP) | Pk;
+  kpre[s] = (P << bitsS) | S;
+  ksuf[s] = (S << bitsP) | P;
   vals[s] = (uint32_t)s;
 }
 
@@ -283,12 +259,10 @@ int64_t radix_hist_len(int64_t m) {
 }
 
 void launch_make_keys(cudaStream_t s, const int32_t* idx, int64_t m, int d, const int* n_dev,
-                      int KL, int bitsP, int bitsS, int64_t NL, int64_t NR, int nbL, int nbR,
-                      int nsubL, int nsubR, uint64_t* kpre, uint64_t* ksuf, uint32_t* vals,
+                      int KL, int bitsP, int bitsS, uint64_t* kpre, uint64_t* ksuf, uint32_t* vals,
                       Scalars* sc, int64_t* launches) {
   if (m <= 0) return;
-  k_make_keys<<<grid_for(m, 256), 256, 0, s>>>(idx, m, d, n_dev, KL, bitsP, bitsS, NL, NR, nbL,
-                                                nbR, nsubL, nsubR, kpre, ksuf, vals, sc);
+  k_make_keys<<<grid_for(m, 256), 256, 0, s>>>(idx, m, d, n_dev, KL, bitsP, bitsS, kpre, ksuf, vals, sc);
   ++*launches;
 }
 

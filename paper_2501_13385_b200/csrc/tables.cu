@@ -488,354 +488,3 @@ void launch_back_level(cudaStream_t s, bool left, const double* X, int ldX, cons
 }
 
 }  // namespace prgd
-
-namespace prgd {
-// ============================================================================ DMMA versions
-// The table levels and the backward recursions are skinny GEMMs over the "flat" rows of a
-// table level: for a parent row p the n_k child rows (ld columns each) are contiguous, i.e.
-// a row of W = n_k ld doubles (PAPER.md:99-105 recursion):
-//   forward   out[p, :] = in[p, 0:K] . Cst[0:K, 0:W]                  (K = r_in <= 32)
-//   backward  O[p, 0:olen] = X[p, :] . Ust[:, 0:olen]                   (next E / F level)
-//             Z[v, :]      += sum_p V[p, v] X[p, :]                      (Y_k, split over CTAs)
-// with the core staged (zero-padded) in the order each side needs.  FP64 tensor-core tiles
-// (mma.sync m8n8k4 f64, SASS DMMA); operand strides = 4 (mod 16) doubles keep the fragment
-// loads bank-conflict free.  Used when W <= 512 and ranks <= 32; else the kernels above.
-namespace {
-
-__device__ __forceinline__ void dmma_t(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
-}
-
-__host__ __device__ inline int mma_ld(int w) { return ((w + 15) / 16) * 16 + 4; }
-
-constexpr int kMmaThreads = 256;
-constexpr int kFwdRows = 32;     // parent rows per forward tile
-constexpr int kBackRows = 32;    // parent rows per backward tile
-
-// Forward table level.  left:  Cst[i][(j,c)] = C[i][j][c] (c < r1), K = r0, out ld = ld_out.
-//                       right: Cst[c][(j,i)] = C[i][j][c] (i < r0), K = r1.
-// The flat output row of parent p is out[p*W + q] (child row p*nk + j = q / ld_out for both
-// sides).  Warp w owns the column blocks J = w, w+8, ...; per 32-row tile it loads its A
-// fragments straight from global (in[p][k], the one parent row [1] when in == nullptr) and
-// writes each 8x8 tile as double2 stores.  rowscale (psi) multiplies child row p*nk + j.
-template <int KSM>
-__global__ void __launch_bounds__(kMmaThreads) k_tab_mma(
-    int left, const double* __restrict__ in, int ld_in, const double* __restrict__ core, int r0,
-    int nk, int r1, double* __restrict__ out, int ld_out, int64_t nparent,
-    const double* __restrict__ rowscale, const Scalars* sc) {
-  if (sc && sc->noop) return;
-  extern __shared__ double sm[];
-  const int K = in ? (left ? r0 : r1) : 1;
-  const int KS = (K + 3) >> 2;
-  const int W = nk * ld_out;
-  const int ldc = mma_ld(W);
-  const int lg = __ffs(ld_out) - 1;                 // ld_out is a power of two
-  double* Cs = sm;                                  // 4 KS x ldc
-  for (int t = threadIdx.x; t < 4 * KS * W; t += blockDim.x) {
-    const int k = t / W, q = t - k * W;
-    const int j = q >> lg, o = q & (ld_out - 1);
-    double v = 0.0;
-    if (k < K) {
-      if (left) v = o < r1 ? core[((int64_t)k * nk + j) * r1 + o] : 0.0;
-      else v = o < r0 ? core[((int64_t)o * nk + j) * r1 + k] : 0.0;
-    }
-    Cs[k * ldc + q] = v;
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int gid = lane >> 2, tq = lane & 3;
-  const int nJ = W >> 3;
-  const int64_t ntiles = (nparent + kFwdRows - 1) / kFwdRows;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t p0 = tile * kFwdRows;
-    double af[4][KSM];
-#pragma unroll
-    for (int I = 0; I < 4; ++I) {
-      const int64_t p = p0 + I * 8 + gid;
-#pragma unroll
-      for (int ks = 0; ks < KSM; ++ks) {
-        const int k = 4 * ks + tq;
-        double v = 0.0;
-        if (ks < KS && k < K && p < nparent) v = in ? __ldg(in + p * ld_in + k) : 1.0;
-        af[I][ks] = v;
-      }
-    }
-    for (int J = warp; J < nJ; J += kMmaThreads / 32) {
-      const int q = J * 8 + 2 * tq;
-      const int j = q >> lg;
-#pragma unroll
-      for (int I = 0; I < 4; ++I) {
-        double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < KSM; ++ks)
-          if (ks < KS) dmma_t(d0, d1, af[I][ks], Cs[(4 * ks + tq) * ldc + J * 8 + gid]);
-        const int64_t p = p0 + I * 8 + gid;
-        if (p < nparent) {
-          const double f = rowscale ? __ldg(rowscale + p * nk + j) : 1.0;
-          __stcs(reinterpret_cast<double2*>(out + p * W + q), make_double2(d0 * f, d1 * f));
-        }
-      }
-    }
-  }
-}
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  const int n = pred ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n));
-}
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  const int n = pred ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(n));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
-__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-__device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
-// Backward level.  X rows p (W = nk*wrow doubles, contiguous), V[p][0:vlen] (ldV) or ones,
-// Ust[q][o] = core staged (left: U[o][j][c] at q = (j,c); right: U[i][j][o] at q = (j,i)),
-// O[p][0:ldO] (olen valid, zero pad) or null; partial Z per CTA: [vlen][W].  One CTA per SM
-// walks its 32-row tiles with a two-stage cp.async pipeline (tile t+1 lands while t computes).
-__global__ void __launch_bounds__(kMmaThreads) k_back_mma(
-    int left, const double* __restrict__ X, int wrow, const double* __restrict__ V, int ldV,
-    int vlen, const double* __restrict__ core, int r0, int nk, int r1, double* __restrict__ O,
-    int ldO, int olen, int64_t ngroups, double* __restrict__ partial, const Scalars* sc) {
-  if (sc && sc->noop) return;
-  extern __shared__ double sm[];
-  const int W = nk * wrow;
-  const int ldx = mma_ld(W);
-  const int olen8 = max((olen + 7) & ~7, O ? ((ldO + 7) & ~7) : 0), vlen8 = (vlen + 7) & ~7;
-  const int ldv = mma_ld(vlen8);
-  const int ldu = mma_ld(olen8);
-  double* Us = sm;                                 // W x ldu
-  double* Xs0 = Us + (int64_t)W * ldu;             // 2 x (kBackRows x ldx)
-  double* Vs0 = Xs0 + 2 * (int64_t)kBackRows * ldx;  // 2 x (kBackRows x ldv)
-  if (O) {
-    for (int t = threadIdx.x; t < W * olen8; t += blockDim.x) {
-      const int q = t / olen8, o = t - q * olen8;
-      const int j = q / wrow, x = q - j * wrow;
-      double v = 0.0;
-      if (o < olen) {
-        if (left) v = x < r1 ? core[((int64_t)o * nk + j) * r1 + x] : 0.0;   // U[o=i][j][x=c]
-        else v = x < r0 ? core[((int64_t)x * nk + j) * r1 + o] : 0.0;        // U[x=i][j][o=c]
-      }
-      Us[q * ldu + o] = v;
-    }
-  }
-  if (!V) {
-    for (int t = threadIdx.x; t < 2 * kBackRows * ldv; t += blockDim.x) {
-      const int v = (t % ldv);
-      Vs0[t] = v < vlen ? 1.0 : 0.0;
-    }
-  }
-  const int w2 = W >> 1;
-  auto prefetch = [&](int64_t tile, int buf) {
-    const int64_t p0 = tile * kBackRows;
-    double* Xs = Xs0 + (int64_t)buf * kBackRows * ldx;
-    for (int t = threadIdx.x; t < kBackRows * w2; t += blockDim.x) {
-      const int r = t / w2, q2 = t - r * w2;
-      const int64_t p = p0 + r;
-      const bool ok = p < ngroups;
-      cp_async16(Xs + r * ldx + 2 * q2, X + (ok ? p * W + 2 * q2 : 0), ok);
-    }
-    if (V) {
-      double* Vs = Vs0 + (int64_t)buf * kBackRows * ldv;
-      for (int t = threadIdx.x; t < kBackRows * vlen8; t += blockDim.x) {
-        const int r = t / vlen8, v = t - r * vlen8;
-        const int64_t p = p0 + r;
-        const bool ok = p < ngroups && v < vlen;
-        cp_async8(Vs + r * ldv + v, V + (ok ? p * ldV + v : 0), ok);
-      }
-    }
-  };
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kMmaThreads / 32;
-  const int gid = lane >> 2, tq = lane & 3;
-  const int zt_n = W >> 3, zt = (vlen8 >> 3) * zt_n;
-  constexpr int kZU = 32;
-  double z0[kZU], z1[kZU];
-#pragma unroll
-  for (int u = 0; u < kZU; ++u) z0[u] = z1[u] = 0.0;
-  const int64_t ntiles = (ngroups + kBackRows - 1) / kBackRows;
-  int buf = 0;
-  if ((int64_t)blockIdx.x < ntiles) prefetch(blockIdx.x, 0);
-  cp_commit();
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t p0 = tile * kBackRows;
-    if (tile + gridDim.x < ntiles) prefetch(tile + gridDim.x, buf ^ 1);
-    cp_commit();
-    cp_wait1();
-    __syncthreads();
-    const double* Xs = Xs0 + (int64_t)buf * kBackRows * ldx;
-    const double* Vs = Vs0 + (int64_t)buf * kBackRows * ldv;
-    // Z[v][q] += sum_r Vs[r][v] Xs[r][q]
-#pragma unroll
-    for (int u = 0; u < kZU; ++u) {
-      const int t = warp + nw * u;
-      if (t < zt) {
-        const int vb = t / zt_n, qb = t - vb * zt_n;
-        double d0 = z0[u], d1 = z1[u];
-#pragma unroll
-        for (int k = 0; k < kBackRows; k += 4)
-          dmma_t(d0, d1, Vs[(k + tq) * ldv + vb * 8 + gid], Xs[(k + tq) * ldx + qb * 8 + gid]);
-        z0[u] = d0;
-        z1[u] = d1;
-      }
-    }
-    // O[p][o] = sum_q Xs[r][q] Us[q][o]
-    if (O) {
-      const int ot_n = olen8 >> 3, ot = (kBackRows / 8) * ot_n;
-      for (int t = warp; t < ot; t += nw) {
-        const int rb = t / ot_n, ob = t - rb * ot_n;
-        const double* xr = Xs + (rb * 8 + gid) * ldx + tq;
-        const double* ur = Us + tq * ldu + ob * 8 + gid;
-        double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0, f0 = 0.0, f1 = 0.0, g0 = 0.0, g1 = 0.0;
-        int q = 0;
-        for (; q + 16 <= W; q += 16) {
-          dmma_t(d0, d1, xr[q], ur[q * ldu]);
-          dmma_t(e0, e1, xr[q + 4], ur[(q + 4) * ldu]);
-          dmma_t(f0, f1, xr[q + 8], ur[(q + 8) * ldu]);
-          dmma_t(g0, g1, xr[q + 12], ur[(q + 12) * ldu]);
-        }
-        for (; q < W; q += 4) dmma_t(d0, d1, xr[q], ur[q * ldu]);
-        const int64_t p = p0 + rb * 8 + gid;
-        const int o = ob * 8 + 2 * tq;
-        if (p < ngroups) {
-          if (o < ldO) O[p * ldO + o] = (o < olen) ? (d0 + e0) + (f0 + g0) : 0.0;
-          if (o + 1 < ldO) O[p * ldO + o + 1] = (o + 1 < olen) ? (d1 + e1) + (f1 + g1) : 0.0;
-        }
-      }
-    }
-    __syncthreads();
-    buf ^= 1;
-  }
-  cp_wait0();
-  double* out = partial + (int64_t)blockIdx.x * vlen * W;
-#pragma unroll
-  for (int u = 0; u < kZU; ++u) {
-    const int t = warp + nw * u;
-    if (t < zt) {
-      const int vb = t / zt_n, qb = t - vb * zt_n;
-      const int v = vb * 8 + gid, q = qb * 8 + 2 * tq;
-      if (v < vlen) {
-        out[(int64_t)v * W + q] = z0[u];
-        out[(int64_t)v * W + q + 1] = z1[u];
-      }
-    }
-  }
-}
-
-// Y_k from the CTA partials of Z: one warp per output, lane l sums chunks l, l+32, ... then a
-// fixed shuffle tree (deterministic).  left: Y[i][j][c] = Z[i][j*wrow + c];
-// right: Y[i][j][c] = Z[c][j*wrow + i].
-__global__ void k_Yz_reduce(int left, const double* __restrict__ partial, int64_t nchunks, int vlen,
-                            int W, int wrow, int r0, int nk, int r1, double* __restrict__ Y,
-                            const Scalars* sc) {
-  if (sc && sc->noop) return;
-  const int64_t o = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const int64_t count = (int64_t)r0 * nk * r1;
-  if (o >= count) return;
-  const int i = (int)(o / ((int64_t)nk * r1));
-  const int rem = (int)(o - (int64_t)i * nk * r1);
-  const int j = rem / r1, c = rem - j * r1;
-  const int64_t zi = left ? (int64_t)i * W + j * wrow + c : (int64_t)c * W + j * wrow + i;
-  double acc = 0.0;
-  for (int64_t ch = lane; ch < nchunks; ch += 32) acc += partial[ch * vlen * W + zi];
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (lane == 0) Y[o] = acc;
-}
-
-int g_num_sms = 0;
-int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
-  return g_num_sms;
-}
-
-}  // namespace
-
-bool tab_mma_ok(int r0, int nk, int r1, int ld_out) {
-  return (int64_t)nk * ld_out <= 1024 && r0 <= kMaxRank && r1 <= kMaxRank && (nk * ld_out) % 8 == 0;
-}
-
-size_t tab_mma_smem(bool left, int r0, int nk, int r1, int ld_out) {
-  const int K = left ? r0 : r1;
-  const int W = nk * ld_out;
-  return (size_t)((K + 3) & ~3) * mma_ld(W) * sizeof(double);
-}
-
-void launch_tab_mma(cudaStream_t s, bool left, const double* in, int ld_in, const double* core,
-                    int r0, int nk, int r1, double* out, int ld_out, int64_t rows_out,
-                    const double* rowscale, const Scalars* sc, int64_t* launches) {
-  const int64_t nparent = rows_out / nk;
-  const int64_t ntiles = (nparent + kFwdRows - 1) / kFwdRows;
-  int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms() * 2);
-  if (grid < 1) grid = 1;
-  const int K = in ? (left ? r0 : r1) : 1;
-  const size_t smem = tab_mma_smem(left, r0, nk, r1, ld_out);
-  if (K <= 16)
-    k_tab_mma<4><<<(unsigned)grid, kMmaThreads, smem, s>>>(left ? 1 : 0, in, ld_in, core, r0, nk, r1,
-                                                           out, ld_out, nparent, rowscale, sc);
-  else
-    k_tab_mma<8><<<(unsigned)grid, kMmaThreads, smem, s>>>(left ? 1 : 0, in, ld_in, core, r0, nk, r1,
-                                                           out, ld_out, nparent, rowscale, sc);
-  ++*launches;
-}
-
-static size_t back_mma_smem(int W, int vlen, int olen);
-
-bool back_mma_ok(int r0, int nk, int r1, int wrow) {
-  const int W = nk * wrow;
-  const int mx = std::max(r0, r1);
-  return W <= 512 && W % 8 == 0 && r0 <= kMaxRank && r1 <= kMaxRank &&
-         back_mma_smem(W, mx, pad_rank(mx)) <= 200 * 1024 &&
-         (((r0 + 7) / 8) * (W / 8) <= 32 * (kMmaThreads / 32)) &&
-         (((r1 + 7) / 8) * (W / 8) <= 32 * (kMmaThreads / 32));
-}
-
-static size_t back_mma_smem(int W, int vlen, int olen) {
-  return ((size_t)W * mma_ld((olen + 7) & ~7) + 2 * (size_t)kBackRows * mma_ld(W) +
-          2 * (size_t)kBackRows * mma_ld((vlen + 7) & ~7)) * sizeof(double);
-}
-
-int64_t back_mma_partial_need(int64_t ngroups, int r0, int nk, int r1, int wrow) {
-  const int64_t ntiles = (ngroups + kBackRows - 1) / kBackRows;
-  const int64_t grid = std::min<int64_t>(ntiles, 160);
-  return std::max<int64_t>(grid, 1) * (int64_t)std::max(r0, r1) * nk * wrow;
-}
-
-void launch_back_mma(cudaStream_t s, bool left, const double* X, int wrow, const double* V, int ldV,
-                     const double* core, int r0, int nk, int r1, double* O, int ldO,
-                     int64_t ngroups, double* Y, double* partial, int64_t partial_cap,
-                     const Scalars* sc, int64_t* launches) {
-  const int W = nk * wrow;
-  const int vlen = left ? r0 : r1;
-  const int olen = left ? r0 : r1;
-  const int64_t ntiles = (ngroups + kBackRows - 1) / kBackRows;
-  int64_t grid = std::min<int64_t>(ntiles, std::min(num_sms(), 160));
-  const int64_t per = (int64_t)vlen * W;
-  if (grid * per > partial_cap) grid = partial_cap / per;
-  if (grid < 1) grid = 1;
-  const size_t smem = back_mma_smem(W, vlen, O ? std::max(olen, ldO) : olen);
-  k_back_mma<<<(unsigned)grid, kMmaThreads, smem, s>>>(left ? 1 : 0, X, wrow, V, ldV, vlen, core, r0,
-                                                      nk, r1, O, ldO, olen, ngroups, partial, sc);
-  const int64_t count = (int64_t)r0 * nk * r1;
-  k_Yz_reduce<<<blocks_for(count * 32, 256), 256, 0, s>>>(left ? 1 : 0, partial, grid, vlen, W, wrow,
-                                                          r0, nk, r1, Y, sc);
-  *launches += 2;
-}
-
-void tables_mma_init() {
-  cudaFuncSetAttribute(k_tab_mma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_tab_mma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_back_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-}
-
-}  // namespace prgd

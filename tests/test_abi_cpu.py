@@ -35,12 +35,15 @@ def test_plan_split_and_validation():
            ((4, 4, 4), (2, 2, 2, 1), pkg.TT_ERR_RANK),     # r_0 != 1
            ((2, 3, 2), (1, 2, 5, 1), pkg.TT_ERR_RANK),     # r_2 > r_1 n_2 = 6? no: > n_3 r_3 = 2
            ((4,), (1, 1), pkg.TT_ERR_ARG),                 # d < 2
-           ((100,) * 4, (1, 33, 33, 33, 1), pkg.TT_ERR_UNSUPPORTED),
-           ((1 << 20,) * 4, (1, 2, 2, 2, 1), pkg.TT_ERR_UNSUPPORTED)]
+           ((100,) * 4, (1, 33, 33, 33, 1), pkg.TT_ERR_UNSUPPORTED)]
     for n, r, code in bad:
         with pytest.raises(pkg.PRGDError) as ei:
             pkg.plan(n, r)
         assert ei.value.code == code, (n, r)
+    # shapes whose prefix / suffix tables cannot fit resolve to the per-sample chain path
+    # (tt_plan reports K_L = 0): 2^40 rows per side, or d = 16 binary-free n = 16 (16^8 rows)
+    assert pkg.plan((1 << 20,) * 4, (1, 2, 2, 2, 1)) == (0, 0, 0)
+    assert pkg.plan((16,) * 16, (1,) + (8,) * 15 + (1,)) == (0, 0, 0)
 
 
 def test_create_validates_before_touching_the_device():

@@ -439,53 +439,21 @@ def test_split_point():
     assert oracle.split_point((20, 20, 20)) == 1
 
 
-def test_blocked_stable_order_matches_python_sort():
-    # Gather-blocked A0 order: prefix order sorted by
-    # (block of S, P, S), block = floor(S nb / N_R), stable; suffix by (block of P, S, P).
-    rng = np.random.default_rng(15)
-    n = (3, 5, 2, 4)
-    m = 300
+def test_stable_buckets_match_python_sort():
+    # Per-mode buckets (the chain path): perm_k = the stable order of the
+    # sample ids by x_k, i.e. Python's sorted() on the key (x_{s,k}, s); offs_k = exclusive
+    # cumulative bucket counts, empty buckets included.
+    rng = np.random.default_rng(17)
+    n = (3, 7, 1, 4)
+    m = 250
     idx = np.stack([rng.integers(0, nk, m) for nk in n], axis=1).astype(np.int32)
-    KL = oracle.split_point(n)
-    NL, NR = int(np.prod(n[:KL])), int(np.prod(n[KL:]))
-    for nbL, nbR in [(2, 4), (4, 2), (1, 1)]:
-        o = oracle.stable_order(idx, n, KL, nbL, nbR)
-
-        def P(s):
-            v = 0
-            for k in range(KL):
-                v = v * n[k] + int(idx[s, k])
-            return v
-
-        def S(s):
-            v = 0
-            for k in range(len(n) - 1, KL - 1, -1):
-                v = v * n[k] + int(idx[s, k])
-            return v
-
-        pre = sorted(range(m), key=lambda s: (S(s) * nbL // NR, P(s), S(s), s))
-        suf = sorted(range(m), key=lambda s: (P(s) * nbR // NL, S(s), P(s), s))
-        assert list(o["perm_pre"]) == pre and list(o["perm_suf"]) == suf
-        assert len(o["offs_L"]) == nbL * NL + 1 and len(o["offs_R"]) == nbR * NR + 1
-        vp = [(S(s) * nbL // NR) * NL + P(s) for s in pre]
-        for v in range(nbL * NL):
-            assert o["offs_L"][v + 1] - o["offs_L"][v] == vp.count(v)
-
-
-def test_middle_stable_order_matches_python_sort():
-    # Middle-split in-row order: prefix rows sorted by (x_{K_L+1}, S'),
-    # suffix rows by (x_{K_L}, P'), stable; 1-based modes as in the paper.
-    rng = np.random.default_rng(16)
-    n = (3, 4, 5, 2)
-    m = 300
-    idx = np.stack([rng.integers(0, nk, m) for nk in n], axis=1).astype(np.int32)
-    KL = 2
-    o = oracle.stable_order(idx, n, KL, middle=True)
-
-    def P(s):
-        return int(idx[s, 0]) * n[1] + int(idx[s, 1])
-
-    pre = sorted(range(m), key=lambda s: (P(s), int(idx[s, 2]), int(idx[s, 3]), s))
-    suf = sorted(range(m), key=lambda s: (int(idx[s, 3]) * n[2] + int(idx[s, 2]),
-                                          int(idx[s, 1]), int(idx[s, 0]), s))
-    assert list(o["perm_pre"]) == pre and list(o["perm_suf"]) == suf
+    idx[:, 1] = np.where(idx[:, 1] == 5, 6, idx[:, 1])          # bucket 5 of mode 1 stays empty
+    out = oracle.stable_buckets(idx, n)
+    for k in range(len(n)):
+        perm, offs = out[k]
+        assert list(perm) == sorted(range(m), key=lambda s: (int(idx[s, k]), s))
+        assert len(offs) == n[k] + 1 and offs[0] == 0 and offs[-1] == m
+        for j in range(n[k]):
+            assert offs[j + 1] - offs[j] == int(np.sum(idx[:, k] == j))
+            assert np.all(idx[perm[offs[j]:offs[j + 1]], k] == j)
+    assert out[1][1][6] == out[1][1][5]
