@@ -145,6 +145,17 @@ PRGD_API int tt_get_core(tt_ctx* ctx, int k, double* h_core_out);
  * TT (the multi-indices of Omega stay on the device for this). */
 PRGD_API int tt_set_metric(tt_ctx* ctx, int eps_rule, double eps, int step_rule);
 
+/* Retraction (Alg. 2 line 5):
+ *   TT_RETRACT_PLAIN     T_{l+1} = SVD_r^tt(W_l), Alg. 1 as TT-rounding of the rank-2r W_l (default;
+ *                        reading R8).  Output cores 0..d-2 left-orthogonal.
+ *   TT_RETRACT_WEIGHTED  T_{l+1} = W_l^{-1/2} SVD_r^tt(W_l^{1/2} W_l), the alternative of the Remark
+ *                        at PAPER.md:365-367 (PRGD becomes "almost RGD on That"): the rounding acts on
+ *                        the weighted blocks and the rounded cores' mode-2 slices are divided by
+ *                        phi_{k,j} (Prop. 3.1).  Output cores are then not left-orthogonal.
+ * Takes effect from the next tt_prgd_step. */
+enum { TT_RETRACT_PLAIN = 0, TT_RETRACT_WEIGHTED = 1 };
+PRGD_API int tt_set_retraction(tt_ctx* ctx, int kind);
+
 /* Spectral initialisation at scale: set every core to
  * T_0 = SVD_r^tt(p^{-1} P_Omega(y)), Alg. 1 (TT-SVD) applied to the sparse
  * zero-filled, rescaled observations (the "TT-SVD spectral initialization" of PAPER.md:42;

@@ -393,10 +393,12 @@ def tangent_sum(Ttil, A):
 
 # --------------------------------------------------------------------------- Alg. 2
 def prgd_step(cores, idx, y, n, r, step_size, eps_rule="vee", eps_value=None,
-              step_rule="theory", return_info=False):
+              step_rule="theory", return_info=False, retraction="plain"):
     """One iteration of Alg. 2 without trimming (reading R9):
     G_l = P_Omega(T_l - T*); alpha_l; W_l = T_l - alpha_l P~_T W^{-1} G_l with
-    P~_T = W^{-1/2} P_{That} W^{1/2} (Lemma, PAPER.md:331-336); T_{l+1} = SVD_r^tt(W_l).
+    P~_T = W^{-1/2} P_{That} W^{1/2} (Lemma, PAPER.md:331-336); T_{l+1} = SVD_r^tt(W_l)
+    (retraction "plain", Alg. 2 line 5) or W_l^{-1/2} SVD_r^tt(W_l^{1/2} W_l) ("weighted", the
+    Remark at PAPER.md:365-367; W^{+-1/2} applied to the TT by Prop. 3.1).
     """
     d = len(n)
     cores = [np.asarray(c, dtype=np.float64) for c in cores]
@@ -423,7 +425,12 @@ def prgd_step(cores, idx, y, n, r, step_size, eps_rule="vee", eps_value=None,
     else:
         alpha = step_length(step_size, eps, p, step_rule)        # A12
     B = assemble(tv["Ttil"], tv["A"], alpha)                     # A13
-    new = tt_round(B, r)                                         # A14
+    if retraction == "plain":
+        new = tt_round(B, r)                                     # A14
+    elif retraction == "weighted":
+        new = weight_cores(tt_round(weight_cores(B, phi, 1.0), r), phi, -1.0)
+    else:
+        raise ValueError(retraction)
     info.update(noop=False, w=w, phi=phi, ghat=ghat, alpha=alpha, B=B, **tv)
     return (new, info) if return_info else new
 

@@ -78,6 +78,7 @@ def load() -> ctypes.CDLL:
         "tt_plan": (ctypes.c_int, [ctypes.c_int, i64p, i64p, ctypes.POINTER(ctypes.c_int),
                                    i64p, i64p]),
         "tt_set_path": (ctypes.c_int, [P, ctypes.c_int]),
+        "tt_set_retraction": (ctypes.c_int, [P, ctypes.c_int]),
         "tt_get_path": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_int)]),
         "tt_spectral_init": (ctypes.c_int, [P]),
         "tt_set_allreduce": (ctypes.c_int, [P, ALLREDUCE_FN, P, ctypes.c_int64]),
@@ -249,6 +250,11 @@ class TTContext:
     def set_metric(self, eps_rule: str = "vee", eps: float = 0.0, step_rule: str = "theory"):
         self._check(self.lib.tt_set_metric(self._h, EPS_RULES[eps_rule], float(eps),
                                            STEP_RULES[step_rule]), "tt_set_metric")
+
+    def set_retraction(self, kind: str = "plain"):
+        """"plain": SVD_r^tt(W_l) (Alg. 2 line 5); "weighted": W^{-1/2} SVD_r^tt W^{1/2}."""
+        self._check(self.lib.tt_set_retraction(self._h, {"plain": 0, "weighted": 1}[kind]),
+                    "tt_set_retraction")
 
     # -- hot path
     def step(self, step_size: float = 1.0):

@@ -177,6 +177,7 @@ struct tt_ctx {
   std::vector<char> core_set;
   bool evalValid = false, tablesC = false;
   int eps_rule = TT_EPS_VEE, step_rule = TT_STEP_THEORY;
+  int retraction = TT_RETRACT_PLAIN;
   double eps_fixed = 0.0;
 
   cudaGraphExec_t gA = nullptr, gB = nullptr;
@@ -417,6 +418,7 @@ DenseArgs dense_args(tt_ctx* ctx) {
   a.clw_len = ctx->clw_len;
   a.sc = ctx->sc;
   a.smem_doubles = dense_smem_doubles();
+  a.wretr = ctx->retraction == TT_RETRACT_WEIGHTED ? 1 : 0;
   return a;
 }
 
@@ -1203,6 +1205,15 @@ int tt_set_metric(tt_ctx* ctx, int eps_rule, double eps, int step_rule) {
   ctx->eps_fixed = eps;
   ctx->step_rule = step_rule;
   drop_graphs(ctx);   // rules are baked into the captured update graph
+  return TT_OK;
+}
+
+int tt_set_retraction(tt_ctx* ctx, int kind) {
+  if (!ctx) return TT_ERR_ARG;
+  if (kind != TT_RETRACT_PLAIN && kind != TT_RETRACT_WEIGHTED)
+    return fail(ctx, TT_ERR_ARG, "unknown retraction");
+  ctx->retraction = kind;
+  drop_graphs(ctx);   // baked into the captured update graph
   return TT_OK;
 }
 

@@ -1076,20 +1076,24 @@ __global__ void __launch_bounds__(kProjThreads) k_project(DenseArgs a) {
     if (threadIdx.x == 0) sc->adapt_num[k] = red[0];
     return;
   }
-  // A11 + A13: B_k from Ttil = U/phi and X = -alpha Ahat/phi
+  // A11 + A13: B_k from Ttil = U/phi and X = -alpha Ahat/phi.  With the weighted retraction
+  // the rounding acts on W^{1/2} W_l, i.e. on the same blocks without the
+  // 1/phi slice scaling (Prop. 3.1: W^{1/2} scales mode-k slices by phi); k_unweight_out
+  // applies W^{-1/2} to the rounded cores.
   const double* ph = a.phi + a.phi_off[k];
+  const bool wr = a.wretr != 0;
   double* B = a.B + a.b_off[k];
   if (k == 0) {
     const int Rb1 = 2 * r1;
     for (int e = threadIdx.x; e < nk * Rb1; e += blockDim.x) {
       const int x = e / Rb1, c = e - x * Rb1;
-      const double inv = 1.0 / ph[x];
+      const double inv = wr ? 1.0 : 1.0 / ph[x];
       B[e] = c < r1 ? -alpha * Ah[x * r1 + c] * inv : U[x * r1 + (c - r1)] * inv;
     }
   } else if (k == d - 1) {
     for (int e = threadIdx.x; e < 2 * r0 * nk; e += blockDim.x) {
       const int aa = e / nk, x = e - aa * nk;
-      const double inv = 1.0 / ph[x];
+      const double inv = wr ? 1.0 : 1.0 / ph[x];
       B[e] = aa < r0 ? U[aa * nk + x] * inv
                      : (U[(aa - r0) * nk + x] - alpha * Ah[(aa - r0) * nk + x]) * inv;
     }
@@ -1100,7 +1104,7 @@ __global__ void __launch_bounds__(kProjThreads) k_project(DenseArgs a) {
       const int c = e % Rb1;
       const int x = (e / Rb1) % nk;
       const int aa = e / (Rb1 * nk);
-      const double inv = 1.0 / ph[x];
+      const double inv = wr ? 1.0 : 1.0 / ph[x];
       double v;
       if (aa < r0) v = c < r1 ? U[(aa * nk + x) * r1 + c] * inv : 0.0;
       else if (c < r1) v = -alpha * Ah[((aa - r0) * nk + x) * r1 + c] * inv;
@@ -1243,6 +1247,20 @@ __global__ void __launch_bounds__(kDenseThreads) k_dense_round(DenseArgs a) {
 
 #include "round_cs.inc"
 
+// Weighted retraction, last step: T_{l+1} = W^{-1/2} SVD_r^tt(W^{1/2} W_l),
+// the rounded cores' mode-2 slices divided by phi (Prop. 3.1).  One CTA per core.
+__global__ void k_unweight_out(DenseArgs a) {
+  if (a.sc->noop) return;
+  const int k = blockIdx.x;
+  const int r0 = a.r[k], nk = a.n[k], r1 = a.r[k + 1];
+  double* C = a.C + a.core_off[k];
+  const double* ph = a.phi + a.phi_off[k];
+  for (int64_t e = threadIdx.x; e < (int64_t)r0 * nk * r1; e += blockDim.x) {
+    const int64_t x = (e / r1) % nk;
+    C[e] = C[e] / ph[x];
+  }
+}
+
 }  // namespace
 
 int dense_smem_doubles() { return (200 * 1024) / 8; }
@@ -1274,6 +1292,10 @@ void launch_dense_round(cudaStream_t s, const DenseArgs& a, int64_t* launches) {
   k_project<<<a.d, kProjThreads, bytes, s>>>(a);
   if (!(a.clw && launch_round_cs(s, a, bytes))) k_dense_round<<<1, kDenseThreads, bytes, s>>>(a);
   *launches += 2;
+  if (a.wretr) {
+    k_unweight_out<<<a.d, 256, 0, s>>>(a);
+    ++*launches;
+  }
 }
 
 void launch_project(cudaStream_t s, const DenseArgs& a, int mode, int64_t* launches) {
@@ -1287,6 +1309,10 @@ void launch_round_only(cudaStream_t s, const DenseArgs& a, int64_t* launches) {
   const size_t bytes = (size_t)a.smem_doubles * sizeof(double);
   if (!(a.clw && launch_round_cs(s, a, bytes))) k_dense_round<<<1, kDenseThreads, bytes, s>>>(a);
   ++*launches;
+  if (a.wretr) {
+    k_unweight_out<<<a.d, 256, 0, s>>>(a);
+    ++*launches;
+  }
 }
 
 }  // namespace prgd

@@ -85,6 +85,7 @@ struct DenseArgs {
   Scalars* sc;
   int smem_doubles;  // dynamic shared memory available to the kernel, in doubles
   int proj_mode;     // k_project: 0 project + assemble, 1 project + adaptive numerator, 2 assemble
+  int wretr;         // 1: weighted retraction W^{-1/2} SVD_r^tt W^{1/2}
 };
 
 // ------------------------------------------------------------------ kernels (launchers)

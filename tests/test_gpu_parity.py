@@ -348,3 +348,26 @@ def test_full_size_config5_properties(pkg):
     assert all(b < a for a, b in zip(res, res[1:])), res
     assert res[-1] < 0.1 * res[0], res
     ctx.close()
+
+
+# Weighted retraction W^{-1/2} SVD_r^tt W^{1/2} (Remark; tt_set_retraction) on
+# both paths: one step <= 1e-11, ten steps <= 1e-9 against the oracle's "weighted" retraction.
+@pytest.mark.parametrize("cfg,m,path,steps", [(1, None, "tables", 1), (2, 50_000, "tables", 10),
+                                              (5, 200_000, "tables", 1), (6, None, "tables", 1),
+                                              (2, 50_000, "chains", 1)])
+def test_weighted_retraction(pkg, cfg, m, path, steps):
+    pr, y, init = problem(cfg, m)
+    ctx = pkg.TTContext(pr.n, pr.r, path=path)
+    ctx.set_observations(pr.idx, y)
+    ctx.set_cores(init)
+    ctx.set_retraction("weighted")
+    T = init
+    for it in range(steps):
+        ctx.step(1.0)
+        T = oracle.prgd_step(T, pr.idx, y, pr.n, pr.r, 1.0, retraction="weighted")
+    err = oracle.tt_diff_norm(ctx.get_cores(), T)
+    assert err <= (1e-11 if steps == 1 else 1e-9), err
+    plain = oracle.prgd_step(init, pr.idx, y, pr.n, pr.r, 1.0)
+    if steps == 1:
+        assert oracle.tt_diff_norm(plain, T) > 1e-9      # the variant is a different iterate
+    ctx.close()

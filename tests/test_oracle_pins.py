@@ -10,6 +10,7 @@ import numpy as np
 import pytest
 
 import oracle
+import synth
 from tests import _brute as bf
 
 
@@ -457,3 +458,25 @@ def test_stable_buckets_match_python_sort():
             assert offs[j + 1] - offs[j] == int(np.sum(idx[:, k] == j))
             assert np.all(idx[perm[offs[j]:offs[j + 1]], k] == j)
     assert out[1][1][6] == out[1][1][5]
+
+
+# ----------------------------------------------------------------- weighted retraction
+def test_weighted_retraction_matches_dense_definition():
+    # Remark at PAPER.md:365-367: T_{l+1} = W^{-1/2} SVD_r^tt(W^{1/2} W_l).  Dense check: W_l
+    # densified from the step's rank-2r blocks, W^{+-1/2} as the Kronecker diagonal
+    # prod_k phi_{k,x_k}^{+-1} applied entrywise, SVD_r^tt as the literal dense
+    # Alg. 1 (tt_svd); with eps_rule "none" (phi = 1) the two retractions coincide.
+    pr = synth.make_problem(1, seed=99, n=(5, 6, 4), r=(1, 2, 2, 1), m=60)
+    y = oracle.eval_at(pr.truth, pr.idx)
+    T0 = [c + 0.3 * np.random.default_rng(1).standard_normal(c.shape) for c in pr.truth]
+    new, info = oracle.prgd_step(T0, pr.idx, y, pr.n, pr.r, 1.0, return_info=True,
+                                 retraction="weighted")
+    Wd = oracle.to_dense(info["B"])
+    D = np.einsum("i,j,k->ijk", *info["phi"])
+    ref = oracle.to_dense(oracle.tt_svd(Wd * D, pr.r)) / D
+    assert np.linalg.norm(oracle.to_dense(new) - ref) <= 1e-12 * np.linalg.norm(ref)
+    plain = oracle.to_dense(oracle.prgd_step(T0, pr.idx, y, pr.n, pr.r, 1.0))
+    assert np.linalg.norm(plain - ref) > 1e-6 * np.linalg.norm(ref)     # a different iterate
+    a = oracle.prgd_step(T0, pr.idx, y, pr.n, pr.r, 1.0, eps_rule="none", retraction="weighted")
+    b = oracle.prgd_step(T0, pr.idx, y, pr.n, pr.r, 1.0, eps_rule="none")
+    assert oracle.tt_diff_norm(a, b) <= 1e-13
