@@ -480,3 +480,37 @@ def test_weighted_retraction_matches_dense_definition():
     a = oracle.prgd_step(T0, pr.idx, y, pr.n, pr.r, 1.0, eps_rule="none", retraction="weighted")
     b = oracle.prgd_step(T0, pr.idx, y, pr.n, pr.r, 1.0, eps_rule="none")
     assert oracle.tt_diff_norm(a, b) <= 1e-13
+
+
+def test_spectral_init_rescales_by_inverse_p():
+    # BASELINE.json config 1 / SPEC.md:371-376: T_0 = SVD_r^tt(p^{-1} P_Omega(y)).  At full TT rank
+    # (r_k = min(prod_{i<=k} n_i, prod_{i>k} n_i)) Alg. 1 is exact, so the initial tensor must equal
+    # the zero-filled observations divided by p = |Omega| / prod(n) entrywise: a x p or missing
+    # rescaling fails by a factor p^2 or p.
+    rng = np.random.default_rng(31)
+    n = (3, 4, 2)
+    r = (1, 3, 2, 1)
+    N = 24
+    lin = rng.choice(N, size=9, replace=False)
+    idx = np.stack(np.unravel_index(lin, n), axis=1).astype(np.int32)
+    y = rng.standard_normal(9)
+    T0 = oracle.to_dense(oracle.spectral_init(idx, y, n, r))
+    ref = np.zeros(n)
+    ref[tuple(idx.T)] = y * (N / 9.0)
+    np.testing.assert_allclose(T0, ref, rtol=0, atol=1e-13 * np.abs(ref).max())
+
+
+def test_step_length_theory_rule_worked_examples():
+    # Thm 4.1: alpha_l = 1.001 eps_l^{1/2} / p; SPEC.md:393 worked values 2.002 at
+    # (eps, p) = (1, 0.5) and (4, 1) -- through the rule prgd_step actually calls (A12).
+    assert oracle.step_length(1.001, 1.0, 0.5) == pytest.approx(2.002, rel=1e-15)
+    assert oracle.step_length(1.001, 4.0, 1.0) == pytest.approx(2.002, rel=1e-15)
+    assert oracle.step_length(0.5, 9.0, 0.25) == pytest.approx(6.0, rel=1e-15)
+    assert oracle.step_length(0.3, None, 0.2) == pytest.approx(1.5, rel=1e-15)   # W = I: step / p
+    assert oracle.step_length(0.7, 123.0, 0.01, "raw") == 0.7
+    # and prgd_step reports exactly that alpha for its own eps and p
+    pr = synth.make_problem(1)
+    y = oracle.eval_at(pr.truth, pr.idx)
+    T0 = [c + 0.1 for c in pr.truth]
+    _, info = oracle.prgd_step(T0, pr.idx, y, pr.n, pr.r, 1.001, return_info=True)
+    assert info["alpha"] == pytest.approx(1.001 * math.sqrt(info["eps"]) / 0.3, rel=1e-15)
