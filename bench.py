@@ -30,8 +30,13 @@ if ROOT not in sys.path:
 import numpy as np  # noqa: E402
 
 METRIC = "PRGD iter/s (observed entries/s = M x iter/s) at d=10, n=16, r=16, |Omega|~3e7, fp64"
-FP64_DMMA_TFS = 37.1   # measured DMMA fp64 peak (tools/fp64_peak.cu), DESIGN.md 8
 UNIT = "iter/s"
+# FP64 peak (MEASURED_PEAKS.json has none): 148 SMs x 64 FP64 FMA lanes x 2 flop x 1.965 GHz =
+# 37.2 TF/s (the guide's SM count and max clock); the mma.sync m8n8k4 f64 (DMMA) loop of
+# tools/fp64_peak.cu measured 37.1 TF/s at 1965 MHz (profiles/r02_fp64_peak.md) -> 37.1 is used.
+FP64_PEAK_TFS = 37.1
+FP64_PEAK_SRC = "measured DMMA loop (tools/fp64_peak.cu, profiles/r02_fp64_peak.md); derived 37.2"
+NCU_KERNELS = os.path.join(ROOT, "profiles", "r02_ncu_kernels.json")
 
 
 def peaks():
@@ -93,20 +98,68 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def algorithmic_bytes(group, m, KL, NL, NR, ld, nvrows_L, nvrows_R):
-    """Compulsory DRAM bytes of one launch of a pass kernel: streamed
-    per-sample arrays + each table row read once + outputs written once + plan."""
-    tab = lambda N: N * ld * 8  # noqa: E731
-    plan = lambda nv: nv * 20   # noqa: E731
-    if group == "passA_prefix":
-        return m * (4 + 8 + 8) + tab(NL) + tab(NR) + NL * 8 + plan(nvrows_L)
-    if group == "passA_suffix":
-        return m * (4 + 8 + 8) + NR * 8 + plan(nvrows_R)      # pos_suf, g gathered, g_suf written
-    if group == "passB_prefix":
-        return m * (4 + 8) + tab(NR) + tab(NL) + NL * 8 + plan(nvrows_L)
-    if group == "passB_suffix":
-        return m * (4 + 4 + 8) + tab(NL) + tab(NR) + NR * 8 + plan(nvrows_R)
-    return None
+def group_models(pr, KL, NL, NR):
+    """Algorithmic work of one launch of each kernel group per step: compulsory
+    DRAM bytes for the HBM-bound groups (streamed per-sample arrays + each table row read once +
+    each output written once), FP64 flops for the arithmetic groups.  Returns
+    {group: (bound, units, unit_name)}."""
+    m, d, n, r = pr.m, pr.d, pr.n, pr.r
+    ld = lambda k: 2 if r[k] <= 2 else 1 << (r[k] - 1).bit_length()   # noqa: E731  pad(r)
+    tab = lambda rows, k: rows * ld(k) * 8                             # noqa: E731
+    rows_L = [math.prod(n[:k]) for k in range(KL + 1)]
+    rows_R = [math.prod(n[k:]) for k in range(d + 1)]
+    tables = sum(tab(rows_L[k], k) for k in range(1, KL + 1)) + sum(tab(rows_R[k], k) for k in range(KL, d))
+    out = {
+        "tables_C": ("hbm", tables, "B"), "tables_U": ("hbm", tables, "B"),
+        "passA_prefix": ("hbm", m * (4 + 8 + 8) + tab(NL, KL) + tab(NR, KL) + NL * 8, "B"),
+        "passA_suffix": ("hbm", m * (4 + 8 + 8) + NR * 8, "B"),
+        "passB_prefix": ("hbm", m * (4 + 8) + tab(NR, KL) + tab(NL, KL) + NL * 8, "B"),
+        "passB_suffix": ("hbm", m * (4 + 4 + 8) + tab(NL, KL) + tab(NR, KL) + NR * 8, "B"),
+        "marginals": ("hbm", (NL + NR) * 8, "B"), "weights_psi": ("hbm", (NL + NR) * 8, "B"),
+    }
+    # backward recursions (A9 as DMMA GEMMs over the table levels): per level 4 r_k n_k r_{k+1}
+    # flops per parent row (the O and Z products)
+    fl = 0.0
+    for k in range(d):
+        parents = math.prod(n[:k]) if k < KL else math.prod(n[k + 1:])
+        fl += 4.0 * r[k] * n[k] * r[k + 1] * parents
+    out["backward_Y"] = ("fp64", fl, "flop")
+    # dense sweeps: CholeskyQR2 of each unfolding (2 Grams + 2 triangular applies, 8 rows cols^2)
+    # plus the neighbour push (2 R^2 rows); A4-A6 on r-sized cores, A10-A14 on 2r-sized blocks
+    orth = 0.0
+    for k in range(d - 1):
+        rows, cols = r[k] * n[k], r[k + 1]
+        orth += 8.0 * rows * cols ** 2 + 2.0 * cols * cols * n[k + 1] * r[k + 2] + 4.0 * rows * cols ** 2
+    out["dense_orth"] = ("fp64", orth, "flop")
+    rnd = 0.0
+    for k in range(d):
+        R0 = 1 if k == 0 else 2 * r[k]
+        R1 = 1 if k == d - 1 else 2 * r[k + 1]
+        rnd += 6.0 * r[k] * n[k] * r[k + 1] ** 2          # projection (solve, U^T Z, U W)
+        if k > 0:
+            rnd += 8.0 * n[k] * R1 * R0 ** 2 + 2.0 * R0 * R0 * n[k - 1] * (2 * r[k - 1] or 1)   # r2l QR + push
+        if k < d - 1:
+            rnd += 8.0 * r[k] * n[k] * R1 ** 2 + 2.0 * r[k + 1] * R1 * n[k + 1] * 2 * r[k + 2] \
+                + 4.0 * R1 ** 3                                                              # l2r QR, push, Jacobi
+    out["dense_round"] = ("fp64", rnd, "flop")
+    return out
+
+
+def stage_latency(pr, ms):
+    """Latency model of the dense sweeps: 2(d-1) dependent QR / truncation stages (A14) or
+    d-1 (A4-A5) + d-2 Gram steps (A6); per-stage time = group time / stages."""
+    d = pr.d
+    return {"dense_round": {"stages": 2 * (d - 1), "us_per_stage": round(1e3 * ms.get("dense_round", 0) / (2 * (d - 1)), 2)},
+            "dense_orth": {"stages": 2 * d - 3, "us_per_stage": round(1e3 * ms.get("dense_orth", 0) / max(2 * d - 3, 1), 2)}}
+
+
+def ncu_kernels():
+    """Per-kernel ncu counters captured at this build (profiles/r02_ncu_kernels.json, written by
+    tools/ncu_table.py from one ncu run of bench.py --profile-steps 1)."""
+    if not os.path.exists(NCU_KERNELS):
+        return None
+    with open(NCU_KERNELS) as f:
+        return json.load(f)
 
 
 def dist_setup(args):
@@ -136,6 +189,12 @@ def run_ours(args, rank, ws, dist):
         pr = synth.make_problem(args.config, m=args.m, rank=rank, world=ws)
     else:
         pr = synth.make_problem(args.config, m=args.m)
+    if args.rank:
+        # diagnostic only: the same Omega with every interior TT rank set to
+        # args.rank (truth and init truncated), e.g. r = 1 for the HBM-bound shape of the passes
+        pr.r = (1,) + (args.rank,) * (pr.d - 1) + (1,)
+        pr.truth = [c[:pr.r[k], :, :pr.r[k + 1]].copy() for k, c in enumerate(pr.truth)]
+        pr.init = [c[:pr.r[k], :, :pr.r[k + 1]].copy() for k, c in enumerate(pr.init)]
     t_gen = time.perf_counter() - t0
     m_global = pr.m
     if dist is not None:
@@ -285,6 +344,27 @@ def oracle_sample(pr, y, init, m_sample, steps=1, warmup=0):
     return times
 
 
+def host_info():
+    """CPU model, BLAS vendor / version and threads of the oracle's numpy."""
+    out = {"cpu_model": None, "blas": None, "affinity_cores": len(os.sched_getaffinity(0))}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    out["cpu_model"] = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+        b = [i for i in threadpool_info() if i.get("user_api") == "blas"]
+        if b:
+            out["blas"] = f"{b[0].get('internal_api')} {b[0].get('version')} ({b[0].get('num_threads')} threads)"
+    except Exception:
+        pass
+    return out
+
+
 def cpu_cores():
     try:
         from threadpoolctl import threadpool_info
@@ -304,6 +384,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--m", type=int, default=None, help="override |Omega| draws (debug only)")
+    ap.add_argument("--rank", type=int, default=0,
+                    help="diagnostic: override every interior TT rank (e.g. 1: HBM-bound passes)")
     ap.add_argument("--step-size", type=float, default=1.0)
     ap.add_argument("--step-rule", choices=["theory", "adaptive"], default="theory",
                     help="A12 rule: theory (Thm 4.1 form, the default) or adaptive (steepest step, "
@@ -311,7 +393,7 @@ def main():
     ap.add_argument("--profile-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=1_000_000)
+    ap.add_argument("--cpu-sample", type=int, default=2_000_000)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -333,44 +415,42 @@ def main():
     nsteps = max(prof["steps"], 1)
     per = {k: v / nsteps for k, v in prof["ms"].items()}
     tot = sum(per.values())
-    import paper_2501_13385_b200 as pkg  # noqa: F401
-    ld = 2
-    while ld < pr.r[r["KL"]]:
-        ld *= 2
-    pass_groups = ["passA_prefix", "passA_suffix", "passB_prefix", "passB_suffix"]
-    dom = max(per, key=per.get)
-    dom_pass = max(pass_groups, key=lambda g: per.get(g, 0.0))
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tf):
-        with open(tf) as f:
-            traffic = json.load(f).get(dom_pass)
-    alg = algorithmic_bytes(dom_pass, m, r["KL"], r["NL"], r["NR"], ld, r["NL"], r["NR"])
-    t_dom = per[dom_pass] / 1e3
-    achieved = alg / t_dom / 1e9 if t_dom > 0 else 0.0
-    roof = {"bound": "hbm", "kernel": dom_pass, "achieved": round(achieved, 1),
-            "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
-            "traffic": traffic, "peak_src": pk["src"],
-            # the kernel's measured DRAM traffic (ncu, profiles/traffic.json) over its live time:
-            # the gathers re-read table rows, so this exceeds the algorithmic bytes
-            "dram_gbs": round(traffic / t_dom / 1e9, 1) if traffic and t_dom > 0 else None,
-            "dram_frac": round(traffic / t_dom / 1e9 / pk["hbm_gbs"], 4) if traffic and t_dom > 0 else None,
-            "share_of_step": round(per[dom_pass] / tot, 4) if tot else None,
-            "group_ms": {k: round(v, 4) for k, v in per.items()},
-            "dominant_group": dom}
-    # FP64 side (SURVEY 8(d) "FP64 util vs peak"): the backward recursions are the path's dense
-    # contraction (A9 as DMMA GEMMs over the table levels); algorithmic flops per level k =
-    # 4 r_k n_k r_{k+1} per parent row (the O and Z products), parents = prod of the other modes
-    # on that side.  Peak: DMMA measured with tools/fp64_peak.cu on this pool.
-    fl = 0.0
-    for k in range(pr.d):
-        parents = math.prod(pr.n[:k]) if k < r["KL"] else math.prod(pr.n[k + 1:])
-        fl += 4.0 * pr.r[k] * pr.n[k] * pr.r[k + 1] * parents
-    t_back = per.get("backward_Y", 0.0) / 1e3
-    fp64 = {"kernel": "backward_Y", "bound": "tensor (DMMA fp64)", "flops": fl,
-            "achieved": round(fl / t_back / 1e12, 2) if t_back > 0 else None, "peak": FP64_DMMA_TFS,
-            "unit": "TFLOP/s", "frac": round(fl / t_back / 1e12 / FP64_DMMA_TFS, 4) if t_back > 0 else None,
-            "peak_src": "tools/fp64_peak.cu (mma.sync m8n8k4 f64, measured on the pool's B200)"}
+    models = group_models(pr, r["KL"], r["NL"], r["NR"])
+    ncu = ncu_kernels()
+    ncu_groups = (ncu or {}).get("groups", {})
+    table = {}
+    for g, t in per.items():
+        if t <= 0 or g not in models:
+            continue
+        bound, units, uname = models[g]
+        if bound == "hbm":
+            ach, peak, unit = units / (t / 1e3) / 1e9, pk["hbm_gbs"], "GB/s"
+        else:
+            ach, peak, unit = units / (t / 1e3) / 1e12, FP64_PEAK_TFS, "TFLOP/s"
+        ng = ncu_groups.get(g, {})
+        table[g] = {"ms": round(t, 4), "share": round(t / tot, 4), "bound": bound,
+                    "algorithmic": units, "algorithmic_unit": uname, "achieved": round(ach, 3),
+                    "peak": peak, "unit": unit, "frac": round(ach / peak, 5),
+                    "ncu_dram_bytes": ng.get("dram_bytes"), "ncu_dmma_pct": ng.get("dmma_pct"),
+                    "ncu_fp64_pct": ng.get("fp64_pct")}
+    dom = max(table, key=lambda g: table[g]["ms"])
+    td = table[dom]
+    bound = "alu" if td["bound"] == "fp64" else "hbm"
+    roof = {"bound": bound, "kernel": dom, "achieved": td["achieved"], "peak": td["peak"],
+            "unit": td["unit"], "frac": td["frac"], "traffic": td["ncu_dram_bytes"],
+            "peak_src": (pk["src"] + " MEASURED_PEAKS.json hbm_gbs") if bound == "hbm" else FP64_PEAK_SRC,
+            "share_of_step": td["share"],
+            "note": ("latency-bound dependent sweeps (one 8-CTA cluster); see latency_model"
+                     if dom in ("dense_round", "dense_orth") else ""),
+            "latency_model": stage_latency(pr, per),
+            "traffic_src": (f"{os.path.relpath(NCU_KERNELS, ROOT)} (commit {ncu.get('commit')})"
+                            if ncu else None),
+            "kernels": table}
+    # FP64 side (SURVEY 8(d) "FP64 util vs peak"): the backward recursions (the DMMA contraction)
+    bY = table.get("backward_Y", {})
+    fp64 = {"kernel": "backward_Y", "bound": "tensor (DMMA fp64)", "flops": bY.get("algorithmic"),
+            "achieved": bY.get("achieved"), "peak": FP64_PEAK_TFS, "unit": "TFLOP/s",
+            "frac": bY.get("frac"), "ncu_dmma_pipe_pct": bY.get("ncu_dmma_pct"), "peak_src": FP64_PEAK_SRC}
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
         ms_ = min(args.cpu_sample, m)
@@ -379,7 +459,7 @@ def main():
         cpu = {"value": round((ms_ / m) / t, 6), "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
                "sample": f"one oracle PRGD step on the first {ms_} of {m} observed entries; "
                          f"value = (sample/M)/t_step (linear in |Omega|); entries/s = {ms_ / t:.3e}",
-               "step_s": round(t, 3)}
+               "step_s": round(t, 3), **host_info()}
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
@@ -390,6 +470,7 @@ def main():
                    "d": pr.d, "n": list(pr.n), "r": list(pr.r), "m": m, "K_L": r["KL"],
                    "l2": "inputs larger than L2 (Omega arrays + tables > 126 MB); no flush",
                    "m_global": r["m_global"], "step_rule": args.step_rule,
+                   "diagnostic_rank_override": args.rank or None,
                    "parallelism": (f"sharded Omega over {ws} GPUs (h and Y all-reduced, NCCL); "
                                    "value = N x iter/s of the N-times-larger problem") if ws > 1
                                   else "single"},
