@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libprgd.so")
-SOURCES = ["api.cu", "sort.cu", "plan.cu", "adaptive.cu", "spectral.cu", "tables.cu", "levels.cu", "passes.cu", "chains.cu", "dense.cu"]
+SOURCES = ["api.cu", "sort.cu", "plan.cu", "adaptive.cu", "spectral.cu", "tables.cu", "levels.cu", "passes.cu", "passes_flat.cu", "chains.cu", "dense.cu"]
 INCLUDES = ["round_cs.inc"]
 HEADERS = ["prgd_internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -171,6 +171,8 @@ struct tt_ctx {
   int32_t *Spre = nullptr, *sid_pre = nullptr, *pos_suf = nullptr, *Psuf = nullptr,
           *sid_suf = nullptr;
   double *ypre = nullptr, *g = nullptr;
+  int32_t* Ppre = nullptr;    // bucket (prefix table row) of each sample, prefix order
+  void* frec = nullptr;       // chunk records of the flat pass A
   int64_t *offsL = nullptr, *offsR = nullptr;
   SegPlan planL, planR;
 
@@ -518,30 +520,34 @@ void enqueue_evaluate(tt_ctx* ctx, int64_t* lc, bool with_sumsq = true) {
   grp(ctx, 0, false);
   if (ctx->obs_set && (ctx->m > 0 || ctx->allreduce)) {
     grp(ctx, 1, true);
-    {
-      SegArgs a{};
-      a.plan = &ctx->planL;
-      a.mode = kSDDMM;
-      a.ld = ctx->ldr[KL];
+    {   // flat sample-major SDDMM with the bucket sums H_L (passes_flat.cu)
+      FlatArgs a;
+      a.row = ctx->Ppre;
       a.col = ctx->Spre;
-      a.y = ctx->ypre;
+      a.x = ctx->ypre;
       a.g = ctx->g;
+      a.m = ctx->m;
+      a.nrows = ctx->plan.NL;
+      a.ld = ctx->ldr[KL];
       a.rowtab = ctx->LT[KL];
       a.coltab = ctx->RT[KL];
       a.out = ctx->HL;
-      launch_seg(s, a, nullptr, lc);
+      a.rec = ctx->frec;
+      launch_flat_sddmm(s, a, lc);
     }
     grp(ctx, 1, false);
     grp(ctx, 2, true);
-    SegArgs b{};
-    b.plan = &ctx->planR;
-    b.mode = kGSQ;
-    b.ld = ctx->ldr[KL];
-    b.perm = ctx->pos_suf;
-    b.g = ctx->g;
-    b.g2 = ctx->g_suf;      // the gathered g, stored in suffix order for pass B
-    b.out = ctx->HR;
-    launch_seg(s, b, nullptr, lc);
+    {
+      SegArgs b{};
+      b.plan = &ctx->planR;
+      b.mode = kGSQ;
+      b.ld = ctx->ldr[KL];
+      b.perm = ctx->pos_suf;
+      b.g = ctx->g;
+      b.g2 = ctx->g_suf;      // the gathered g, stored in suffix order for pass B
+      b.out = ctx->HR;
+      launch_seg(s, b, nullptr, lc);
+    }
     grp(ctx, 2, false);
     grp(ctx, 3, true);
     launch_marginals(s, ctx->HL, ctx->plan.NL, KL, ctx->n_i.data(), true, ctx->h,
@@ -1278,6 +1284,8 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
             A(ctx, &ctx->Psuf, m + 8, OL) && A(ctx, &ctx->sid_suf, m, OL) &&
             A(ctx, &ctx->g_suf, m + 8, OL) && A(ctx, &ctx->pre2suf, m, OL) &&
             A(ctx, &ctx->offsL, NLv + 1 + 40, OL) && A(ctx, &ctx->offsR, NRv + 1 + 40, OL) &&
+            A(ctx, &ctx->Ppre, m + 8, OL) &&
+            A(ctx, reinterpret_cast<char**>(&ctx->frec), flat_rec_bytes(m), OL) &&
             (!adapt_by_chains(ctx) || A(ctx, &ctx->dval, m, OL));
   ctx->idx_dev = idx_dev;
   auto cleanup = [&]() { dfree_all(ctx, tmp); };
@@ -1324,7 +1332,7 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
     radix_sort_pairs(s, kpre, vals, ktmp, vtmp, m, bitsVP + bitsS, hist, hl, &ko, &vo, &lc);
     CK(cudaStreamWaitEvent(s, ctx->ev_side[1], 0));
     launch_after_sort_pre(s, ko, vo, m, bitsS, NLv, y_orig, ctx->Spre, ctx->ypre, ctx->sid_pre, inv,
-                          ctx->offsL, &lc);
+                          ctx->offsL, ctx->Ppre, &lc);
     ptm.mark("sort_pre");
     radix_sort_pairs(s, ksuf, vals2, ktmp, vtmp, m, bitsVS + bitsP, hist, hl, &ko, &vo, &lc);
     launch_after_sort_suf(s, ko, vo, m, bitsP, NRv, inv, ctx->pos_suf, ctx->Psuf, ctx->sid_suf,

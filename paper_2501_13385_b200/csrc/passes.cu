@@ -1,8 +1,8 @@
 // passes.cu — the two passes over Omega and the weight computation.
 //
-// Pass A, prefix side (A1-A2, SDDMM): for every bucket P and sample s in it,
+// Pass A, prefix side (A1-A2, SDDMM; passes_flat.cu): for every bucket P and sample s in it,
 //   v_s = T^{<=KL-1}(P) . T^{>=KL}(:, S(s)),  g_s = v_s - y_s,  H_L[P] = sum g_s^2
-// Pass A, suffix side (A3 input): H_R[S] = sum_{s in S} g_s^2.
+// Pass A, suffix side (A3 input, k_seg GSQ): H_R[S] = sum_{s in S} g_s^2.
 // Marginals (A3): h_{k,j} = sum of H over table rows whose k-th digit is j
 //   (= ||M_k(G)(j,:)||^2).
 // Weights (A3, A12): eps, w = eps + h, phi = w^{1/(4d)}, alpha.
@@ -464,14 +464,13 @@ inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t
 template <int LPS>
 void seg_dispatch_mode(cudaStream_t s, int mode, const SegDev& dv, unsigned grid,
                        const Scalars* sc) {
-  // SDDMM / DPASS: from 16-wide rows on, 4 columns per lane (half the lanes per sample, half the
-  // transpose-reduction and index shuffles per sample)
+  // DPASS: from 16-wide rows on, 4 columns per lane (half the lanes per sample, half the
+  // transpose-reduction and index shuffles per sample).  (Pass A's SDDMM runs as the flat
+  // sample-major kernel of passes_flat.cu.)
   if constexpr (LPS >= 8) {
-    if (mode == kSDDMM) { k_seg<LPS / 2, kSDDMM, 2><<<grid, 256, 0, s>>>(dv, sc); return; }
     if (mode == kDPASS) { k_seg<LPS / 2, kDPASS, 2><<<grid, 256, 0, s>>>(dv, sc); return; }
   }
-  if (mode == kSDDMM) k_seg<LPS, kSDDMM><<<grid, 256, 0, s>>>(dv, sc);
-  else if (mode == kDPASS) k_seg<LPS, kDPASS><<<grid, 256, 0, s>>>(dv, sc);
+  if (mode == kDPASS) k_seg<LPS, kDPASS><<<grid, 256, 0, s>>>(dv, sc);
   else if (mode == kGSQ) k_seg<1, kGSQ><<<grid, 256, 0, s>>>(dv, sc);
   else k_seg<LPS, kSPMM><<<grid, 256, 0, s>>>(dv, sc);   // (V = 2 measured slower for SpMM)
 }

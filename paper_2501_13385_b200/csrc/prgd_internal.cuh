@@ -100,7 +100,7 @@ int64_t radix_hist_len(int64_t m);
 void launch_after_sort_pre(cudaStream_t s, const uint64_t* keys, const uint32_t* sids, int64_t m,
                            int bitsS, int64_t NL, const double* y_orig, int32_t* Spre,
                            double* ypre, int32_t* sid_pre, int32_t* inv, int64_t* offsL,
-                           int64_t* launches);
+                           int32_t* Ppre, int64_t* launches);
 void launch_after_sort_suf(cudaStream_t s, const uint64_t* keys, const uint32_t* sids, int64_t m,
                            int bitsP, int64_t NR, const int32_t* inv, int32_t* pos_suf,
                            int32_t* Psuf, int32_t* sid_suf, int32_t* pre2suf, int64_t* offsR,
@@ -207,6 +207,22 @@ struct SegArgs {
   double* out;          // SDDMM/GSQ/DPASS: scalar per row; SPMM: vector per row (ld)
 };
 void launch_seg(cudaStream_t s, const SegArgs& a, const Scalars* sc, int64_t* launches);
+
+// passes_flat.cu: pass A (prefix order) as a flat sample-major SDDMM with the bucket sums H_L
+struct FlatArgs {
+  const int32_t* row = nullptr;     // [m] bucket (table row) of each sample, nondecreasing
+  const int32_t* col = nullptr;     // [m] gathered table row
+  const double* x = nullptr;        // [m] y
+  double* g = nullptr;              // [m] output g = v - y
+  int64_t m = 0, nrows = 0;
+  int ld = 2;                       // table row stride (pad(r))
+  const double* rowtab = nullptr;   // row vectors (left table)
+  const double* coltab = nullptr;   // gathered table (right table)
+  double* out = nullptr;            // [nrows] bucket sums of g^2 (H_L)
+  void* rec = nullptr;              // chunk records (flat_rec_bytes)
+};
+int64_t flat_rec_bytes(int64_t m);
+void launch_flat_sddmm(cudaStream_t s, const FlatArgs& a, int64_t* launches);
 // n_host / phi_off_host are HOST arrays (values are passed by kernel argument).
 // scratch: >= 32 * (sum of the nmodes mode sizes) doubles
 void launch_marginals(cudaStream_t s, const double* H, int64_t N, int nmodes, const int* n_host,

@@ -208,7 +208,7 @@ __global__ void k_after_pre(const uint64_t* __restrict__ keys, const uint32_t* _
                             int64_t m, int bitsS, int64_t NL, const double* __restrict__ y_orig,
                             int32_t* __restrict__ Spre, double* __restrict__ ypre,
                             int32_t* __restrict__ sid_pre, int32_t* __restrict__ inv,
-                            int64_t* __restrict__ offsL) {
+                            int64_t* __restrict__ offsL, int32_t* __restrict__ Ppre) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= m) return;
   const uint64_t mask = (1ull << bitsS) - 1ull;
@@ -216,6 +216,7 @@ __global__ void k_after_pre(const uint64_t* __restrict__ keys, const uint32_t* _
   int64_t P = (int64_t)(key >> bitsS);
   uint32_t sid = sids[t];
   Spre[t] = (int32_t)(key & mask);
+  Ppre[t] = (int32_t)P;
   ypre[t] = y_orig[sid];
   sid_pre[t] = (int32_t)sid;
   inv[sid] = (int32_t)t;
@@ -310,10 +311,10 @@ void radix_sort_pairs(cudaStream_t s, uint64_t* keys, uint32_t* vals, uint64_t* 
 void launch_after_sort_pre(cudaStream_t s, const uint64_t* keys, const uint32_t* sids, int64_t m,
                            int bitsS, int64_t NL, const double* y_orig, int32_t* Spre,
                            double* ypre, int32_t* sid_pre, int32_t* inv, int64_t* offsL,
-                           int64_t* launches) {
+                           int32_t* Ppre, int64_t* launches) {
   if (m <= 0) return;
   k_after_pre<<<grid_for(m, 256), 256, 0, s>>>(keys, sids, m, bitsS, NL, y_orig, Spre, ypre,
-                                                sid_pre, inv, offsL);
+                                                sid_pre, inv, offsL, Ppre);
   ++*launches;
 }
 
