@@ -161,10 +161,13 @@ PRGD_API int tt_set_retraction(tt_ctx* ctx, int kind);
  * zero-filled, rescaled observations (the "TT-SVD spectral initialization" of PAPER.md:42;
  * BASELINE.json config 1) without densifying it: step k takes the top r_k eigenvectors of the
  * Gram of the projected unfolding, accumulated over the samples grouped by (x_{k+1..d}, x_k)
- * (DESIGN.md §2).  Gram-based, so the kept subspace is accurate to ~u ||G|| / eigen-gap.
- * Needs observations (TT_ERR_STATE otherwise, and in sharded mode), prod(n) < 2^62 and
- * r_{k-1} n_k <= 1024 for k < d (TT_ERR_ARG), and the table path (TT_ERR_STATE on the chain
- * path).  Synchronous.  Output cores 0..d-2 have orthonormal columns L(T_k). */
+ * (DESIGN.md §2); an unfolding with r_{k-1} n_k > 1024 rows (config 3: 4096) is taken from the
+ * other side when it has at most 1024 nonzero columns (the Gram M_k^T M_k, U = M_k V Lambda^{-1/2},
+ * re-orthonormalised).  Gram-based, so the kept subspace is accurate to ~u ||G|| / eigen-gap.
+ * Needs observations (TT_ERR_STATE otherwise, and in sharded mode), prod(n) < 2^62, per step
+ * r_{k-1} n_k <= 1024 or at most 1024 distinct suffixes (x_{k+1}..x_d) in Omega (TT_ERR_ARG),
+ * and the table path (TT_ERR_STATE on the chain path).  Synchronous.  Output cores 0..d-2 have
+ * orthonormal columns L(T_k). */
 PRGD_API int tt_spectral_init(tt_ctx* ctx);
 
 /* ------------------------------------------------------------------ the hot path */

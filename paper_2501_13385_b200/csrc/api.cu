@@ -1378,12 +1378,20 @@ int tt_spectral_init(tt_ctx* ctx) {
     cs = std::max<int>(cs, (int)ctx->r[k + 1]);
   }
   if (nstar >= (long double)(1ull << 62)) return fail(ctx, TT_ERR_ARG, "spectral init needs prod(n) < 2^62");
-  int64_t Wuse = 1;
-  for (int k = 0; k + 1 < d; ++k) Wuse = std::max<int64_t>(Wuse, ctx->r[k] * ctx->n[k]);
-  if (Wuse > 1024) return fail(ctx, TT_ERR_ARG, "spectral init needs r_{k-1} n_k <= 1024 for k < d");
-  for (int k = 0; k + 1 < d; ++k)
+  // step k < d-1 takes the left Gram (W = r_{k-1} n_k <= 1024 and the Gram kernel's shared
+  // memory bound) or the right Gram (W > 1024; at most 1024 nonzero columns, checked at run time)
+  int64_t Wuse = 1, Wr = 0;
+  for (int k = 0; k + 1 < d; ++k) {
+    const int64_t W = ctx->r[k] * ctx->n[k];
+    if (W > kSpRightMax) {
+      Wr = std::max<int64_t>(Wr, W);
+      continue;
+    }
+    Wuse = std::max<int64_t>(Wuse, W);
     if ((ctx->r[k] <= 8 ? 64 : (ctx->r[k] <= 16 ? 256 : 1024)) * ctx->n[k] > 25 * 1024)
-      return fail(ctx, TT_ERR_ARG, "spectral init needs pad(r_{k-1})^2 n_k <= 25600");
+      return fail(ctx, TT_ERR_ARG, "spectral init needs pad(r_{k-1})^2 n_k <= 25600 where r_{k-1} n_k <= 1024");
+  }
+  if (Wr > ((int64_t)1 << 20)) return fail(ctx, TT_ERR_ARG, "spectral init needs r_{k-1} n_k <= 2^20");
   int rc = ensure_base(ctx);
   if (rc) return rc;
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1419,6 +1427,11 @@ int tt_spectral_init(tt_ctx* ctx) {
             A(ctx, &a.llist, m + 1, tmp) && A(ctx, &a.lchoff, m + 1, tmp) && A(ctx, &a.lchl, m + 1, tmp) &&
             A(ctx, &a.gparts, a.gram_parts_cap, tmp) && A(ctx, &a.G, Wuse * Wuse, tmp) &&
             A(ctx, &a.V, Wuse * Wuse, tmp);
+  a.Wr_max = Wr;
+  if (ok && Wr > 0)
+    ok = A(ctx, &a.Md, Wr * kSpRightMax, tmp) && A(ctx, &a.Gr, (int64_t)kSpRightMax * kSpRightMax, tmp) &&
+         A(ctx, &a.Vr, (int64_t)kSpRightMax * kSpRightMax, tmp) && A(ctx, &a.Vsel, (int64_t)kSpRightMax * kMaxRank, tmp) &&
+         A(ctx, &a.lam, kMaxRank, tmp);
   if (!ok) {
     dfree_all(ctx, tmp);
     return fail(ctx, TT_ERR_OOM, "device allocation failed (spectral init)");

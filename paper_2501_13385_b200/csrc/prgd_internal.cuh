@@ -273,8 +273,13 @@ struct SpectralArgs {
   long long* bsum;
   double* gparts;
   int64_t gram_parts_cap;     // doubles in gparts
-  double *G, *V;              // W_max^2 each
+  double *G, *V;              // W_max^2 each (left Gram path, W = r_{k-1} n_k <= 1024)
+  // right Gram path (W > 1024, at most kSpRightMax nonzero columns): dense M_k (Wr_max x Q),
+  // its Gram M_k^T M_k and eigenvectors (Q x Q), the selected eigenvectors / eigenvalues
+  int64_t Wr_max;             // max W over the right-path steps (0: none)
+  double *Md, *Gr, *Vr, *Vsel, *lam;
 };
+constexpr int kSpRightMax = 1024;
 int spectral_init_run(cudaStream_t s, const SpectralArgs& a, std::string* msg, int64_t* launches);
 
 // chains.cu: the per-sample chain path.

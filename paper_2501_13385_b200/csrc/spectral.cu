@@ -17,6 +17,12 @@
 //   * a_s <- a_s U_k(:, x_{s,k}, :).
 // The last core is M_d itself: C_d[a, x] = sum_{s: x_{s,d} = x} a_s[a] z_s.
 // Gram-based: the kept subspace is accurate to ~u ||G|| / gap (the singular values squared).
+// When W > 1024 (config 3's 16 x 256 = 4096 rows at k = 2) but M_k has at most 1024 nonzero
+// columns (the distinct suffixes q present in Omega; 128 there), the same subspace comes from
+// the other side: M_k is formed densely (W x Q, one entry per run), the Q x Q Gram M_k^T M_k is
+// diagonalised by the same Jacobi kernel, U = M_k V_r Lambda_r^{-1/2}, and U's columns are
+// re-orthonormalised (two modified Gram-Schmidt passes) so that the core is left-orthogonal to
+// rounding.
 #include <algorithm>
 #include <vector>
 
@@ -320,7 +326,7 @@ constexpr int kJT = 512;
 constexpr int kJU = 4;       // element pairs per thread per batch
 __global__ void __launch_bounds__(kJT) k_sp_jacobi(double* __restrict__ G, double* __restrict__ V, int W,
                                                    int r0, int nk, int r1, double* __restrict__ core,
-                                                   int max_sweeps) {
+                                                   int max_sweeps, double* __restrict__ lam = nullptr) {
   __shared__ double cs_c[512], cs_s[512];
   __shared__ int pp[512], qq[512];
   __shared__ int rot_any;
@@ -454,6 +460,76 @@ __global__ void __launch_bounds__(kJT) k_sp_jacobi(double* __restrict__ G, doubl
     const int a = row / nk, x = row - a * nk;
     core[((int64_t)a * nk + x) * r1 + c] = V[(int64_t)row * W + sel[c]];
   }
+  if (lam && tid < r1) lam[tid] = G[(int64_t)sel[tid] * W + sel[tid]];
+}
+
+// ---- right Gram path (W > 1024): M_k dense, row (a nk + x), column = group of the run
+__global__ void k_sp_dense_M(const int* __restrict__ rx, const int64_t* __restrict__ rgroup,
+                             const double* __restrict__ w, int64_t nruns, int cs, int r0, int nk, int64_t Q,
+                             double* __restrict__ M) {
+  const int64_t r = blockIdx.x * (int64_t)kT + threadIdx.x;
+  if (r >= nruns) return;
+  const int x = rx[r];
+  const int64_t q = rgroup[r];
+  for (int a = 0; a < r0; ++a) M[((int64_t)a * nk + x) * Q + q] = w[r * cs + a];
+}
+
+// G = M^T M (Q x Q), thread per entry, rows in order (fixed)
+__global__ void k_sp_gram_right(const double* __restrict__ M, int64_t W, int64_t Q, double* __restrict__ G) {
+  const int64_t e = blockIdx.x * (int64_t)kT + threadIdx.x;
+  if (e >= Q * Q) return;
+  const int64_t i = e / Q, j = e - i * Q;
+  double s = 0.0;
+  for (int64_t row = 0; row < W; ++row) s = fma(M[row * Q + i], M[row * Q + j], s);
+  G[e] = s;
+}
+
+// core[row][c] = sum_q M[row][q] Vsel[q][c] / sqrt(lam[c])   (U = M V_r Lambda_r^{-1/2})
+__global__ void k_sp_right_core(const double* __restrict__ M, const double* __restrict__ Vsel,
+                                const double* __restrict__ lam, int64_t W, int64_t Q, int r1,
+                                double* __restrict__ core) {
+  const int64_t e = blockIdx.x * (int64_t)kT + threadIdx.x;
+  if (e >= W * r1) return;
+  const int64_t row = e / r1;
+  const int c = (int)(e - row * r1);
+  double s = 0.0;
+  for (int64_t q = 0; q < Q; ++q) s = fma(M[row * Q + q], Vsel[q * r1 + c], s);
+  core[e] = lam[c] > 0.0 ? s / sqrt(lam[c]) : 0.0;
+}
+
+// two passes of modified Gram-Schmidt on the r1 columns (length W) of core [W][r1]; one CTA
+__global__ void __launch_bounds__(512) k_sp_mgs(double* __restrict__ core, int64_t W, int r1) {
+  __shared__ double red[512 / 32];
+  __shared__ double bc;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  auto dot = [&](int a, int b) {
+    double s = 0.0;
+    for (int64_t i = tid; i < W; i += 512) s = fma(core[i * r1 + a], core[i * r1 + b], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    __syncthreads();
+    if (lane == 0) red[wid] = s;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int i = 0; i < 512 / 32; ++i) t += red[i];
+      bc = t;
+    }
+    __syncthreads();
+    return bc;
+  };
+  for (int pass = 0; pass < 2; ++pass)
+    for (int c = 0; c < r1; ++c) {
+      for (int c2 = 0; c2 < c; ++c2) {
+        const double h = dot(c2, c);
+        for (int64_t i = tid; i < W; i += 512) core[i * r1 + c] = fma(-h, core[i * r1 + c2], core[i * r1 + c]);
+        __syncthreads();
+      }
+      const double nn = dot(c, c);
+      const double f = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+      for (int64_t i = tid; i < W; i += 512) core[i * r1 + c] *= f;
+      __syncthreads();
+    }
 }
 
 // a_t <- a_t U_k(:, x_{t,k}, :)
@@ -569,6 +645,23 @@ int spectral_init_run(cudaStream_t s, const SpectralArgs& A, std::string* msg, i
     cudaStreamSynchronize(s);
     k_sp_gstart<<<bl(nruns), kT, 0, s>>>(A.gflag, A.gidx, nruns, A.gstart);
     k_sp_rgroup<<<bl(nruns), kT, 0, s>>>(A.gidx, A.gflag, nruns, A.rgroup);
+    if (W > kSpRightMax) {   // right Gram path
+      if (ngroups > kSpRightMax || W > A.Wr_max || !A.Md) {
+        *msg = "spectral init: step " + std::to_string(k) + " has r_{k-1} n_k = " + std::to_string(W) +
+               " > 1024 rows and " + std::to_string(ngroups) + " nonzero columns (both above 1024)";
+        return TT_ERR_ARG;
+      }
+      const int64_t Q = ngroups;
+      cudaMemsetAsync(A.Md, 0, (size_t)W * Q * sizeof(double), s);
+      k_sp_dense_M<<<bl(nruns), kT, 0, s>>>(A.rx, A.rgroup, A.w, nruns, cs, r0, nk, Q, A.Md);
+      k_sp_gram_right<<<bl(Q * Q), kT, 0, s>>>(A.Md, W, Q, A.Gr);
+      k_sp_jacobi<<<1, kJT, 0, s>>>(A.Gr, A.Vr, (int)Q, 1, (int)Q, r1, A.Vsel, 40, A.lam);
+      k_sp_right_core<<<bl((int64_t)W * r1), kT, 0, s>>>(A.Md, A.Vsel, A.lam, W, Q, r1, core);
+      k_sp_mgs<<<1, 512, 0, s>>>(core, W, r1);
+      k_sp_chain<<<bl(m), kT, 0, s>>>(A.Ppos, A.Spre, m, D, k, core, r0, r1, A.chain, cs);
+      lc += 8;
+      continue;
+    }
     // runs of each x in group order: stable radix sort of the run indices by x, offsets by x
     k_sp_xkeys<<<bl(nruns), kT, 0, s>>>(A.rx, nruns, A.keys, A.vals);
     {

@@ -170,9 +170,11 @@ def test_adaptive_step_matches_oracle(pkg, cfg, m, eps_rule):
 
 
 # Spectral initialisation at scale: the GPU's sparse TT-SVD of
-# p^{-1} P_Omega(y) (Gram + Jacobi per mode, tt_spectral_init) against the oracle's dense
-# Alg. 1 (numpy SVD of the densified tensor) on shapes of configs 1, 2, 4, 5, 6.
+# p^{-1} P_Omega(y) (Gram + Jacobi per mode, tt_spectral_init; config 3's 4096-row unfolding by
+# the right Gram) against the oracle's dense Alg. 1 (numpy SVD of the densified tensor) on the
+# shapes of configs 1-6.
 @pytest.mark.parametrize("cfg,kw", [(1, {}), (2, dict(n=(20, 20, 20, 20), m=40_000)),
+                                    (3, dict(m=60_000)),    # full 256x256x128 shape: r_1 n_2 = 4096 rows
                                     (4, dict(n=(2,) * 14, m=3_000)),
                                     (5, dict(n=(6,) * 6, r=(1, 4, 4, 4, 4, 4, 1), m=20_000)),
                                     (6, {})])
@@ -261,8 +263,8 @@ def test_single_sample_and_matrix_case(pkg):
 def test_maximal_rank_and_rule_limits(pkg):
     # r = 32 = kMaxRank: rank-2r = 64 unfoldings exceed the cluster sweeps' S <= 32 and take
     # the single-CTA Householder path; the adaptive rule evaluates its denominator by
-    # per-sample chains of the rank-64 tangent TT (2r > 32); the spectral init refuses
-    # r_{k-1} n_k > 1024 with its documented status code (include/prgd.h).
+    # per-sample chains of the rank-64 tangent TT (2r > 32); the spectral init's third step
+    # (r_2 n_3 = 1280 > 1024 rows) takes the right-Gram path.
     rng = np.random.default_rng(21)
     n, r = (8, 40, 40, 8), (1, 8, 32, 8, 1)
     truth = [rng.standard_normal((r[k], n[k], r[k + 1])) / math.sqrt(r[k + 1]) for k in range(4)]
@@ -286,9 +288,8 @@ def test_maximal_rank_and_rule_limits(pkg):
         alpha = ctx.debug("eps")[2]
         assert abs(alpha - info["alpha"]) <= 1e-10 * info["alpha"], (alpha, info["alpha"])
         assert oracle.tt_diff_norm(ctx.get_cores(), T) <= 1e-10
-    with pytest.raises(pkg.PRGDError) as ei:
-        ctx.spectral_init()                       # r_1 n_2 = 320 ok, r_2 n_3 = 1280 > 1024
-    assert ei.value.code == pkg.TT_ERR_ARG
+    ctx.spectral_init()
+    assert oracle.tt_diff_norm(ctx.get_cores(), oracle.spectral_init(idx, y, n, r)) <= 1e-9
     ctx.close()
 
 
