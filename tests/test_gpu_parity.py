@@ -372,3 +372,38 @@ def test_weighted_retraction(pkg, cfg, m, path, steps):
     if steps == 1:
         assert oracle.tt_diff_norm(plain, T) > 1e-9      # the variant is a different iterate
     ctx.close()
+
+
+# Numeric faults (reading R6, include/prgd.h): tt_prgd_step is asynchronous, so a fault raised on
+# the device is reported by the next synchronising call as TT_ERR_NUMERIC, once (the flag is
+# cleared when read), and the faulting update leaves the iterate unchanged (noop).
+@pytest.mark.parametrize("path", ["tables", "chains"])
+def test_numeric_faults_reported_by_next_sync(pkg, path):
+    pr, y, init = problem(2, 20_000)
+    # NaN in an observed value: the residual is not finite
+    ybad = y.copy()
+    ybad[17] = np.nan
+    ctx = pkg.TTContext(pr.n, pr.r, path=path)
+    ctx.set_observations(pr.idx, ybad)
+    ctx.set_cores(init)
+    ctx.step(1.0)                                    # enqueued: no status yet
+    with pytest.raises(pkg.PRGDError) as ei:
+        ctx.sync()
+    assert ei.value.code == pkg.TT_ERR_NUMERIC
+    ctx.sync()                                       # reported once
+    for k in range(pr.d):
+        np.testing.assert_array_equal(ctx.get_core(k), init[k])
+    ctx.close()
+    # rank-deficient right Gram: a zero last core makes P_{d-1} = 0 (Cholesky breakdown)
+    zero = [c.copy() for c in init]
+    zero[-1][:] = 0.0
+    ctx = pkg.TTContext(pr.n, pr.r, path=path)
+    ctx.set_observations(pr.idx, y)
+    ctx.set_cores(zero)
+    ctx.step(1.0)
+    with pytest.raises(pkg.PRGDError) as ei:
+        ctx.residual_norm()
+    assert ei.value.code == pkg.TT_ERR_NUMERIC and "Cholesky" in str(ei.value)
+    got = ctx.get_cores()
+    assert all(np.array_equal(a, b) for a, b in zip(got, zero))
+    ctx.close()
