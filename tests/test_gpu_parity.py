@@ -407,3 +407,30 @@ def test_numeric_faults_reported_by_next_sync(pkg, path):
     got = ctx.get_cores()
     assert all(np.array_equal(a, b) for a, b in zip(got, zero))
     ctx.close()
+
+
+# Race detection by determinism (compute-sanitizer is closed on this GPU pool, profiles/
+# r02_sanitizer.md): every reduction of the library has a fixed order, so two independent runs of
+# the same steps must give bit-identical cores and residuals; a shared-memory or cluster race
+# would show up as run-to-run differences.
+@pytest.mark.parametrize("cfg,m,path,rule", [(2, 50_000, "tables", "theory"), (2, 50_000, "chains", "theory"),
+                                             (5, 200_000, "tables", "adaptive"), (4, 100_000, "tables", "theory"),
+                                             (3, 100_000, "tables", "theory")])
+def test_bitwise_deterministic(pkg, cfg, m, path, rule):
+    pr, y, init = problem(cfg, m)
+    outs = []
+    for rep in range(2):
+        ctx = pkg.TTContext(pr.n, pr.r, path=path)
+        ctx.set_observations(pr.idx, y)
+        ctx.set_cores(init)
+        ctx.set_metric("vee", 0.0, rule)
+        res = []
+        for _ in range(3):
+            ctx.step(0.5 if cfg == 3 else 1.0)
+            res.append(ctx.residual_norm())
+        outs.append((ctx.get_cores(), res, ctx.debug("resid")))
+        ctx.close()
+    (c0, r0, g0), (c1, r1, g1) = outs
+    assert r0 == r1
+    assert all(np.array_equal(a, b) for a, b in zip(c0, c1))
+    assert np.array_equal(g0, g1)
