@@ -73,7 +73,7 @@ def test_chain_buckets_eval_and_one_step(pkg, cfg, m, kw):
     ctx.close()
 
 
-@pytest.mark.parametrize("cfg,m", [(1, None), (2, 50_000), (4, 300_000), (6, None)])
+@pytest.mark.parametrize("cfg,m", [(1, None), (2, 50_000), (6, None)])   # cfg 3-5: test_gpu_parity_long
 def test_chain_many_steps(pkg, cfg, m):
     pr, y, init = problem(cfg, m)
     ctx = context(pkg, pr, y, init)

@@ -22,9 +22,13 @@ def pkg():
     return p
 
 
-@pytest.mark.parametrize("case", ["cfg3_full_50steps", "cfg4_full_50steps", "cfg5_4e6_50steps",
-                                  "cfg5_full_1step", "cfg5_full_50steps"])
-def test_golden_iterates(pkg, case):
+@pytest.mark.parametrize("case,path", [("cfg3_full_50steps", "tables"), ("cfg4_full_50steps", "tables"),
+                                       ("cfg5_4e6_50steps", "tables"), ("cfg5_full_1step", "tables"),
+                                       ("cfg5_full_50steps", "tables"),
+                                       # the per-sample chain path on the same references
+                                       ("cfg3_full_50steps", "chains"), ("cfg4_full_50steps", "chains"),
+                                       ("cfg5_4e6_50steps", "chains")])
+def test_golden_iterates(pkg, case, path):
     cfg, m, step, steps, keep = G.CASES[case]
     gold = G.load(case)                     # a missing file fails the test (no skip)
     pr = G.problem(cfg, m)
@@ -33,7 +37,7 @@ def test_golden_iterates(pkg, case):
     assert pr.m == gold["m"]
     assert abs(float(np.sum(y)) - gold["ysum"]) <= 1e-10 * np.sqrt(gold["ysq"] * pr.m)
     assert abs(float(np.dot(y, y)) - gold["ysq"]) <= 1e-12 * gold["ysq"]
-    ctx = pkg.TTContext(pr.n, pr.r)
+    ctx = pkg.TTContext(pr.n, pr.r, path=path)
     ctx.set_observations(pr.idx, y)
     ctx.set_cores(pr.init)
     res0 = ctx.residual_norm()
@@ -54,4 +58,4 @@ def test_golden_iterates(pkg, case):
             errs[it] = err
             assert err <= (1e-11 if it == 1 else 1e-8), (it, err)
     ctx.close()
-    print(f"{case}: relative errors {errs}")
+    print(f"{case} ({path}): relative errors {errs}")
