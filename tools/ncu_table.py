@@ -59,6 +59,8 @@ def group_of(seq):
         elif "k_tab" in k or "k_table" in k:
             g = "tables_U" if phase in ("orth", "tabU") else "tables_C"
             phase = "tabU" if phase in ("orth", "tabU") else "tabC"
+        elif "k_flat" in k:                        # pass A prefix (flat SDDMM + fix-up)
+            phase, nseg, g = "passA", 1, "passA_prefix"
         elif "k_seg" in k:
             if phase == "tabU" or phase == "passB":
                 if "k_seg_fix" not in k:
