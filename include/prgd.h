@@ -265,6 +265,13 @@ enum {
 };
 PRGD_API int tt_debug_get(tt_ctx* ctx, int what, int k, void* h_out, int64_t cap, int64_t* count);
 
+/* Test hook for A14 alone: upload a rank-2r block TT h_B (count doubles, the layout the step
+ * assembles: core k is [R_k][n_k][R_{k+1}] with R_0 = R_d = 1 and R_k = 2 r_k otherwise, cores
+ * concatenated) and run only the TT-rounding SVD_r^tt (Alg. 1 as TT-rounding)
+ * into the context's cores (read them with tt_get_core).  Synchronous; TT_ERR_ARG on a count
+ * mismatch, TT_ERR_NUMERIC if the rounding reports a fault. */
+PRGD_API int tt_debug_round(tt_ctx* ctx, const double* h_B, int64_t count);
+
 #ifdef __cplusplus
 }
 #endif

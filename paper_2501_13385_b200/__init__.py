@@ -88,6 +88,7 @@ def load() -> ctypes.CDLL:
                                           ctypes.POINTER(ctypes.c_int), i64p]),
         "tt_profile_name": (ctypes.c_char_p, [ctypes.c_int]),
         "tt_debug_get": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, ctypes.c_int64, i64p]),
+        "tt_debug_round": (ctypes.c_int, [P, P, ctypes.c_int64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -300,6 +301,13 @@ class TTContext:
         self._check(self.lib.tt_debug_get(self._h, code, k, _ptr(out), out.shape[0],
                                           ctypes.byref(cnt)), f"tt_debug_get({what})")
         return out[:cnt.value]
+
+    def debug_round(self, blocks):
+        """Round a rank-2r block TT (list of cores [R_k, n_k, R_{k+1}], R = 2r inside) with the
+        library's A14 kernels into the context's cores (tt_debug_round; tests only)."""
+        flat = np.ascontiguousarray(np.concatenate([np.ascontiguousarray(b, dtype=np.float64).ravel()
+                                                    for b in blocks]))
+        self._check(self.lib.tt_debug_round(self._h, _ptr(flat), flat.shape[0]), "tt_debug_round")
 
     def _debug_size(self, code, k):
         if code in (1, 3, 5, 13):

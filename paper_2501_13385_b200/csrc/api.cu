@@ -1587,6 +1587,27 @@ const char* tt_profile_name(int group) {
   return kGroupNames[group];
 }
 
+int tt_debug_round(tt_ctx* ctx, const double* h_B, int64_t count) {
+  if (!ctx || !h_B) return TT_ERR_ARG;
+  int rc = ensure_base(ctx);
+  if (rc) return rc;
+  if (count != ctx->b_off[ctx->d]) return fail(ctx, TT_ERR_ARG, "count must equal the rank-2r block size");
+  cudaStream_t s = ctx->stream;
+  CK(cudaStreamSynchronize(s));
+  CK(cudaMemcpyAsync(ctx->B, h_B, (size_t)count * sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(&ctx->sc->noop, 0, sizeof(int), s));
+  DenseArgs da = dense_args(ctx);
+  da.wretr = 0;
+  int64_t lc = 0;
+  launch_round_only(s, da, &lc);
+  ctx->launches += lc;
+  CK(cudaGetLastError());
+  for (auto& c : ctx->core_set) c = 1;
+  ctx->evalValid = false;
+  ctx->tablesC = false;
+  return read_scalars(ctx);
+}
+
 int tt_debug_get(tt_ctx* ctx, int what, int k, void* h_out, int64_t cap, int64_t* count) {
   if (!ctx || !h_out || !count) return TT_ERR_ARG;
   int rc = ensure_base(ctx);

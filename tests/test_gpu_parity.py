@@ -434,3 +434,42 @@ def test_bitwise_deterministic(pkg, cfg, m, path, rule):
     assert r0 == r1
     assert all(np.array_equal(a, b) for a, b in zip(c0, c1))
     assert np.array_equal(g0, g1)
+
+
+# A14 alone (tt_debug_round) on constructed rank-2r block TTs whose bond-1 spectrum is known: the
+# kept group ends in a weak direction (0.3) just above the discarded group (0.25 / 0.299), so the
+# cluster truncation's norm-ordered split is not the answer from the start (the
+# cross-angle exit of the one-sided Jacobi must not certify a wrong split).  d = 3,
+# n = (20, 10, 16), r = (1, 8, 8, 1): B_0 = U diag(sigma) (U orthonormal 20 x 16), B_1 B_2 an
+# orthonormal right part, so W^<1> = U diag(sigma) Q^T exactly.  Against the oracle's
+# numpy-SVD TT-rounding (Alg. 1), tensors compared.
+@pytest.mark.parametrize("gap", [0.05, 1e-3])
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 4])
+def test_rounding_weak_kept_direction(pkg, gap, seed):
+    rng = np.random.default_rng(100 + seed)
+    n, r = (20, 10, 16), (1, 8, 8, 1)
+    kept = np.array([5.0, 4.5, 4.0, 3.5, 3.0, 2.5, 2.0, 0.3])
+    disc = np.array([0.3 - gap, 0.2, 0.1, 0.05, 1e-3, 1e-4, 1e-6, 1e-8])
+    sig = np.concatenate([kept, disc])[rng.permutation(16)]
+    U, _ = np.linalg.qr(rng.standard_normal((20, 16)))
+    Q, _ = np.linalg.qr(rng.standard_normal((10 * 16, 16)))
+    B0 = (U * sig[None, :])[None, :, :]                       # [1][20][16]
+    B1 = Q.T.reshape(16, 10, 16)                              # [16][10][16]
+    B2 = np.eye(16)[:, :, None]                               # [16][16][1]
+    ref = oracle.tt_round([B0, B1, B2], r)
+    ctx = pkg.TTContext(n, r)
+    e0 = ctx.debug("eps")
+    ctx.debug_round([B0, B1, B2])
+    got = ctx.get_cores()
+    e1 = ctx.debug("eps")
+    err = oracle.tt_diff_norm(got, ref)
+    assert err <= 1e-11, (err, e1[4] - e0[4])
+    np.testing.assert_allclose(got[0].reshape(20, 8).T @ got[0].reshape(20, 8), np.eye(8), atol=1e-12)
+    # bond 1 kept exactly the kept singular directions: the first core spans U's kept columns
+    Uk = U[:, np.isin(sig, kept)]
+    P0 = got[0].reshape(20, 8)
+    np.testing.assert_allclose(np.linalg.svd(Uk.T @ P0, compute_uv=False), np.ones(8), atol=1e-12)
+    print(f"seed {seed} gap {gap}: err {err:.2e}, Jacobi sweeps {int(e1[4] - e0[4])}, "
+          f"cross {int(e1[5 + 14] - e0[5 + 14])}, full {int(e1[5 + 19] - e0[5 + 19])}, "
+          f"cert failures {int(e1[5 + 17] - e0[5 + 17])}")
+    ctx.close()
