@@ -26,18 +26,14 @@ constexpr unsigned kFull = 0xffffffffu;
 struct SegDev {
   int64_t nwarps;
   int64_t warp_off;       // first plan warp of this launch
-  int64_t nrow_real;      // table rows: virtual row v -> table row v % nrow_real
-  int accum;              // SpMM: add into out (gather blocks after the first)
   const int4* vrow;       // {row, count, first sample, partial slot} per virtual row
   const int64_t* warp_vbegin;
   double* part;
   int ld;
   const int32_t* col;
   const int32_t* perm;
-  const double* y;
   double* g;
-  double* g2;             // SDDMM: g also scattered to g2[perm2[s]]; GSQ: gathered g stored to g2[s]
-  const int32_t* perm2;
+  double* g2;             // GSQ: the gathered g stored to g2[s] (suffix order)
   const double* rowtab;
   const double* coltab;
   const double* rowtab2;  // DPASS second row / gathered tables
@@ -64,8 +60,7 @@ __device__ __forceinline__ double2 ld2(const double* p) {
 #endif
 template <int MODE>
 struct SegOcc {
-  static constexpr int v = (MODE == kSDDMM || MODE == kDPASS) ? PRGD_SEG_OCC_SDDMM
-                                                             : (MODE == kSPMM ? PRGD_SEG_OCC_SPMM : 8);
+  static constexpr int v = MODE == kDPASS ? PRGD_SEG_OCC_SDDMM : (MODE == kSPMM ? PRGD_SEG_OCC_SPMM : 8);
 };
 
 // LPS lanes per sample, each holding V double2 of the row (ld = 2 LPS V)
@@ -86,14 +81,14 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
   for (int64_t v = v0; v < v1; ++v) {
     const int4 vr = a.vrow[v];
     const int32_t row = vr.x;
-    const int64_t trow = row < a.nrow_real ? row : row % a.nrow_real;   // gather blocks only
+    const int64_t trow = row;
     const int64_t beg = vr.z;
     const int cnt = vr.y;
     double2 rv[V], rv2[V];
 #pragma unroll
     for (int q = 0; q < V; ++q) {
       rv[q] = rv2[q] = make_double2(0.0, 0.0);
-      if (MODE == kSDDMM || MODE == kDPASS) rv[q] = ld2(a.rowtab + trow * ld + 2 * (V * sub + q));
+      if (MODE == kDPASS) rv[q] = ld2(a.rowtab + trow * ld + 2 * (V * sub + q));
       if (MODE == kDPASS) rv2[q] = ld2(a.rowtab2 + trow * ld + 2 * (V * sub + q));
     }
     double accs = 0.0;
@@ -105,22 +100,17 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
       const int64_t s = beg + c0 + lane;
       const bool have = lane < nc;
       // lane-parallel loads of this chunk's per-sample data (coalesced / independent)
-      int colv = 0, p2v = 0;
-      double xv = 0.0;    // y (SDDMM) or g (GSQ, SPMM)
+      int colv = 0;
+      double xv = 0.0;    // g (GSQ, SPMM)
       if (have) {
         if (MODE != kGSQ) colv = a.col[s];
-        if (MODE == kSDDMM) {
-          xv = a.y[s];
-          if (a.g2) p2v = a.perm2[s];
-        } else if (MODE != kDPASS) {
-          xv = a.perm ? a.g[a.perm[s]] : a.g[s];
-        }
+        if (MODE != kDPASS) xv = a.perm ? a.g[a.perm[s]] : a.g[s];
       }
       if constexpr (MODE == kGSQ) {
         if (have && a.g2) a.g2[s] = xv;
         accs = fma(xv, xv, accs);
         continue;
-      } else if constexpr (MODE == kSDDMM || MODE == kDPASS) {
+      } else if constexpr (MODE == kDPASS) {
         // partial dot products of the chunk's STEPS samples of this lane group, then a
         // transpose-reduction over the group's LPS lanes (LPS - 1 shuffles for LPS samples
         // instead of log2(LPS) per sample): afterwards lane `sub` holds the dot product of
@@ -165,16 +155,7 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
           }
         }
         const int t = sub * G + grp;
-        if constexpr (MODE == kSDDMM) {
-          const double yv = __shfl_sync(kFull, xv, t & 31);
-          const int p2 = a.g2 ? __shfl_sync(kFull, p2v, t & 31) : 0;
-          if (t < nc) {
-            const double gv = pd[0] - yv;
-            a.g[beg + c0 + t] = gv;
-            if (a.g2) a.g2[p2] = gv;
-            accs = fma(gv, gv, accs);
-          }
-        } else {
+        {
           if (t < nc) accs = fma(pd[0], pd[0], accs);
         }
       } else {
@@ -211,7 +192,7 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
         if (pslot < 0) a.out[row] = accs;
         else a.part[pslot] = accs;
       }
-    } else if (MODE == kSDDMM || MODE == kDPASS) {
+    } else if (MODE == kDPASS) {
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) accs += __shfl_xor_sync(kFull, accs, o);   // every lane holds samples
       if (lane == 0) {
@@ -235,11 +216,6 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
           for (int q = 0; q < V; ++q) {
             accv[q].x *= f;
             accv[q].y *= f;
-            if (a.accum) {
-              const double2 o = *reinterpret_cast<const double2*>(dst + 2 * q);
-              accv[q].x += o.x;
-              accv[q].y += o.y;
-            }
           }
         } else {
           dst = a.part + (int64_t)pslot * ld + 2 * V * sub;
@@ -252,26 +228,23 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
 }
 
 // Sum the partial slots of split buckets in slot order.
-__global__ void k_seg_fix(int vec, int64_t s0, int64_t nsplit, const int32_t* __restrict__ split_row,
+__global__ void k_seg_fix(int vec, int64_t nsplit, const int32_t* __restrict__ split_row,
                           const int64_t* __restrict__ split_first, const double* __restrict__ part,
                           int ld, const double* __restrict__ rowscale, double* __restrict__ out,
-                          int64_t nrow_real, int accum, const Scalars* sc) {
+                          const Scalars* sc) {
   if (sc && sc->noop) return;
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int w = vec ? ld : 1;
   int64_t i = e / w;
   int c = (int)(e - i * w);
   if (i >= nsplit) return;
-  i += s0;
   const int32_t row = split_row[i];
   double acc = 0.0;
   for (int64_t sl = split_first[i]; sl < split_first[i + 1]; ++sl)
     acc += vec ? part[sl * ld + c] : part[sl];
   if (vec) {
-    const int64_t trow = row % nrow_real;
-    if (rowscale) acc *= rowscale[trow];
-    double* dst = out + trow * ld + c;
-    *dst = accum ? *dst + acc : acc;
+    if (rowscale) acc *= rowscale[row];
+    out[(int64_t)row * ld + c] = acc;
   } else {
     out[row] = acc;
   }
@@ -483,18 +456,14 @@ void launch_seg(cudaStream_t s, const SegArgs& a, const Scalars* sc, int64_t* la
   SegDev dv;
   dv.nwarps = p.nwarps;
   dv.warp_off = 0;
-  dv.nrow_real = p.nrow_real > 0 ? p.nrow_real : p.nrows;
-  dv.accum = 0;
   dv.vrow = p.vrow;
   dv.warp_vbegin = p.warp_vbegin;
   dv.part = p.part;
   dv.ld = a.ld;
   dv.col = a.col;
   dv.perm = a.perm;
-  dv.y = a.y;
   dv.g = a.g;
   dv.g2 = a.g2;
-  dv.perm2 = a.perm2;
   dv.rowtab = a.rowtab;
   dv.coltab = a.coltab;
   dv.rowtab2 = a.rowtab2;
@@ -502,34 +471,20 @@ void launch_seg(cudaStream_t s, const SegArgs& a, const Scalars* sc, int64_t* la
   dv.rowscale = a.rowscale;
   dv.out = a.out;
   const int vec = a.mode == kSPMM ? 1 : 0;
-  // SpMM outputs are table rows shared by all gather blocks: one launch per block, the later
-  // ones accumulating (launch order = fixed summation order).  Scalar outputs are per virtual
-  // row: one launch.
-  const int nb = (vec && p.nblk > 1) ? p.nblk : 1;
-  for (int b = 0; b < nb; ++b) {
-    const int64_t w0 = nb > 1 ? p.blk_warp[b] : 0, w1 = nb > 1 ? p.blk_warp[b + 1] : p.nwarps;
-    const int64_t s0 = nb > 1 ? p.blk_split[b] : 0, s1 = nb > 1 ? p.blk_split[b + 1] : p.nsplit;
-    dv.warp_off = w0;
-    dv.nwarps = w1 - w0;
-    dv.accum = b > 0 ? 1 : 0;
-    if (dv.nwarps > 0) {
-      unsigned grid = blocks_for(dv.nwarps * 32, 256);
-      switch (a.ld / 2) {
-        case 1: seg_dispatch_mode<1>(s, a.mode, dv, grid, sc); break;
-        case 2: seg_dispatch_mode<2>(s, a.mode, dv, grid, sc); break;
-        case 4: seg_dispatch_mode<4>(s, a.mode, dv, grid, sc); break;
-        case 8: seg_dispatch_mode<8>(s, a.mode, dv, grid, sc); break;
-        default: seg_dispatch_mode<16>(s, a.mode, dv, grid, sc); break;
-      }
-      ++*launches;
-    }
-    if (s1 > s0) {
-      int64_t n = (s1 - s0) * (vec ? a.ld : 1);
-      k_seg_fix<<<blocks_for(n, 256), 256, 0, s>>>(vec, s0, s1 - s0, p.split_row, p.split_first,
-                                                   p.part, a.ld, a.rowscale, a.out, dv.nrow_real,
-                                                   dv.accum, sc);
-      ++*launches;
-    }
+  const unsigned grid = blocks_for(dv.nwarps * 32, 256);
+  switch (a.ld / 2) {
+    case 1: seg_dispatch_mode<1>(s, a.mode, dv, grid, sc); break;
+    case 2: seg_dispatch_mode<2>(s, a.mode, dv, grid, sc); break;
+    case 4: seg_dispatch_mode<4>(s, a.mode, dv, grid, sc); break;
+    case 8: seg_dispatch_mode<8>(s, a.mode, dv, grid, sc); break;
+    default: seg_dispatch_mode<16>(s, a.mode, dv, grid, sc); break;
+  }
+  ++*launches;
+  if (p.nsplit > 0) {
+    const int64_t n = p.nsplit * (vec ? a.ld : 1);
+    k_seg_fix<<<blocks_for(n, 256), 256, 0, s>>>(vec, p.nsplit, p.split_row, p.split_first, p.part, a.ld,
+                                                 a.rowscale, a.out, sc);
+    ++*launches;
   }
 }
 

@@ -188,18 +188,16 @@ void launch_backward_levels(cudaStream_t s, const std::vector<BackwardLevel>& le
 void levels_init();
 
 // passes.cu
-enum SegMode { kSDDMM = 0, kGSQ = 1, kSPMM = 2, kDPASS = 3 };
+enum SegMode { kGSQ = 1, kSPMM = 2, kDPASS = 3 };   // (pass A's SDDMM: passes_flat.cu)
 struct SegArgs {
   const SegPlan* plan;  // host copy (device pointers inside)
   int mode;
   int ld;               // row stride of the tables / outputs (pad(r))
   const int32_t* col;   // per-sample column / gather index (SDDMM, SPMM)
   const int32_t* perm;  // per-sample index into g (GSQ, SPMM suffix side) or null
-  const double* y;      // SDDMM
   double* g;            // SDDMM writes, GSQ/SPMM read
-  double* g2 = nullptr;         // SDDMM: also writes g2[perm2[s]] (g in the other order)
-  const int32_t* perm2 = nullptr;
-  const double* rowtab; // SDDMM row vectors
+  double* g2 = nullptr;         // GSQ: the gathered g stored to g2[s]
+  const double* rowtab; // DPASS row vectors
   const double* coltab; // gathered table
   const double* rowtab2 = nullptr;  // DPASS: v_s = rowtab.coltab + rowtab2.coltab2
   const double* coltab2 = nullptr;
