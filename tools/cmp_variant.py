@@ -1,0 +1,39 @@
+"""Compare the iterates of two library builds bit for bit (diagnostic):
+    python tools/cmp_variant.py libA.so libB.so cfg [m] [steps]"""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if len(sys.argv) > 1 and sys.argv[1] == "--run":
+    sys.path.insert(0, ROOT)
+    import numpy as np
+    import paper_2501_13385_b200 as pkg
+    import synth
+    cfg, m, steps, out = int(sys.argv[2]), (int(sys.argv[3]) or None), int(sys.argv[4]), sys.argv[5]
+    pr = synth.make_problem(cfg, m=m)
+    t = pkg.TTContext(pr.n, pr.r)
+    t.set_cores(pr.truth)
+    y = pr.observations(t.eval_at(pr.idx))
+    t.close()
+    ctx = pkg.TTContext(pr.n, pr.r)
+    ctx.set_observations(pr.idx, y)
+    ctx.set_cores(pr.init if pr.init is not None else pr.truth)
+    for _ in range(steps):
+        ctx.step(0.5 if cfg == 3 else 1.0)
+    np.savez(out, *ctx.get_cores(), res=ctx.residual_norm())
+    sys.exit(0)
+a, b, cfg = sys.argv[1], sys.argv[2], sys.argv[3]
+m = sys.argv[4] if len(sys.argv) > 4 else "0"
+steps = sys.argv[5] if len(sys.argv) > 5 else "3"
+import numpy as np  # noqa: E402
+outs = []
+for lib, tag in ((a, "a"), (b, "b")):
+    f = f"/tmp/cmp_{tag}.npz"
+    subprocess.run([sys.executable, __file__, "--run", cfg, m, steps, f], check=True,
+                   env=dict(os.environ, PRGD_LIB_PATH=lib))
+    outs.append(np.load(f))
+za, zb = outs
+same = all(np.array_equal(za[k], zb[k]) for k in za.files)
+diff = max(float(np.max(np.abs(za[k] - zb[k]))) for k in za.files)
+print(f"cfg {cfg}: bitwise identical {same}, max abs diff {diff:.3e}")
