@@ -45,9 +45,12 @@ class PairAllreduce:
         return call
 
 
-@pytest.mark.parametrize("cfg,m,steps,rule", [(2, 20000, 3, "theory"), (5, 60000, 2, "theory"),
-                                              (2, 20000, 2, "adaptive")])
-def test_sharded_two_contexts_match_oracle(cfg, m, steps, rule):
+@pytest.mark.parametrize("cfg,m,steps,rule,path", [(2, 20000, 3, "theory", "tables"),
+                                                   (5, 60000, 2, "theory", "tables"),
+                                                   (2, 20000, 2, "adaptive", "tables"),
+                                                   (2, 20000, 3, "theory", "chains"),
+                                                   (2, 20000, 2, "adaptive", "chains")])
+def test_sharded_two_contexts_match_oracle(cfg, m, steps, rule, path):
     import paper_2501_13385_b200 as pkg
     pkg.load()
     pr = synth.make_problem(cfg, m=m)
@@ -57,7 +60,7 @@ def test_sharded_two_contexts_match_oracle(cfg, m, steps, rule):
     ar = PairAllreduce()
     ctxs = []
     for rank in range(2):
-        c = pkg.TTContext(pr.n, pr.r)
+        c = pkg.TTContext(pr.n, pr.r, path=path)
         c.set_metric("vee", 0.0, rule)
         c.set_allreduce(ar.fn(rank), pr.m)
         c.set_observations(pr.idx[rank::2], y[rank::2])
