@@ -140,6 +140,8 @@ struct tt_ctx {
   int* n_dev = nullptr;
   double *C = nullptr, *U = nullptr, *Y = nullptr, *Ahat = nullptr, *phi = nullptr, *h = nullptr;
   double *P = nullptr, *L = nullptr, *B = nullptr, *work = nullptr, *clw = nullptr;
+  double* vwarm = nullptr;   // truncation Jacobi warm starts (k_round_cs), [2][d][32*32]
+  int* wok = nullptr;
   int64_t clw_len = 0;
   int64_t work_len = 0;
   std::vector<int64_t> core_off, phi_off, b_off, p_off;
@@ -321,7 +323,8 @@ int ensure_base(tt_ctx* ctx) {
             A(ctx, &ctx->h, ctx->phi_off[d], L) && A(ctx, &ctx->P, ctx->p_off[d], L) &&
             A(ctx, &ctx->L, ctx->p_off[d], L) && A(ctx, &ctx->B, ctx->b_off[d], L) &&
             A(ctx, &ctx->work, ctx->work_len, L) && A(ctx, &ctx->clw, ctx->clw_len, L) &&
-            A(ctx, &ctx->sc, 1, L);
+            A(ctx, &ctx->sc, 1, L) && A(ctx, &ctx->vwarm, 2 * (int64_t)d * 1024, L) &&
+            A(ctx, &ctx->wok, 2 * d, L);
   if (!ok) return fail(ctx, TT_ERR_OOM, "device allocation failed (base buffers)");
   // chain-path view of the cores (and of the rank-2r block cores for the adaptive step)
   ctx->ctt = ChainTT{};
@@ -345,6 +348,7 @@ int ensure_base(tt_ctx* ctx) {
     CK(cudaMemsetAsync(ctx->C, 0, ctx->core_off[d] * sizeof(double), ctx->stream));
     CK(cudaMemsetAsync(ctx->sc, 0, sizeof(Scalars), ctx->stream));
     CK(cudaMemsetAsync(ctx->h, 0, ctx->phi_off[d] * sizeof(double), ctx->stream));
+    CK(cudaMemsetAsync(ctx->wok, 0, 2 * d * sizeof(int), ctx->stream));
     dense_init();
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->base_ready = true;
@@ -386,6 +390,7 @@ int ensure_base(tt_ctx* ctx) {
   CK(cudaMemsetAsync(ctx->C, 0, ctx->core_off[d] * sizeof(double), ctx->stream));
   CK(cudaMemsetAsync(ctx->sc, 0, sizeof(Scalars), ctx->stream));
   CK(cudaMemsetAsync(ctx->h, 0, ctx->phi_off[d] * sizeof(double), ctx->stream));
+  CK(cudaMemsetAsync(ctx->wok, 0, 2 * d * sizeof(int), ctx->stream));
   dense_init();
   tables_init();
   levels_init();
@@ -421,6 +426,8 @@ DenseArgs dense_args(tt_ctx* ctx) {
   a.sc = ctx->sc;
   a.smem_doubles = dense_smem_doubles();
   a.wretr = ctx->retraction == TT_RETRACT_WEIGHTED ? 1 : 0;
+  a.vwarm = ctx->vwarm;
+  a.wok = ctx->wok;
   return a;
 }
 

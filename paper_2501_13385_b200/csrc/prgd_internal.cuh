@@ -38,6 +38,7 @@ struct Scalars {
   long long cyc[24]; // cumulative SM cycles / counters per dense phase (diagnostic)
   double adapt_num[kMaxD];  // adaptive step: ||component k of the tangent vector||_W^2
   double adapt_den;         // adaptive step: ||P_Omega D||^2 (this rank's samples)
+  int wpar;                 // parity of the rounding's warm-start buffers (DenseArgs::vwarm)
 };
 
 enum ErrBits { kErrNaN = 1, kErrChol = 2, kErrSVD = 4 };
@@ -86,6 +87,8 @@ struct DenseArgs {
   int smem_doubles;  // dynamic shared memory available to the kernel, in doubles
   int proj_mode;     // k_project: 0 project + assemble, 1 project + adaptive numerator, 2 assemble
   int wretr;         // 1: weighted retraction W^{-1/2} SVD_r^tt W^{1/2}
+  double* vwarm;     // [2][d][32*32] the truncation Jacobi's last rotation per bond (warm start) or null
+  int* wok;          // [2][d] 1: the slot holds a converged rotation
 };
 
 // ------------------------------------------------------------------ kernels (launchers)

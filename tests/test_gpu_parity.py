@@ -130,7 +130,9 @@ def test_many_steps_parity(pkg, cfg, m, steps):
     assert err <= 1e-8, err
     res = ctx.residual_norm()
     ref = float(np.linalg.norm(oracle.residual(T, pr.idx, y)))
-    assert abs(res - ref) <= 1e-8 * max(ref, 1e-300) + 1e-14 * np.linalg.norm(y)
+    # relative 1e-8 plus a floor for residuals converged to rounding noise (config 4); the
+    # iterate bar implies |res_gpu - res_orc| <~ 1e-8 ||y||
+    assert abs(res - ref) <= 1e-8 * max(ref, 1e-300) + 1e-10 * np.linalg.norm(y)
     ctx.close()
 
 
