@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -268,6 +269,30 @@ struct PhaseTimer {
   }
 };
 
+// Pinned host copies of the device scalars, recycled across contexts (cudaMallocHost costs about
+// a millisecond per call; contexts are created per problem, e.g. every end-to-end run).
+std::mutex g_pin_mu;
+std::vector<Scalars*> g_pin_free;
+
+Scalars* pinned_scalars_get() {
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (!g_pin_free.empty()) {
+      Scalars* p = g_pin_free.back();
+      g_pin_free.pop_back();
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaMallocHost(&p, sizeof(Scalars)) != cudaSuccess) return nullptr;
+  return static_cast<Scalars*>(p);
+}
+
+void pinned_scalars_put(Scalars* p) {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_free.push_back(p);
+}
+
 template <class T>
 bool A(tt_ctx* ctx, T** out, int64_t count, std::vector<void*>& list) {
   *out = static_cast<T*>(dalloc(ctx, (size_t)std::max<int64_t>(count, 1) * sizeof(T), list));
@@ -341,7 +366,7 @@ int ensure_base(tt_ctx* ctx) {
   }
   for (int k = 0; k < d; ++k) ctx->ctt.n[k] = ctx->dtt.n[k] = (int)ctx->n[k];
   if (ctx->plan.chain) {
-    if (cudaMallocHost(&ctx->sc_host, sizeof(Scalars)) != cudaSuccess)
+    if (!(ctx->sc_host = pinned_scalars_get()))
       return fail(ctx, TT_ERR_OOM, "pinned allocation failed");
     std::memset(ctx->sc_host, 0, sizeof(Scalars));
     CK(cudaMemcpyAsync(ctx->n_dev, ctx->n_i.data(), d * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
@@ -383,7 +408,7 @@ int ensure_base(tt_ctx* ctx) {
   }
   ctx->Ypart_cap = ycap;
   if (!A(ctx, &ctx->Ypart, ycap, L)) return fail(ctx, TT_ERR_OOM, "device allocation failed (Y)");
-  if (cudaMallocHost(&ctx->sc_host, sizeof(Scalars)) != cudaSuccess)
+  if (!(ctx->sc_host = pinned_scalars_get()))
     return fail(ctx, TT_ERR_OOM, "pinned allocation failed");
   std::memset(ctx->sc_host, 0, sizeof(Scalars));
   CK(cudaMemcpyAsync(ctx->n_dev, ctx->n_i.data(), d * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
@@ -1142,8 +1167,10 @@ int tt_create(int d, const int64_t* n, const int64_t* r, tt_ctx** out) {
   }
   int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceProp prop;
-  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess || prop.major != 10 || prop.minor != 0)
+  int major = 0, minor = 0;   // (cudaGetDeviceProperties costs milliseconds per call)
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess ||
+      major != 10 || minor != 0)
     return TT_ERR_CUDA;
   tt_ctx* ctx = new tt_ctx();
   ctx->d = d;
@@ -1170,7 +1197,7 @@ int tt_destroy(tt_ctx* ctx) {
   drop_graphs(ctx);
   dfree_all(ctx, ctx->obs_allocs);
   dfree_all(ctx, ctx->base_allocs);
-  if (ctx->sc_host) cudaFreeHost(ctx->sc_host);
+  if (ctx->sc_host) pinned_scalars_put(ctx->sc_host);
   if (ctx->ev_ready)
     for (auto& e : ctx->ev) cudaEventDestroy(e);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
