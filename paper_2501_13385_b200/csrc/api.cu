@@ -851,6 +851,15 @@ int run_piece(tt_ctx* ctx, int piece) {
     return TT_OK;
   }
   if (!*ge) {
+    // First use: enqueue the piece directly (the GPU starts on it at once), then capture and
+    // instantiate its graph on the host while the GPU runs it; later calls launch the graph.
+    {
+      int64_t lc = 0;
+      enqueue(&lc);
+      ctx->launches += lc;
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
+    }
     // capture on a private stream (the launch stream may be shared with other contexts /
     // threads), launch on ctx->stream
     if (!ctx->cap) CK(cudaStreamCreateWithFlags(&ctx->cap, cudaStreamNonBlocking));
@@ -871,6 +880,7 @@ int run_piece(tt_ctx* ctx, int piece) {
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "graph instantiate");
     *nl = lc;
+    return TT_OK;
   }
   CK(cudaGraphLaunch(*ge, ctx->stream));
   ctx->launches += *nl;
