@@ -98,6 +98,18 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def chain_models(pr):
+    """Per-step FP64 work of the chain path's groups (SURVEY §8(d) per-sample flop model, App. X.4):
+    pass A = sum_{k>=2} 2 r_{k-1} r_k + 1 per sample (the left chain), interfaces = both chains,
+    contraction = sum_k 2 r_{k-1} r_k per sample; h = d adds per sample."""
+    m, d, r = pr.m, pr.d, pr.r
+    chain = sum(2.0 * r[k - 1] * r[k] for k in range(2, d + 1))
+    contr = sum(2.0 * r[k] * r[k + 1] for k in range(d))
+    return {"passA_prefix": ("fp64", m * (chain + 1), "flop"), "marginals": ("fp64", m * d, "flop"),
+            "passB_prefix": ("fp64", m * 2 * chain, "flop"), "backward_Y": ("fp64", m * contr, "flop"),
+            "dense_orth": group_models(pr, 1, 1, 1)["dense_orth"], "dense_round": group_models(pr, 1, 1, 1)["dense_round"]}
+
+
 def group_models(pr, KL, NL, NR):
     """Algorithmic work of one launch of each kernel group per step: compulsory
     DRAM bytes for the HBM-bound groups (streamed per-sample arrays + each table row read once +
@@ -188,8 +200,10 @@ def run_ours(args, rank, ws, dist):
         # sharded Omega: same truth and init on every rank, disjoint samples
         pr = synth.make_problem(args.config, m=args.m, rank=rank, world=ws)
     else:
-        pr = synth.make_problem(args.config, m=args.m)
-    if args.rank:
+        nov = tuple(int(x) for x in args.n_override.split(",")) if args.n_override else None
+        rov = ((1,) + (args.rank,) * (len(nov) - 1) + (1,)) if (nov and args.rank) else None
+        pr = synth.make_problem(args.config, m=args.m, n=nov, r=rov)
+    if args.rank and not args.n_override:
         # diagnostic only: the same Omega with every interior TT rank set to
         # args.rank (truth and init truncated), e.g. r = 1 for the HBM-bound shape of the passes
         pr.r = (1,) + (args.rank,) * (pr.d - 1) + (1,)
@@ -219,12 +233,13 @@ def run_ours(args, rank, ws, dist):
         sctx.close()
     KL, NL, NR = pkg.plan(pr.n, pr.r)
 
-    ctx = pkg.TTContext(pr.n, pr.r)
+    ctx = pkg.TTContext(pr.n, pr.r, path=args.path)
     if args.step_rule != "theory":
         ctx.set_metric("vee", 0.0, args.step_rule)
     if ar is not None:
         ctx.set_allreduce(ar, m_global)
     stream = ctx.stream
+    path = ctx.path
     t1 = time.perf_counter()
     ctx.set_observations(pr.idx, y)
     t_setobs = time.perf_counter() - t1
@@ -276,7 +291,7 @@ def run_ours(args, rank, ws, dist):
     ctx.set_profiling(False)
     ctx.close()
 
-    out = dict(pr=pr, y=y, init=init, KL=KL, NL=NL, NR=NR, ms=ms_max, launches=launches,
+    out = dict(pr=pr, y=y, init=init, KL=KL, NL=NL, NR=NR, ms=ms_max, launches=launches, path=path,
                m_global=m_global,
                clocks=clocks, prof=prof, t_gen=t_gen, t_setobs=t_setobs, res0=res0, res1=res1,
                dense_diag=dense_diag)
@@ -384,6 +399,10 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--m", type=int, default=None, help="override |Omega| draws (debug only)")
+    ap.add_argument("--path", choices=["auto", "tables", "chains"], default="auto",
+                    help="path over Omega (tt_set_path); auto = tables when they fit")
+    ap.add_argument("--n-override", type=str, default=None,
+                    help="diagnostic: comma-separated mode sizes with --config 5 (e.g. 16x15 as '16,...')")
     ap.add_argument("--rank", type=int, default=0,
                     help="diagnostic: override every interior TT rank (e.g. 1: HBM-bound passes)")
     ap.add_argument("--step-size", type=float, default=1.0)
@@ -415,7 +434,7 @@ def main():
     nsteps = max(prof["steps"], 1)
     per = {k: v / nsteps for k, v in prof["ms"].items()}
     tot = sum(per.values())
-    models = group_models(pr, r["KL"], r["NL"], r["NR"])
+    models = chain_models(pr) if r["path"] == "chains" else group_models(pr, r["KL"], r["NL"], r["NR"])
     ncu = ncu_kernels()
     ncu_groups = (ncu or {}).get("groups", {})
     table = {}
@@ -470,7 +489,7 @@ def main():
                    "d": pr.d, "n": list(pr.n), "r": list(pr.r), "m": m, "K_L": r["KL"],
                    "l2": "inputs larger than L2 (Omega arrays + tables > 126 MB); no flush",
                    "m_global": r["m_global"], "step_rule": args.step_rule,
-                   "diagnostic_rank_override": args.rank or None,
+                   "diagnostic_rank_override": args.rank or None, "path": args.path,
                    "parallelism": (f"sharded Omega over {ws} GPUs (h and Y all-reduced, NCCL); "
                                    "value = N x iter/s of the N-times-larger problem") if ws > 1
                                   else "single"},

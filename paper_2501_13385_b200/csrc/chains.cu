@@ -49,50 +49,62 @@ __device__ __forceinline__ int bucket_mode(const ChainTT& tt, int64_t e) {
 }
 
 // One chain step for a group of G lanes holding a row vector a (entry j = lane + G w in slot w):
-// out(j) = sum_{i < r0} a(i) core[(i n + x) r1 + j],  j < r1.  All lanes of the warp execute it
-// (warp-uniform shapes), so full-mask shuffles are safe.
+// out(j) = sum_{i < r0} a(i) core[(i n + x) r1 + j],  j < r1.  Fully unrolled over the
+// compile-time group rank G V with predication on the runtime ranks: the rows are loaded in
+// chunks of up to 8 (all loads of a chunk in flight together, each a coalesced 8 r1-byte row
+// of the slice), then a(i) is broadcast by shuffle and accumulated.  All lanes of the warp
+// execute it (warp-uniform shapes), so full-mask shuffles are safe.
 template <int G, int V>
 __device__ __forceinline__ void chain_step(const double (&a)[V], double (&o)[V], const double* __restrict__ core,
                                            int r0, int64_t n, int r1, int64_t x, int lane) {
+  constexpr int R = G * V, CH = R < 8 ? R : 8;
 #pragma unroll
   for (int w = 0; w < V; ++w) o[w] = 0.0;
 #pragma unroll
-  for (int v = 0; v < V; ++v) {
-    for (int ii = 0; ii < G; ++ii) {
-      const int i = v * G + ii;
-      if (i >= r0) break;
-      const double ai = __shfl_sync(0xffffffffu, a[v], ii, G);
+  for (int i0 = 0; i0 < R; i0 += CH) {
+    double c[CH][V];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int i = i0 + u;
       const double* row = core + ((int64_t)i * n + x) * r1;
 #pragma unroll
       for (int w = 0; w < V; ++w) {
         const int j = lane + G * w;
-        if (j < r1) o[w] = fma(ai, __ldg(row + j), o[w]);
+        c[u][w] = (i < r0 && j < r1) ? __ldg(row + j) : 0.0;
       }
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const int i = i0 + u;
+      const double ai = __shfl_sync(0xffffffffu, a[i / G], i % G, G);
+#pragma unroll
+      for (int w = 0; w < V; ++w) o[w] = fma(ai, c[u][w], o[w]);
     }
   }
 }
 
 // out(i) = sum_{c < r1} core[(i n + x) r1 + c] b(c),  i < r0 (right-part recursion,
-// PAPER.md:102-105), b held like a.
-template <int G, int V>
-__device__ __forceinline__ void chain_step_right(const double (&b)[V], double (&o)[V],
-                                                 const double* __restrict__ core, int r0, int64_t n,
-                                                 int r1, int64_t x, int lane) {
+// PAPER.md:102-105), b held like a (one entry per lane, G >= r): lane c forms the products
+// core(i, x, c) b(c) for every i (loads coalesced over c), then a transpose-reduction over the
+// group (G - 1 shuffles) leaves out(lane) in lane `lane`.
+template <int G>
+__device__ __forceinline__ double chain_step_right(double b, const double* __restrict__ core, int r0,
+                                                   int64_t n, int r1, int64_t x, int lane) {
+  double p[G];
 #pragma unroll
-  for (int w = 0; w < V; ++w) o[w] = 0.0;
+  for (int i = 0; i < G; ++i)
+    p[i] = (i < r0 && lane < r1) ? __ldg(core + ((int64_t)i * n + x) * r1 + lane) * b : 0.0;
 #pragma unroll
-  for (int v = 0; v < V; ++v) {
-    for (int cc = 0; cc < G; ++cc) {
-      const int c = v * G + cc;
-      if (c >= r1) break;
-      const double bc = __shfl_sync(0xffffffffu, b[v], cc, G);
+  for (int o = G / 2; o > 0; o >>= 1) {
+    const bool up = (lane & o) != 0;
 #pragma unroll
-      for (int w = 0; w < V; ++w) {
-        const int i = lane + G * w;
-        if (i < r0) o[w] = fma(__ldg(core + ((int64_t)i * n + x) * r1 + c), bc, o[w]);
-      }
+    for (int j = 0; j < o; ++j) {
+      const double send = up ? p[j] : p[j + o];
+      const double keep = up ? p[j + o] : p[j];
+      p[j] = keep + __shfl_xor_sync(0xffffffffu, send, o, G);
     }
   }
+  return p[0];
 }
 
 // MODE 0: out[s] = T(x_s); MODE 1: out[s] = T(x_s) - y[s] (pass A residual g); MODE 2:
@@ -183,8 +195,7 @@ __global__ void __launch_bounds__(kT) k_chain_iface(const int32_t* __restrict__ 
       if (k == d - 1) {
         a[0] = lane < tt.r[k] ? __ldg(core + (int64_t)lane * tt.n[k] + x) : 0.0;   // r_d = 1
       } else {
-        chain_step_right<G, 1>(a, o, core, tt.r[k], tt.n[k], tt.r[k + 1], x, lane);
-        a[0] = o[0];
+        a[0] = chain_step_right<G>(a[0], core, tt.r[k], tt.n[k], tt.r[k + 1], x, lane);
       }
       if (act && lane < tt.r[k]) IR[tt.il_off[k] + s * tt.r[k] + lane] = a[0];
     }

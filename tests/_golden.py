@@ -24,8 +24,6 @@ CASES = {
     # draws (OS ~ 30) the theory step at 1.0 stops converging after 8 steps (residual 0.44 ->
     # 13), which would turn a 50-step comparison into a test of error amplification.
     "cfg5_4e6_50steps": (5, 4_000_000, 1.0, 50, (1, 10, 50)),
-    # full config 5, 50 steps (the metric's workload)
-    "cfg5_full_50steps": (5, None, 1.0, 50, (1, 10, 50)),
     # full config 3 (838,861 samples); theory rule at step_size 0.5: at 1.0 the theory step
     # diverges on this noisy stand-in (profiles/r01_convergence.md)
     "cfg3_full_50steps": (3, None, 0.5, 50, (1, 10, 50)),

@@ -26,7 +26,7 @@ ctx.set_cores(pr.init)
 NAMES = {0: "r2l_qr", 1: "r2l_push", 2: "l2r_qr", 3: "trunc", 4: "l2r_prod", 5: "orth_qr",
          8: "gram", 9: "reduce", 10: "chol", 11: "apply", 12: "racc", 15: "certify", 16: "fullJacobi",
          20: "round_total"}
-COUNTS = {17: "cert_fail", 18: "qr_fallbacks", 14: "cross_sweeps", 19: "full_sweeps", 6: "orth_cholqr_ok"}
+COUNTS = {17: "cert_fail", 18: "qr_fallbacks", 14: "cross_sweeps", 19: "full_sweeps", 6: "orth_cholqr_ok", 21: "chols", 22: "first_order", 23: "cholqr_calls"}
 prev = np.zeros(29)
 for i in range(steps):
     show = i >= steps - 3
