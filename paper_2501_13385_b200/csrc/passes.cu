@@ -13,9 +13,11 @@
 // psi_L psi_R g_s = ghat_s = (W^{-1/2} G)_s.
 //
 // Work decomposition: a warp owns a run of "virtual rows" (<= kSplit samples of one
-// bucket); LPS lanes per sample gather one table row (2 fp64 per lane, 16-byte
-// loads); results of split buckets go to partial slots reduced in order by
-// k_seg_fix, so every sum has a fixed order (deterministic).
+// bucket); results of split buckets go to partial slots reduced in order by k_seg_fix, so
+// every sum has a fixed order (deterministic).  k_seg (GSQ, and the adaptive step's DPASS)
+// walks the virtual rows one by one with LPS lanes per sample gathering one table row (2 fp64
+// per lane, 16-byte loads); the SpMM passes run as k_spmm_pipe, which streams the warp's whole
+// sample range through a cp.async gather pipeline in shared memory.
 #include "prgd_internal.cuh"
 
 namespace prgd {
@@ -46,12 +48,8 @@ __device__ __forceinline__ double2 ld2(const double* p) {
   return __ldg(reinterpret_cast<const double2*>(p));
 }
 
-// Minimum resident CTAs per SM (register cap), measured on B200 at config 5: the SDDMM pass
-// is fastest at 4 (64 registers; 5 spills and is 10 % slower), the SpMM passes at 5
-// (48 registers; 6 and 4 are 3 % / 0.5 % slower).
-#ifndef PRGD_SEG_OCC_SPMM
-#define PRGD_SEG_OCC_SPMM 5
-#endif
+// Minimum resident CTAs per SM (register cap), measured on B200 at config 5: the dot-product
+// (DPASS) pass is fastest at 4 (64 registers; 5 spills and is 10 % slower).
 #ifndef PRGD_SEG_OCC_SDDMM
 #define PRGD_SEG_OCC_SDDMM 4
 #endif
@@ -60,7 +58,7 @@ __device__ __forceinline__ double2 ld2(const double* p) {
 #endif
 template <int MODE>
 struct SegOcc {
-  static constexpr int v = MODE == kDPASS ? PRGD_SEG_OCC_SDDMM : (MODE == kSPMM ? PRGD_SEG_OCC_SPMM : 8);
+  static constexpr int v = MODE == kDPASS ? PRGD_SEG_OCC_SDDMM : 8;
 };
 
 // LPS lanes per sample, each holding V double2 of the row (ld = 2 LPS V)
@@ -92,16 +90,13 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
       if (MODE == kDPASS) rv2[q] = ld2(a.rowtab2 + trow * ld + 2 * (V * sub + q));
     }
     double accs = 0.0;
-    double2 accv[V];
-#pragma unroll
-    for (int q = 0; q < V; ++q) accv[q] = make_double2(0.0, 0.0);
     for (int c0 = 0; c0 < cnt; c0 += 32) {
       const int nc = cnt - c0 < 32 ? cnt - c0 : 32;
       const int64_t s = beg + c0 + lane;
       const bool have = lane < nc;
       // lane-parallel loads of this chunk's per-sample data (coalesced / independent)
       int colv = 0;
-      double xv = 0.0;    // g (GSQ, SPMM)
+      double xv = 0.0;    // g (GSQ)
       if (have) {
         if (MODE != kGSQ) colv = a.col[s];
         if (MODE != kDPASS) xv = a.perm ? a.g[a.perm[s]] : a.g[s];
@@ -158,30 +153,6 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
         {
           if (t < nc) accs = fma(pd[0], pd[0], accs);
         }
-      } else {
-#pragma unroll
-      for (int st0 = 0; st0 < STEPS; st0 += UNR) {
-        double2 b[UNR][V];
-        double xs[UNR];
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-          // lanes past the chunk hold colv = 0 and xv = 0: they read table row 0 and add
-          // 0 x row (finite tables), so no predicate is needed
-          const int t = (st0 + u) * G + grp;
-          const int cidx = __shfl_sync(kFull, colv, t & 31);
-          xs[u] = __shfl_sync(kFull, xv, t & 31);
-          const int off = cidx * ld + 2 * V * sub;   // < 2^31 (planner)
-#pragma unroll
-          for (int q = 0; q < V; ++q) b[u][q] = ld2(a.coltab + off + 2 * q);
-        }
-#pragma unroll
-        for (int u = 0; u < UNR; ++u)
-#pragma unroll
-          for (int q = 0; q < V; ++q) {
-            accv[q].x = fma(xs[u], b[u][q].x, accv[q].x);
-            accv[q].y = fma(xs[u], b[u][q].y, accv[q].y);
-          }
-      }
       }
     }
     const int32_t pslot = vr.w;
@@ -192,36 +163,12 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
         if (pslot < 0) a.out[row] = accs;
         else a.part[pslot] = accs;
       }
-    } else if (MODE == kDPASS) {
+    } else {   // DPASS
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) accs += __shfl_xor_sync(kFull, accs, o);   // every lane holds samples
       if (lane == 0) {
         if (pslot < 0) a.out[row] = accs;
         else a.part[pslot] = accs;
-      }
-    } else {
-#pragma unroll
-      for (int o = LPS; o < 32; o <<= 1)
-#pragma unroll
-        for (int q = 0; q < V; ++q) {
-          accv[q].x += __shfl_xor_sync(kFull, accv[q].x, o);
-          accv[q].y += __shfl_xor_sync(kFull, accv[q].y, o);
-        }
-      if (grp == 0) {
-        double* dst;
-        if (pslot < 0) {
-          const double f = a.rowscale ? a.rowscale[trow] : 1.0;
-          dst = a.out + trow * ld + 2 * V * sub;
-#pragma unroll
-          for (int q = 0; q < V; ++q) {
-            accv[q].x *= f;
-            accv[q].y *= f;
-          }
-        } else {
-          dst = a.part + (int64_t)pslot * ld + 2 * V * sub;
-        }
-#pragma unroll
-        for (int q = 0; q < V; ++q) *reinterpret_cast<double2*>(dst + 2 * q) = accv[q];
       }
     }
   }
@@ -434,6 +381,154 @@ __global__ void k_sumsq(const double* __restrict__ h0, int n0, Scalars* sc) {
 
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// ------------------------------------------------------------------ pipelined SpMM (pass B)
+// Same sums as k_seg<SPMM> (out[row] = rowscale[row] sum_{s in vrow} g_s coltab[col_s], split
+// rows to partial slots), same plan, different schedule: a warp walks the contiguous sample
+// range of its virtual rows in 32-sample chunks.  The gathered table rows of chunk c + 1 land
+// in shared memory by cp.async while chunk c is accumulated, and the per-sample streams (col,
+// g) are loaded one to two chunks ahead, so a warp keeps one chunk of row gathers in flight and
+// has no dependent load chain per row (k_seg: plan record -> col / g -> gathers, per row).
+// Within a chunk, sample i is accumulated by lane group i mod G (LPS lanes, one double2 of the
+// row each); a virtual row ending in the chunk is reduced over the groups and written.  Fixed
+// order throughout (deterministic).
+constexpr int kPipeWarps = 8;
+
+__device__ __forceinline__ void pipe_cp16(double* smem, const double* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void pipe_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void pipe_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int LPS, int NB>
+__global__ void __launch_bounds__(32 * kPipeWarps) k_spmm_pipe(SegDev a, const Scalars* sc) {
+  if (sc && sc->noop) return;
+  constexpr int G = 32 / LPS, STEPS = LPS, LD = 2 * LPS, CH = 32 * LD;
+  extern __shared__ double pipe_smem[];
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / LPS, sub = lane - grp * LPS;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (warp >= a.nwarps) return;
+  double* buf = pipe_smem + (size_t)(threadIdx.x >> 5) * NB * CH;
+  const int64_t v0 = a.warp_vbegin[warp], v1 = a.warp_vbegin[warp + 1];
+  const int64_t S0 = a.vrow[v0].z;
+  const int4 lastv = a.vrow[v1 - 1];
+  const int64_t S1 = (int64_t)lastv.z + lastv.y;
+  const int nch = S1 > S0 ? (int)((S1 - S0 + 31) >> 5) : 1;
+  auto ld_col = [&](int c) -> int {
+    const int64_t t = S0 + 32 * (int64_t)c + lane;
+    return (c < nch && t < S1) ? a.col[t] : 0;   // past the end: row 0 (valid), weight 0
+  };
+  auto ld_g = [&](int c) -> double {
+    const int64_t t = S0 + 32 * (int64_t)c + lane;
+    if (c >= nch || t >= S1) return 0.0;
+    return a.perm ? a.g[a.perm[t]] : a.g[t];
+  };
+  auto issue = [&](int c, int colv) {   // chunk c's table rows -> buf[c % NB] (LD / 2 x 16 B per lane)
+    double* dst = buf + (c % NB) * CH;
+#pragma unroll
+    for (int j = 0; j < LD / 2; ++j) {
+      const int e = j * 32 + lane;
+      const int i = e / (LD / 2), p = e - i * (LD / 2);
+      const int ci = __shfl_sync(kFull, colv, i);
+      pipe_cp16(dst + i * LD + 2 * p, a.coltab + (int64_t)ci * LD + 2 * p);
+    }
+  };
+  // current virtual row (warp-uniform); records cached 32 at a time
+  int64_t vb = v0, cur = v0;
+  int4 rec = vb + lane < v1 ? a.vrow[vb + lane] : make_int4(0, 0, 0, -1);
+  int row = __shfl_sync(kFull, rec.x, 0), cnt = __shfl_sync(kFull, rec.y, 0);
+  int64_t beg = __shfl_sync(kFull, rec.z, 0);
+  int slot = __shfl_sync(kFull, rec.w, 0);
+  double2 acc = make_double2(0.0, 0.0);
+
+  double gC = ld_g(0);
+#pragma unroll
+  for (int j = 0; j + 1 < NB; ++j) {   // chunks 0 .. NB-2 in flight
+    if (j < nch) issue(j, ld_col(j));
+    pipe_commit();
+  }
+  int colN = ld_col(NB - 1);
+  for (int c = 0; c < nch; ++c) {
+    const int colNN = ld_col(c + NB);
+    const double gN = ld_g(c + 1);
+    if (c + NB - 1 < nch) issue(c + NB - 1, colN);
+    pipe_commit();
+    pipe_wait<NB - 1>();
+    __syncwarp();
+    const double* cb = buf + (c % NB) * CH;
+    const int64_t c0 = S0 + 32 * (int64_t)c;
+    while (cur < v1) {
+      const int64_t e = beg + cnt;
+      const int lo = beg > c0 ? (int)(beg - c0) : 0;
+      const int hi = e < c0 + 32 ? (int)(e - c0) : 32;
+#pragma unroll
+      for (int st = 0; st < STEPS; ++st) {
+        const int i = st * G + grp;
+        const double gv = __shfl_sync(kFull, gC, i);
+        if (i >= lo && i < hi) {
+          const double2 r = *reinterpret_cast<const double2*>(cb + i * LD + 2 * sub);
+          acc.x = fma(gv, r.x, acc.x);
+          acc.y = fma(gv, r.y, acc.y);
+        }
+      }
+      if (e > c0 + 32) break;   // the virtual row continues in the next chunk
+#pragma unroll
+      for (int o = LPS; o < 32; o <<= 1) {
+        acc.x += __shfl_xor_sync(kFull, acc.x, o);
+        acc.y += __shfl_xor_sync(kFull, acc.y, o);
+      }
+      if (grp == 0) {
+        double* dst;
+        if (slot < 0) {
+          const double f = a.rowscale ? a.rowscale[row] : 1.0;
+          acc.x *= f;
+          acc.y *= f;
+          dst = a.out + (int64_t)row * LD + 2 * sub;
+        } else {
+          dst = a.part + (int64_t)slot * LD + 2 * sub;
+        }
+        *reinterpret_cast<double2*>(dst) = acc;
+      }
+      acc = make_double2(0.0, 0.0);
+      if (++cur >= v1) break;
+      if (cur - vb >= 32) {   // warp-uniform
+        vb += 32;
+        rec = vb + lane < v1 ? a.vrow[vb + lane] : make_int4(0, 0, 0, -1);
+      }
+      const int sl = (int)(cur - vb);
+      row = __shfl_sync(kFull, rec.x, sl);
+      cnt = __shfl_sync(kFull, rec.y, sl);
+      beg = __shfl_sync(kFull, rec.z, sl);
+      slot = __shfl_sync(kFull, rec.w, sl);
+    }
+    __syncwarp();   // every lane is done with buf[c % NB] before chunk c + NB lands there
+    colN = colNN;
+    gC = gN;
+  }
+}
+
+template <int LPS, int NB>
+void spmm_pipe_launch_nb(cudaStream_t s, const SegDev& dv, const Scalars* sc) {
+  const size_t smem = (size_t)kPipeWarps * NB * 32 * (2 * LPS) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_spmm_pipe<LPS, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  const unsigned grid = blocks_for(dv.nwarps, kPipeWarps);
+  k_spmm_pipe<LPS, NB><<<grid, 32 * kPipeWarps, smem, s>>>(dv, sc);
+}
+
+// Two chunk buffers per warp (64 KB per CTA at 16-wide rows, 3 CTAs = 24 warps per SM).
+// Measured at config 5: three buffers (2 CTAs per SM) 0.79 ms per pass vs 0.65 ms; L2
+// evict_last hints on the gathers with evict-first streams / outputs: no change.
+template <int LPS>
+void spmm_pipe_launch(cudaStream_t s, const SegDev& dv, const Scalars* sc) {
+  spmm_pipe_launch_nb<LPS, 2>(s, dv, sc);
+}
+
 template <int LPS>
 void seg_dispatch_mode(cudaStream_t s, int mode, const SegDev& dv, unsigned grid,
                        const Scalars* sc) {
@@ -445,7 +540,7 @@ void seg_dispatch_mode(cudaStream_t s, int mode, const SegDev& dv, unsigned grid
   }
   if (mode == kDPASS) k_seg<LPS, kDPASS><<<grid, 256, 0, s>>>(dv, sc);
   else if (mode == kGSQ) k_seg<1, kGSQ><<<grid, 256, 0, s>>>(dv, sc);
-  else k_seg<LPS, kSPMM><<<grid, 256, 0, s>>>(dv, sc);   // (V = 2 measured slower for SpMM)
+  else spmm_pipe_launch<LPS>(s, dv, sc);
 }
 
 }  // namespace
