@@ -34,6 +34,38 @@ for lib, tag in ((a, "a"), (b, "b")):
                    env=dict(os.environ, PRGD_LIB_PATH=lib))
     outs.append(np.load(f))
 za, zb = outs
+
+
+def tt_norm(C):
+    """||T||_F by a left-to-right QR sweep (stable)."""
+    R = np.ones((1, 1))
+    for c in C:
+        M = np.einsum("ab,bic->aic", R, c)
+        M = M.reshape(-1, M.shape[2])
+        _, R = np.linalg.qr(M)
+    return float(np.linalg.norm(R))
+
+
+def tt_sub(A, B):
+    """A - B as a block TT of rank r_A + r_B."""
+    d, out = len(A), []
+    for k, (a, b) in enumerate(zip(A, B)):
+        if k == 0:
+            out.append(np.concatenate([a, -b], axis=2))
+        elif k == d - 1:
+            out.append(np.concatenate([a, b], axis=0))
+        else:
+            c = np.zeros((a.shape[0] + b.shape[0], a.shape[1], a.shape[2] + b.shape[2]))
+            c[:a.shape[0], :, :a.shape[2]] = a
+            c[a.shape[0]:, :, a.shape[2]:] = b
+            out.append(c)
+    return out
+
+
+ca = [za[f"arr_{k}"] for k in range(len([f for f in za.files if f.startswith("arr_")]))]
+cb = [zb[f"arr_{k}"] for k in range(len(ca))]
 same = all(np.array_equal(za[k], zb[k]) for k in za.files)
 diff = max(float(np.max(np.abs(za[k] - zb[k]))) for k in za.files)
-print(f"cfg {cfg}: bitwise identical {same}, max abs diff {diff:.3e}")
+rel = tt_norm(tt_sub(ca, cb)) / tt_norm(ca)
+print(f"cfg {cfg}: bitwise identical {same}, max abs core diff {diff:.3e}, "
+      f"relative tensor difference {rel:.3e}")
