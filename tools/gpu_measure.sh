@@ -1,4 +1,4 @@
-# Measurement lease (round 2): FP64 peak with its clock record, the default bench line, the r = 1
+# Measurement lease (round 2, final build): FP64 peak with its clock record, the default bench line, the r = 1
 # HBM diagnostic, per-config bench lines, one ncu-counted PRGD step at config 5 (per-kernel DRAM
 # bytes, DMMA / FP64 pipe utilisation) -> tools/ncu_table.py -> profiles/r02_ncu_kernels.json, and
 # the ncu launch list of the bench command.
@@ -22,3 +22,7 @@ timeout 1200 ncu --profile-from-start off --clock-control none --metrics $M --cs
 timeout 600 $CMD > gpurun_out/launch_plain.log 2>&1 && \
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
 echo "ncu rc=$?"
+# full ncu captures of the SpMM pipeline kernel and the cluster rounding (one launch each)
+timeout 1200 ncu --profile-from-start off --clock-control none --set full --import-source on \
+    -k regex:"k_spmm_pipe|k_round_cs|k_flat_sddmm" -c 4 -o gpurun_out/full_head python tools/ncu_step.py 5 > gpurun_out/ncu_full.log 2>&1
+echo "ncu full rc=$?"

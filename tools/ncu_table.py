@@ -61,7 +61,7 @@ def group_of(seq):
             phase = "tabU" if phase in ("orth", "tabU") else "tabC"
         elif "k_flat" in k:                        # pass A prefix (flat SDDMM + fix-up)
             phase, nseg, g = "passA", 1, "passA_prefix"
-        elif "k_seg" in k:
+        elif "k_seg" in k or "k_spmm_pipe" in k:
             if phase == "tabU" or phase == "passB":
                 if "k_seg_fix" not in k:
                     nseg += 1
