@@ -49,7 +49,11 @@ __device__ __forceinline__ double2 ld2(const double* p) {
 }
 
 // Minimum resident CTAs per SM (register cap), measured on B200 at config 5: the dot-product
-// (DPASS) pass is fastest at 4 (64 registers; 5 spills and is 10 % slower).
+// (DPASS) pass is fastest at 4 (64 registers; 5 spills and is 10 % slower), the row-plan SpMM
+// at 5 (48 registers).
+#ifndef PRGD_SEG_OCC_SPMM
+#define PRGD_SEG_OCC_SPMM 5
+#endif
 #ifndef PRGD_SEG_OCC_SDDMM
 #define PRGD_SEG_OCC_SDDMM 4
 #endif
@@ -58,7 +62,7 @@ __device__ __forceinline__ double2 ld2(const double* p) {
 #endif
 template <int MODE>
 struct SegOcc {
-  static constexpr int v = MODE == kDPASS ? PRGD_SEG_OCC_SDDMM : 8;
+  static constexpr int v = MODE == kDPASS ? PRGD_SEG_OCC_SDDMM : (MODE == kSPMM ? PRGD_SEG_OCC_SPMM : 8);
 };
 
 // LPS lanes per sample, each holding V double2 of the row (ld = 2 LPS V)
@@ -90,6 +94,9 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
       if (MODE == kDPASS) rv2[q] = ld2(a.rowtab2 + trow * ld + 2 * (V * sub + q));
     }
     double accs = 0.0;
+    double2 accv[V];
+#pragma unroll
+    for (int q = 0; q < V; ++q) accv[q] = make_double2(0.0, 0.0);
     for (int c0 = 0; c0 < cnt; c0 += 32) {
       const int nc = cnt - c0 < 32 ? cnt - c0 : 32;
       const int64_t s = beg + c0 + lane;
@@ -153,6 +160,30 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
         {
           if (t < nc) accs = fma(pd[0], pd[0], accs);
         }
+      } else {
+#pragma unroll
+      for (int st0 = 0; st0 < STEPS; st0 += UNR) {
+        double2 b[UNR][V];
+        double xs[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          // lanes past the chunk hold colv = 0 and xv = 0: they read table row 0 and add
+          // 0 x row (finite tables), so no predicate is needed
+          const int t = (st0 + u) * G + grp;
+          const int cidx = __shfl_sync(kFull, colv, t & 31);
+          xs[u] = __shfl_sync(kFull, xv, t & 31);
+          const int off = cidx * ld + 2 * V * sub;   // < 2^31 (planner)
+#pragma unroll
+          for (int q = 0; q < V; ++q) b[u][q] = ld2(a.coltab + off + 2 * q);
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            accv[q].x = fma(xs[u], b[u][q].x, accv[q].x);
+            accv[q].y = fma(xs[u], b[u][q].y, accv[q].y);
+          }
+      }
       }
     }
     const int32_t pslot = vr.w;
@@ -163,12 +194,36 @@ __global__ void __launch_bounds__(256, SegOcc<MODE>::v) k_seg(SegDev a, const Sc
         if (pslot < 0) a.out[row] = accs;
         else a.part[pslot] = accs;
       }
-    } else {   // DPASS
+    } else if (MODE == kDPASS) {
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) accs += __shfl_xor_sync(kFull, accs, o);   // every lane holds samples
       if (lane == 0) {
         if (pslot < 0) a.out[row] = accs;
         else a.part[pslot] = accs;
+      }
+    } else {
+#pragma unroll
+      for (int o = LPS; o < 32; o <<= 1)
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          accv[q].x += __shfl_xor_sync(kFull, accv[q].x, o);
+          accv[q].y += __shfl_xor_sync(kFull, accv[q].y, o);
+        }
+      if (grp == 0) {
+        double* dst;
+        if (pslot < 0) {
+          const double f = a.rowscale ? a.rowscale[trow] : 1.0;
+          dst = a.out + trow * ld + 2 * V * sub;
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            accv[q].x *= f;
+            accv[q].y *= f;
+          }
+        } else {
+          dst = a.part + (int64_t)pslot * ld + 2 * V * sub;
+        }
+#pragma unroll
+        for (int q = 0; q < V; ++q) *reinterpret_cast<double2*>(dst + 2 * q) = accv[q];
       }
     }
   }
@@ -463,15 +518,16 @@ __global__ void __launch_bounds__(32 * kPipeWarps) k_spmm_pipe(SegDev a, const S
       const int64_t e = beg + cnt;
       const int lo = beg > c0 ? (int)(beg - c0) : 0;
       const int hi = e < c0 + 32 ? (int)(e - c0) : 32;
+      // samples outside the virtual row weigh 0 (every slot holds a finite gathered row), so
+      // the accumulation runs unpredicated
 #pragma unroll
       for (int st = 0; st < STEPS; ++st) {
         const int i = st * G + grp;
         const double gv = __shfl_sync(kFull, gC, i);
-        if (i >= lo && i < hi) {
-          const double2 r = *reinterpret_cast<const double2*>(cb + i * LD + 2 * sub);
-          acc.x = fma(gv, r.x, acc.x);
-          acc.y = fma(gv, r.y, acc.y);
-        }
+        const double w = (i >= lo && i < hi) ? gv : 0.0;
+        const double2 r = *reinterpret_cast<const double2*>(cb + i * LD + 2 * sub);
+        acc.x = fma(w, r.x, acc.x);
+        acc.y = fma(w, r.y, acc.y);
       }
       if (e > c0 + 32) break;   // the virtual row continues in the next chunk
 #pragma unroll
@@ -529,6 +585,15 @@ void spmm_pipe_launch(cudaStream_t s, const SegDev& dv, const Scalars* sc) {
   spmm_pipe_launch_nb<LPS, 2>(s, dv, sc);
 }
 
+// PRGD_SPMM_PIPE=0 / 1 forces the row-plan / pipelined SpMM (A/B measurements)
+inline int spmm_pipe_env() {
+  static const int v = [] {
+    const char* e = getenv("PRGD_SPMM_PIPE");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  return v;
+}
+
 template <int LPS>
 void seg_dispatch_mode(cudaStream_t s, int mode, const SegDev& dv, unsigned grid,
                        const Scalars* sc) {
@@ -540,7 +605,8 @@ void seg_dispatch_mode(cudaStream_t s, int mode, const SegDev& dv, unsigned grid
   }
   if (mode == kDPASS) k_seg<LPS, kDPASS><<<grid, 256, 0, s>>>(dv, sc);
   else if (mode == kGSQ) k_seg<1, kGSQ><<<grid, 256, 0, s>>>(dv, sc);
-  else spmm_pipe_launch<LPS>(s, dv, sc);
+  else if (spmm_pipe_env() == 1 || (spmm_pipe_env() < 0 && LPS >= 8)) spmm_pipe_launch<LPS>(s, dv, sc);
+  else k_seg<LPS, kSPMM><<<grid, 256, 0, s>>>(dv, sc);
 }
 
 }  // namespace
