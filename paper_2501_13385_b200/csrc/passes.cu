@@ -465,36 +465,39 @@ __global__ void __launch_bounds__(32 * kPipeWarps) k_spmm_pipe(SegDev a, const S
   const int grp = lane / LPS, sub = lane - grp * LPS;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (warp >= a.nwarps) return;
-  double* buf = pipe_smem + (size_t)(threadIdx.x >> 5) * NB * CH;
+  // per warp: NB chunk buffers of gathered rows, then NB x 32 staged g values
+  double* buf = pipe_smem + (size_t)(threadIdx.x >> 5) * NB * (CH + 32);
+  double* gsm = buf + NB * CH;
   const int64_t v0 = a.warp_vbegin[warp], v1 = a.warp_vbegin[warp + 1];
-  const int64_t S0 = a.vrow[v0].z;
+  // sample positions fit in 32 bits (m < 2^31: the planner's int4 records)
+  const int S0 = a.vrow[v0].z;
   const int4 lastv = a.vrow[v1 - 1];
-  const int64_t S1 = (int64_t)lastv.z + lastv.y;
-  const int nch = S1 > S0 ? (int)((S1 - S0 + 31) >> 5) : 1;
+  const int S1 = lastv.z + lastv.y;
+  const int nch = S1 > S0 ? (S1 - S0 + 31) >> 5 : 1;
   auto ld_col = [&](int c) -> int {
-    const int64_t t = S0 + 32 * (int64_t)c + lane;
+    const int t = S0 + 32 * c + lane;
     return (c < nch && t < S1) ? a.col[t] : 0;   // past the end: row 0 (valid), weight 0
   };
   auto ld_g = [&](int c) -> double {
-    const int64_t t = S0 + 32 * (int64_t)c + lane;
+    const int t = S0 + 32 * c + lane;
     if (c >= nch || t >= S1) return 0.0;
     return a.perm ? a.g[a.perm[t]] : a.g[t];
   };
+  const double* src0 = a.coltab + 2 * (lane % (LD / 2));
   auto issue = [&](int c, int colv) {   // chunk c's table rows -> buf[c % NB] (LD / 2 x 16 B per lane)
-    double* dst = buf + (c % NB) * CH;
+    double* dst = buf + (c % NB) * CH + 2 * (lane % (LD / 2));
 #pragma unroll
     for (int j = 0; j < LD / 2; ++j) {
-      const int e = j * 32 + lane;
-      const int i = e / (LD / 2), p = e - i * (LD / 2);
+      const int i = (j * 32 + lane) / (LD / 2);   // sample; lane % (LD / 2) is its 16-byte part
       const int ci = __shfl_sync(kFull, colv, i);
-      pipe_cp16(dst + i * LD + 2 * p, a.coltab + (int64_t)ci * LD + 2 * p);
+      pipe_cp16(dst + i * LD, src0 + ci * LD);    // ci * LD < 2^31 (planner)
     }
   };
   // current virtual row (warp-uniform); records cached 32 at a time
   int64_t vb = v0, cur = v0;
   int4 rec = vb + lane < v1 ? a.vrow[vb + lane] : make_int4(0, 0, 0, -1);
   int row = __shfl_sync(kFull, rec.x, 0), cnt = __shfl_sync(kFull, rec.y, 0);
-  int64_t beg = __shfl_sync(kFull, rec.z, 0);
+  int beg = __shfl_sync(kFull, rec.z, 0);
   int slot = __shfl_sync(kFull, rec.w, 0);
   double2 acc = make_double2(0.0, 0.0);
 
@@ -510,22 +513,23 @@ __global__ void __launch_bounds__(32 * kPipeWarps) k_spmm_pipe(SegDev a, const S
     const double gN = ld_g(c + 1);
     if (c + NB - 1 < nch) issue(c + NB - 1, colN);
     pipe_commit();
+    double* gc = gsm + (c % NB) * 32;
+    gc[lane] = gC;
     pipe_wait<NB - 1>();
     __syncwarp();
-    const double* cb = buf + (c % NB) * CH;
-    const int64_t c0 = S0 + 32 * (int64_t)c;
+    const double* cb = buf + (c % NB) * CH + 2 * sub;
+    const int c0 = S0 + 32 * c;
     while (cur < v1) {
-      const int64_t e = beg + cnt;
-      const int lo = beg > c0 ? (int)(beg - c0) : 0;
-      const int hi = e < c0 + 32 ? (int)(e - c0) : 32;
+      const int e = beg + cnt;
+      const int lo = beg > c0 ? beg - c0 : 0;
+      const int hi = e < c0 + 32 ? e - c0 : 32;
       // samples outside the virtual row weigh 0 (every slot holds a finite gathered row), so
       // the accumulation runs unpredicated
 #pragma unroll
       for (int st = 0; st < STEPS; ++st) {
         const int i = st * G + grp;
-        const double gv = __shfl_sync(kFull, gC, i);
-        const double w = (i >= lo && i < hi) ? gv : 0.0;
-        const double2 r = *reinterpret_cast<const double2*>(cb + i * LD + 2 * sub);
+        const double w = (unsigned)(i - lo) < (unsigned)(hi - lo) ? gc[i] : 0.0;
+        const double2 r = *reinterpret_cast<const double2*>(cb + i * LD);
         acc.x = fma(w, r.x, acc.x);
         acc.y = fma(w, r.y, acc.y);
       }
@@ -559,7 +563,7 @@ __global__ void __launch_bounds__(32 * kPipeWarps) k_spmm_pipe(SegDev a, const S
       beg = __shfl_sync(kFull, rec.z, sl);
       slot = __shfl_sync(kFull, rec.w, sl);
     }
-    __syncwarp();   // every lane is done with buf[c % NB] before chunk c + NB lands there
+    __syncwarp();   // every lane is done with buf / gsm[c % NB] before chunk c + NB lands there
     colN = colNN;
     gC = gN;
   }
@@ -567,7 +571,7 @@ __global__ void __launch_bounds__(32 * kPipeWarps) k_spmm_pipe(SegDev a, const S
 
 template <int LPS, int NB>
 void spmm_pipe_launch_nb(cudaStream_t s, const SegDev& dv, const Scalars* sc) {
-  const size_t smem = (size_t)kPipeWarps * NB * 32 * (2 * LPS) * sizeof(double);
+  const size_t smem = (size_t)kPipeWarps * NB * 32 * (2 * LPS + 1) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_spmm_pipe<LPS, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
