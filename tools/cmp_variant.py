@@ -1,5 +1,6 @@
 """Compare the iterates of two library builds bit for bit (diagnostic):
-    python tools/cmp_variant.py libA.so libB.so cfg [m] [steps]"""
+    python tools/cmp_variant.py libA.so libB.so cfg [m] [steps]
+A library argument VAR=VALUE@lib.so runs that side with the environment switch VAR=VALUE."""
 import os
 import subprocess
 import sys
@@ -30,8 +31,13 @@ import numpy as np  # noqa: E402
 outs = []
 for lib, tag in ((a, "a"), (b, "b")):
     f = f"/tmp/cmp_{tag}.npz"
-    subprocess.run([sys.executable, __file__, "--run", cfg, m, steps, f], check=True,
-                   env=dict(os.environ, PRGD_LIB_PATH=lib))
+    env = dict(os.environ)
+    if "@" in lib:                       # VAR=VALUE@lib.so: an environment switch for this run
+        kv, lib = lib.split("@", 1)
+        k, v = kv.split("=", 1)
+        env[k] = v
+    env["PRGD_LIB_PATH"] = lib
+    subprocess.run([sys.executable, __file__, "--run", cfg, m, steps, f], check=True, env=env)
     outs.append(np.load(f))
 za, zb = outs
 
