@@ -89,7 +89,9 @@ enum { TT_STEP_THEORY = 0, TT_STEP_RAW = 1, TT_STEP_ADAPTIVE = 2 };
  * Cores start at zero; observations unset.  *out receives the context. */
 PRGD_API int tt_create(int d, const int64_t* n, const int64_t* r, tt_ctx** out);
 
-/* Release all device memory and the context.  NULL is a no-op. */
+/* Release all device memory and the context.  NULL is a no-op.  (Plumbing: the paper's
+ * method is CPU-only and defines no resource calls; tt_destroy, tt_set_stream and
+ * tt_set_allocator follow SURVEY.md §8(b).) */
 PRGD_API int tt_destroy(tt_ctx* ctx);
 
 /* Use `stream` (a cudaStream_t, e.g. PyTorch's current stream) for all work.
@@ -189,7 +191,9 @@ PRGD_API int tt_prgd_step(tt_ctx* ctx, double step_size);
  * Synchronises. */
 PRGD_API int tt_eval_at(tt_ctx* ctx, const int32_t* h_idx, int64_t count, double* h_out);
 
-/* ||P_Omega(T_cur) - y||_2 at the CURRENT iterate (0 for empty Omega).
+/* ||P_Omega(T_cur) - y||_2 at the CURRENT iterate (0 for empty Omega): the norm of the sparse
+ * residual G_l = P_Omega(T_l - T*) of Alg. 2 line 1 (y replaces T*, reading R14),
+ * i.e. sqrt(2 f(T_cur)) for the objective f(T) = 1/2 <T - T*, P_Omega(T - T*)> of PAPER.md:30-41.
  * Synchronises; reports pending TT_ERR_NUMERIC. */
 PRGD_API int tt_residual_norm(tt_ctx* ctx, double* out);
 
