@@ -277,16 +277,12 @@ __global__ void k_marg_partial(const double* __restrict__ H, MargArgs ma, double
   const int64_t per = (total + kMargChunks - 1) / kMargChunks;
   const int64_t e0 = chunk * per, e1 = e0 + per < total ? e0 + per : total;
   double acc = 0.0;
-  if (st >= 32) {
-    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-      const int64_t hi = e / st, lo = e - hi * st;
-      acc += H[hi * span + (int64_t)j * st + lo];
-    }
-  } else {
-    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-      const int64_t hi = e / st, lo = e - hi * st;
-      acc += H[hi * span + (int64_t)j * st + lo];
-    }
+  // table rows N <= 2^30 (planner): 32-bit index arithmetic (a 64-bit division per element
+  // made this kernel issue-bound)
+  const uint32_t st32 = (uint32_t)st, span32 = (uint32_t)span, off32 = (uint32_t)j * st32;
+  for (uint32_t e = (uint32_t)e0 + threadIdx.x; e < (uint32_t)e1; e += blockDim.x) {
+    const uint32_t hi = e / st32, lo = e - hi * st32;
+    acc += H[hi * span32 + off32 + lo];
   }
   red[threadIdx.x] = acc;
   __syncthreads();
@@ -358,24 +354,25 @@ struct PsiArgs {
 __global__ void k_psi(const double* __restrict__ phi, PsiArgs pa, double* __restrict__ psiL,
                       double* __restrict__ psiR, const Scalars* sc) {
   if (sc && sc->noop) return;
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  // table rows N_L, N_R <= 2^30 (planner): 32-bit digit extraction
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e < pa.NL) {
-    int64_t P = e;
+    uint32_t P = (uint32_t)e;
     double v = 1.0;
     for (int k = pa.KL - 1; k >= 0; --k) {
-      int64_t q = P / pa.n[k];
-      int xk = (int)(P - q * pa.n[k]);
+      const uint32_t q = P / (uint32_t)pa.n[k];
+      const int xk = (int)(P - q * (uint32_t)pa.n[k]);
       P = q;
       v /= phi[pa.phi_off[k] + xk];
     }
     psiL[e] = v;
   } else if (e < pa.NL + pa.NR) {
-    int64_t S = e - pa.NL;
-    const int64_t S0 = S;
+    uint32_t S = (uint32_t)(e - pa.NL);
+    const int64_t S0 = e - pa.NL;
     double v = 1.0;
     for (int k = pa.KL; k < pa.d; ++k) {
-      int64_t q = S / pa.n[k];
-      int xk = (int)(S - q * pa.n[k]);
+      const uint32_t q = S / (uint32_t)pa.n[k];
+      const int xk = (int)(S - q * (uint32_t)pa.n[k]);
       S = q;
       v /= phi[pa.phi_off[k] + xk];
     }
