@@ -1026,10 +1026,23 @@ __global__ void __launch_bounds__(kProjThreads) k_project(DenseArgs a) {
     for (int e = threadIdx.x; e < ngrp * rr; e += blockDim.x) {
       const int gi = e / rr, el = e - gi * rr;
       const int aa = el / r1, bb = el - aa * r1;
-      double acc = 0.0;
-      for (int row = gi; row < m; row += ngrp)
-        acc = fma(Uv[(int64_t)row * uld + aa], Z[(int64_t)row * zld + bb], acc);
-      Wp[e] = acc;
+      // four interleaved accumulators, eight rows' loads in flight (a single dependent chain
+      // over m / ngrp rows of L2 loads was 0.66 ms at config 3's 4096-row core)
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      int row = gi;
+      for (; row + 7 * ngrp < m; row += 8 * ngrp) {
+        double u[8], z[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          u[q] = Uv[(int64_t)(row + q * ngrp) * uld + aa];
+          z[q] = Z[(int64_t)(row + q * ngrp) * zld + bb];
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q & 3] = fma(u[q], z[q], acc[q & 3]);
+      }
+      for (int q = 0; row < m; row += ngrp, ++q)
+        acc[q & 3] = fma(Uv[(int64_t)row * uld + aa], Z[(int64_t)row * zld + bb], acc[q & 3]);
+      Wp[e] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
     }
     __syncthreads();
     for (int e = threadIdx.x; e < rr; e += blockDim.x) {
@@ -1083,17 +1096,24 @@ __global__ void __launch_bounds__(kProjThreads) k_project(DenseArgs a) {
   const double* ph = a.phi + a.phi_off[k];
   const bool wr = a.wretr != 0;
   double* B = a.B + a.b_off[k];
+  // 1 / phi_{k,x} once per slice (a reciprocal per element was the assembly's cost at config 3)
+  double* invp = smraw;
+  const bool inv_sm = nk <= a.smem_doubles;
+  if (inv_sm)
+    for (int x = threadIdx.x; x < nk; x += blockDim.x) invp[x] = wr ? 1.0 : 1.0 / ph[x];
+  __syncthreads();
+  auto inv_of = [&](int x) { return inv_sm ? invp[x] : (wr ? 1.0 : 1.0 / ph[x]); };
   if (k == 0) {
     const int Rb1 = 2 * r1;
     for (int e = threadIdx.x; e < nk * Rb1; e += blockDim.x) {
       const int x = e / Rb1, c = e - x * Rb1;
-      const double inv = wr ? 1.0 : 1.0 / ph[x];
+      const double inv = inv_of(x);
       B[e] = c < r1 ? -alpha * Ah[x * r1 + c] * inv : U[x * r1 + (c - r1)] * inv;
     }
   } else if (k == d - 1) {
     for (int e = threadIdx.x; e < 2 * r0 * nk; e += blockDim.x) {
       const int aa = e / nk, x = e - aa * nk;
-      const double inv = wr ? 1.0 : 1.0 / ph[x];
+      const double inv = inv_of(x);
       B[e] = aa < r0 ? U[aa * nk + x] * inv
                      : (U[(aa - r0) * nk + x] - alpha * Ah[(aa - r0) * nk + x]) * inv;
     }
@@ -1104,7 +1124,7 @@ __global__ void __launch_bounds__(kProjThreads) k_project(DenseArgs a) {
       const int c = e % Rb1;
       const int x = (e / Rb1) % nk;
       const int aa = e / (Rb1 * nk);
-      const double inv = wr ? 1.0 : 1.0 / ph[x];
+      const double inv = inv_of(x);
       double v;
       if (aa < r0) v = c < r1 ? U[(aa * nk + x) * r1 + c] * inv : 0.0;
       else if (c < r1) v = -alpha * Ah[((aa - r0) * nk + x) * r1 + c] * inv;

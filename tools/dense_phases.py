@@ -1,6 +1,6 @@
 """Diagnostic: Jacobi sweeps and per-phase cycles of the dense sweeps (cluster rounding).
 
-    python tools/dense_phases.py [cfg] [m] [steps]
+    python tools/dense_phases.py [cfg] [m] [steps] [step_size]
 """
 import os
 import sys
@@ -14,6 +14,7 @@ import synth  # noqa: E402
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 m = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2] else None
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
+step_size = float(sys.argv[4]) if len(sys.argv) > 4 else 1.0
 pr = synth.make_problem(cfg, m=m)
 t = pkg.TTContext(pr.n, pr.r)
 t.set_cores(pr.truth)
@@ -30,7 +31,7 @@ COUNTS = {17: "cert_fail", 18: "qr_fallbacks", 14: "cross_sweeps", 19: "full_swe
 prev = np.zeros(29)
 for i in range(steps):
     show = i >= steps - 3
-    ctx.step(1.0)
+    ctx.step(step_size)
     e = ctx.debug("eps")
     dl = e - prev
     prev = e.copy()
