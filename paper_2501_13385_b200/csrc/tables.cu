@@ -394,7 +394,8 @@ __global__ void k_jsplit_reduce(const double* __restrict__ part, int nsplit, int
 int rec_jsplit(int64_t rows_out, int nk, int jc, int ld_out, int64_t scratch_cap) {
   const int64_t rb = (rows_out + kRecRows - 1) / kRecRows;
   int64_t js = rb >= 148 ? 1 : (296 + rb - 1) / rb;
-  js = std::min<int64_t>(js, (nk + jc - 1) / jc);
+  js = std::min<int64_t>(js, nk);   // a CTA may cover fewer slices than one staged chunk jc
+  (void)jc;
   if (scratch_cap > 0) js = std::min<int64_t>(js, scratch_cap / std::max<int64_t>(1, rows_out * ld_out));
   else js = 1;
   return (int)std::max<int64_t>(1, js);
