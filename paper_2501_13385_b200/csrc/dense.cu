@@ -1118,18 +1118,32 @@ __global__ void __launch_bounds__(kProjThreads) k_project(DenseArgs a) {
                      : (U[(aa - r0) * nk + x] - alpha * Ah[(aa - r0) * nk + x]) * inv;
     }
   } else {
+    // one thread per source entry (a, x, c) of U / Ahat writes its four B_k entries
+    // [[U, 0], [-alpha Ahat, U]] / phi; four entries per thread in flight (one CTA per core:
+    // the 16 x 256 x 16 core of config 3 was latency-bound here)
     const int Rb1 = 2 * r1;
-    const int tot = 2 * r0 * nk * Rb1;
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-      const int c = e % Rb1;
-      const int x = (e / Rb1) % nk;
-      const int aa = e / (Rb1 * nk);
-      const double inv = inv_of(x);
-      double v;
-      if (aa < r0) v = c < r1 ? U[(aa * nk + x) * r1 + c] * inv : 0.0;
-      else if (c < r1) v = -alpha * Ah[((aa - r0) * nk + x) * r1 + c] * inv;
-      else v = U[((aa - r0) * nk + x) * r1 + (c - r1)] * inv;
-      B[e] = v;
+    const int tot = r0 * nk * r1;
+    const int64_t half = (int64_t)r0 * nk * Rb1;   // offset of the bottom block row
+    for (int e0 = threadIdx.x; e0 < tot; e0 += 4 * blockDim.x) {
+      double u[4], h[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = e0 + q * blockDim.x;
+        u[q] = e < tot ? U[e] : 0.0;
+        h[q] = e < tot ? Ah[e] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = e0 + q * blockDim.x;
+        if (e >= tot) break;
+        const int c = e % r1, ax = e / r1, x = ax % nk;
+        const double inv = inv_of(x);
+        const int64_t o = (int64_t)ax * Rb1 + c;     // (a, x, c) in the top block row
+        B[o] = u[q] * inv;
+        B[o + r1] = 0.0;
+        B[half + o] = -alpha * h[q] * inv;
+        B[half + o + r1] = u[q] * inv;
+      }
     }
   }
 }
