@@ -446,7 +446,12 @@ DenseArgs dense_args(tt_ctx* ctx) {
   a.B = ctx->B;
   a.work = ctx->work;
   a.work_len = ctx->work_len;
-  a.clw = ctx->clw;
+  // PRGD_NO_CLUSTER=1: the one-CTA dense kernels instead of the 8-CTA cluster ones (A/B only)
+  static const bool no_cluster = [] {
+    const char* e = getenv("PRGD_NO_CLUSTER");
+    return e && e[0] == '1';
+  }();
+  a.clw = no_cluster ? nullptr : ctx->clw;
   a.clw_len = ctx->clw_len;
   a.sc = ctx->sc;
   a.smem_doubles = dense_smem_doubles();

@@ -1315,9 +1315,19 @@ bool round_cluster_ok(int d, const int* r) {
   return S <= 32;
 }
 
+// A4-A6 on one CTA (Householder sweep) when every unfolding is tiny: measured faster than the
+// 8-CTA cluster (cluster barriers per stage) for configs 1, 4 and 6 (dense_orth 0.041 / 0.382 /
+// 0.139 ms -> 0.028 / 0.336 / 0.103), equal for config 2 (r_{k-1} n_k = 250).
+bool orth_one_cta(const DenseArgs& a) {
+  int mx = 0;
+  for (int k = 0; k < a.d; ++k) mx = a.r[k] * a.n[k] > mx ? a.r[k] * a.n[k] : mx;
+  return mx <= 64;
+}
+
 void launch_dense_orth(cudaStream_t s, const DenseArgs& a, int64_t* launches) {
   const size_t bytes = (size_t)a.smem_doubles * sizeof(double);
-  if (!(a.clw && launch_orth_cs(s, a, bytes))) k_dense_orth<<<1, kDenseThreads, bytes, s>>>(a);
+  if (orth_one_cta(a) || !(a.clw && launch_orth_cs(s, a, bytes)))
+    k_dense_orth<<<1, kDenseThreads, bytes, s>>>(a);
   ++*launches;
 }
 
