@@ -136,6 +136,8 @@ struct tt_ctx {
   cudaStream_t side = nullptr;               // uploads overlapped with the bucketing sorts
   cudaStream_t cap = nullptr;                // private graph-capture stream
   cudaEvent_t ev_side[2] = {nullptr, nullptr};
+  cudaStream_t ovl = nullptr;                // pass-B suffix branch beside the end of A5 / A6
+  cudaEvent_t ev_ovl[2] = {nullptr, nullptr};
 
   bool base_ready = false;
   int* n_dev = nullptr;
@@ -502,23 +504,24 @@ void grp(tt_ctx* ctx, int id, bool begin) {
 // ------------------------------------------------------------------ enqueue pieces
 // Tables of the left / right parts: left levels 1..K_L, right levels
 // d-1..K_L (the U tables scaled by psi at the split level).
-void enqueue_tables(tt_ctx* ctx, bool useU, int64_t* lc) {
+// `sides`: bit 0 the left levels, bit 1 the right levels; `st` the stream (default ctx->stream).
+void enqueue_tables(tt_ctx* ctx, bool useU, int64_t* lc, int sides = 3, cudaStream_t st = nullptr) {
   const int d = ctx->d, KL = ctx->plan.KL;
-  cudaStream_t s = ctx->stream;
+  cudaStream_t s = st ? st : ctx->stream;
   const double* cores = useU ? ctx->U : ctx->C;
   const Scalars* sc = useU ? ctx->sc : nullptr;
   const int lmax = KL, rmin = KL;
   std::vector<TableLevel> L, R;
   bool ok = true;
   // left levels 1..lmax (A_{k+1} from A_k and core k), right levels d-1..rmin
-  for (int k = 0; k < lmax; ++k) {
+  for (int k = 0; k < lmax && (sides & 1); ++k) {
     TableLevel t{true, k == 0 ? nullptr : ctx->LT[k], ctx->ldr[k], cores + ctx->core_off[k],
                  (int)ctx->r[k], (int)ctx->n[k], (int)ctx->r[k + 1], ctx->LT[k + 1], ctx->ldr[k + 1],
                  ctx->NLk[k + 1], (useU && k + 1 == KL) ? ctx->psiL : nullptr};
     ok = ok && level_tab_ok(t.r0, t.nk, t.r1, t.ld_out);
     L.push_back(t);
   }
-  for (int k = d - 1; k >= rmin; --k) {
+  for (int k = d - 1; k >= rmin && (sides & 2); --k) {
     TableLevel t{false, k == d - 1 ? nullptr : ctx->RT[k + 1], ctx->ldr[k + 1],
                  cores + ctx->core_off[k], (int)ctx->r[k], (int)ctx->n[k], (int)ctx->r[k + 1],
                  ctx->RT[k], ctx->ldr[k], ctx->NRk[k], (useU && k == KL) ? ctx->psiR : nullptr};
@@ -726,8 +729,27 @@ void enqueue_update(tt_ctx* ctx, int64_t* lc, int part = 0) {
                ctx->plan.NR, ctx->psiL, ctx->psiR, ctx->sc, lc);
   grp(ctx, 4, false);
   DenseArgs da = dense_args(ctx);
+  // Overlap (table path, cluster A4-A6): the left tables of U and pass B's suffix-order SpMM
+  // need only the cores < K_L, which the A5 sweep finishes first, so they run on a second
+  // stream beside the rest of A5 and A6 (k_orth_cs split in two launches, identical
+  // arithmetic).  Direct (profiling) runs keep the sequential order for the group timers.
+  static const bool no_overlap = [] {
+    const char* e = getenv("PRGD_NO_OVERLAP");
+    return e && e[0] == '1';
+  }();
+  const bool ovl = !no_overlap && !ctx->profiling && !ctx->plan.chain && orth_cluster_ok(da) &&
+                   ctx->obs_set;
+  if (ovl && !ctx->ovl) {
+    cudaStreamCreateWithFlags(&ctx->ovl, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&ctx->ev_ovl[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->ev_ovl[1], cudaEventDisableTiming);
+  }
+  DenseArgs da1 = da, da2 = da;
+  da1.orth_part = 1;
+  da2.orth_part = 2;
+  da1.orth_split = da2.orth_split = KL;
   grp(ctx, 5, true);
-  launch_dense_orth(s, da, lc);
+  launch_dense_orth(s, ovl ? da1 : da, lc);
   grp(ctx, 5, false);
   if (ctx->plan.chain) {   // pass B by per-sample chains (A7-A8), segmented contraction (A9)
     grp(ctx, 7, true);
@@ -738,9 +760,11 @@ void enqueue_update(tt_ctx* ctx, int64_t* lc, int part = 0) {
     launch_chain_contract(s, ctx->pcs, ctx->ctt, ctx->m, ctx->ghat, ctx->IL, ctx->IR, ctx->Y, ctx->sc, lc);
     grp(ctx, 9, false);
   } else {
-  grp(ctx, 6, true);
-  enqueue_tables(ctx, true, lc);
-  grp(ctx, 6, false);
+  if (!ovl) {
+    grp(ctx, 6, true);
+    enqueue_tables(ctx, true, lc);
+    grp(ctx, 6, false);
+  }
   grp(ctx, 7, true);
   {
   SegArgs a{};
@@ -752,9 +776,6 @@ void enqueue_update(tt_ctx* ctx, int64_t* lc, int part = 0) {
   a.coltab = ctx->RT[KL];
   a.rowscale = ctx->psiL;
   a.out = ctx->EL[KL];
-  launch_seg(s, a, ctx->sc, lc);
-  grp(ctx, 7, false);
-  grp(ctx, 8, true);
   SegArgs b{};
   b.plan = &ctx->planR;
   b.mode = kSPMM;
@@ -764,7 +785,24 @@ void enqueue_update(tt_ctx* ctx, int64_t* lc, int part = 0) {
   b.coltab = ctx->LT[KL];
   b.rowscale = ctx->psiR;
   b.out = ctx->FR[KL];
-  launch_seg(s, b, ctx->sc, lc);
+  if (ovl) {
+    // s: rest of A5 + A6 (launched first, highest priority), right tables, pass B prefix;
+    // ctx->ovl: left tables, pass B suffix; joined before the backward recursions
+    cudaEventRecord(ctx->ev_ovl[0], s);
+    launch_dense_orth(s, da2, lc);
+    cudaStreamWaitEvent(ctx->ovl, ctx->ev_ovl[0], 0);
+    enqueue_tables(ctx, true, lc, 1, ctx->ovl);
+    launch_seg(ctx->ovl, b, ctx->sc, lc);
+    cudaEventRecord(ctx->ev_ovl[1], ctx->ovl);
+    enqueue_tables(ctx, true, lc, 2, s);
+    launch_seg(s, a, ctx->sc, lc);
+    cudaStreamWaitEvent(s, ctx->ev_ovl[1], 0);
+  } else {
+    launch_seg(s, a, ctx->sc, lc);
+    grp(ctx, 7, false);
+    grp(ctx, 8, true);
+    launch_seg(s, b, ctx->sc, lc);
+  }
   grp(ctx, 8, false);
   }
   grp(ctx, 9, true);
@@ -881,7 +919,7 @@ int run_piece(tt_ctx* ctx, int piece) {
     ctx->capturing = false;
     ctx->stream = launch_stream;
     if (e != cudaSuccess) return cuda_fail(ctx, e, "graph capture");
-    e = cudaGraphInstantiate(ge, graph, 0);
+    e = cudaGraphInstantiate(ge, graph, cudaGraphInstantiateFlagUseNodePriority);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "graph instantiate");
     *nl = lc;
@@ -1220,6 +1258,9 @@ int tt_destroy(tt_ctx* ctx) {
   if (ctx->cap) cudaStreamDestroy(ctx->cap);
   for (cudaEvent_t e : ctx->ev_side)
     if (e) cudaEventDestroy(e);
+  if (ctx->ovl) cudaStreamDestroy(ctx->ovl);
+  for (cudaEvent_t e : ctx->ev_ovl)
+    if (e) cudaEventDestroy(e);
   delete ctx;
   return TT_OK;
 }
@@ -1376,17 +1417,22 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
       dfree_all(ctx, OL);
       return fail(ctx, TT_ERR_INDEX, "an observed index is outside [0, n_k)");
     }
-    uint64_t* ko;
-    uint32_t* vo;
+    // Both sorts run while the values are still on the link: the suffix sort takes as its
+    // scratch the pair the prefix sort's result does not occupy, and only the two
+    // after-sort kernels (which read y / the prefix inverse) wait for the value upload.
+    uint64_t *ko, *ko2;
+    uint32_t *vo, *vo2;
     radix_sort_pairs(s, kpre, vals, ktmp, vtmp, m, bitsVP + bitsS, hist, hl, &ko, &vo, &lc);
+    ptm.mark("sort_pre");
+    radix_sort_pairs(s, ksuf, vals2, ko == ktmp ? kpre : ktmp, vo == vtmp ? vals : vtmp, m,
+                     bitsVS + bitsP, hist, hl, &ko2, &vo2, &lc);
+    ptm.mark("sort_suf");
     CK(cudaStreamWaitEvent(s, ctx->ev_side[1], 0));
     launch_after_sort_pre(s, ko, vo, m, bitsS, NLv, y_orig, ctx->Spre, ctx->ypre, ctx->sid_pre, inv,
                           ctx->offsL, ctx->Ppre, &lc);
-    ptm.mark("sort_pre");
-    radix_sort_pairs(s, ksuf, vals2, ktmp, vtmp, m, bitsVS + bitsP, hist, hl, &ko, &vo, &lc);
-    launch_after_sort_suf(s, ko, vo, m, bitsP, NRv, inv, ctx->pos_suf, ctx->Psuf, ctx->sid_suf,
+    launch_after_sort_suf(s, ko2, vo2, m, bitsP, NRv, inv, ctx->pos_suf, ctx->Psuf, ctx->sid_suf,
                           ctx->pre2suf, ctx->offsR, &lc);
-    ptm.mark("sort_suf");
+    ptm.mark("after_sorts");
   } else {
     CK(cudaMemsetAsync(ctx->offsL, 0, (NLv + 1) * sizeof(int64_t), s));
     CK(cudaMemsetAsync(ctx->offsR, 0, (NRv + 1) * sizeof(int64_t), s));

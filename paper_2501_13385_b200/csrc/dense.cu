@@ -1324,10 +1324,21 @@ bool orth_one_cta(const DenseArgs& a) {
   return mx <= 64;
 }
 
+// True when A4-A6 run on the cluster kernel, the only one that takes a split launch
+// (DenseArgs::orth_part).
+bool orth_cluster_ok(const DenseArgs& a) {
+  int S = 2;
+  for (int k = 0; k <= a.d; ++k) S = a.r[k] > S ? a.r[k] : S;
+  return a.clw != nullptr && S <= 32 && !orth_one_cta(a);
+}
+
 void launch_dense_orth(cudaStream_t s, const DenseArgs& a, int64_t* launches) {
   const size_t bytes = (size_t)a.smem_doubles * sizeof(double);
-  if (orth_one_cta(a) || !(a.clw && launch_orth_cs(s, a, bytes)))
+  if (a.orth_part != 0) {   // caller checked orth_cluster_ok
+    launch_orth_cs(s, a, bytes);
+  } else if (orth_one_cta(a) || !(a.clw && launch_orth_cs(s, a, bytes))) {
     k_dense_orth<<<1, kDenseThreads, bytes, s>>>(a);
+  }
   ++*launches;
 }
 

@@ -89,6 +89,8 @@ struct DenseArgs {
   int wretr;         // 1: weighted retraction W^{-1/2} SVD_r^tt W^{1/2}
   double* vwarm;     // [2][d][32*32] the truncation Jacobi's last rotation per bond (warm start) or null
   int* wok;          // [2][d] 1: the slot holds a converged rotation
+  int orth_part;     // k_orth_cs: 0 all of A4-A6; 1 A4 + A5 for cores < orth_split; 2 the rest
+  int orth_split;    //   (part 1's cores are final when it ends: their tables can start)
 };
 
 // ------------------------------------------------------------------ kernels (launchers)
@@ -242,6 +244,7 @@ void launch_gather_sq_sum(cudaStream_t s, const double* h0, int n0, Scalars* sc,
 
 // dense.cu
 void launch_dense_orth(cudaStream_t s, const DenseArgs& a, int64_t* launches);
+bool orth_cluster_ok(const DenseArgs& a);
 void launch_dense_round(cudaStream_t s, const DenseArgs& a, int64_t* launches);
 // k_project alone (mode: 1 projection + adaptive numerator, 2 assembly with sc->alpha) and the
 // rounding alone (adaptive step: alpha is known only after the D pass)
