@@ -154,6 +154,13 @@ struct tt_ctx {
   double *HL = nullptr, *HR = nullptr, *psiL = nullptr, *psiR = nullptr, *Ypart = nullptr;
   double* margp = nullptr;      // marginal chunk partials, 32 * sum(n)
   double* g_suf = nullptr;      // residual in suffix order (written by pass A)
+  // sliced pass A suffix (gsq_q >= 2 slices of g of gsq_slen samples): the sliced order's
+  // prefix positions / suffix buckets, its index of every suffix-ordered sample, the staged g
+  // (sliced order, read by pass B through sl_q) and the per-slice bucket sums
+  int gsq_q = 0;
+  int64_t gsq_slen = 0;
+  int32_t *sl_pos = nullptr, *sl_row = nullptr, *sl_q = nullptr;
+  double *stage = nullptr, *HRq = nullptr;
   int32_t* pre2suf = nullptr;   // suffix position of prefix position t
   int64_t Ypart_cap = 0;
 
@@ -246,6 +253,8 @@ void dfree_all(tt_ctx* ctx, std::vector<void*>& list) {
 }
 
 // Diagnostic host wall-clock phases (env PRGD_TIMING=1): each mark synchronises the stream.
+constexpr int64_t kGsqSliceBytes = 48ll << 20;   // g bytes per slice of the sliced pass A suffix
+
 struct PhaseTimer {
   cudaStream_t s;
   const char* name;
@@ -577,7 +586,15 @@ void enqueue_evaluate(tt_ctx* ctx, int64_t* lc, bool with_sumsq = true) {
     }
     grp(ctx, 1, false);
     grp(ctx, 2, true);
-    {
+    if (ctx->gsq_q >= 2) {
+      for (int q = 0; q < ctx->gsq_q; ++q) {
+        const int64_t off = q * ctx->gsq_slen;
+        const int64_t mq = std::min<int64_t>(ctx->gsq_slen, ctx->m - off);
+        launch_flat_gsq(s, ctx->sl_row + off, ctx->sl_pos + off, ctx->g, std::max<int64_t>(mq, 0),
+                        ctx->plan.NR, ctx->stage + off, ctx->HRq + q * ctx->plan.NR, ctx->frec, lc);
+      }
+      launch_sum_slices(s, ctx->HRq, ctx->gsq_q, ctx->plan.NR, ctx->HR, lc);
+    } else {
       SegArgs b{};
       b.plan = &ctx->planR;
       b.mode = kGSQ;
@@ -781,7 +798,8 @@ void enqueue_update(tt_ctx* ctx, int64_t* lc, int part = 0) {
   b.mode = kSPMM;
   b.ld = ctx->ldr[KL];
   b.col = ctx->Psuf;
-  b.g = ctx->g_suf;
+  b.g = ctx->gsq_q >= 2 ? ctx->stage : ctx->g_suf;
+  b.perm = ctx->gsq_q >= 2 ? ctx->sl_q : nullptr;
   b.coltab = ctx->LT[KL];
   b.rowscale = ctx->psiR;
   b.out = ctx->FR[KL];
@@ -1366,13 +1384,28 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
   int32_t* inv = nullptr;
   int* hist = nullptr;
   const int64_t hl = radix_hist_len(m);
+  // pass A suffix by slices of g when g exceeds one slice (~48 MB, L2-resident gathers);
+  // PRGD_GSQ_SLICES=Q forces Q slices (1: the row-plan gather), read per call (tests)
+  {
+    const char* e = getenv("PRGD_GSQ_SLICES");
+    int64_t q = (m * 8 + kGsqSliceBytes - 1) / kGsqSliceBytes;
+    if (e && *e) q = std::atoll(e);
+    q = std::max<int64_t>(1, std::min<int64_t>(q, 256));
+    if (m < 64 * q) q = 1;
+    ctx->gsq_q = q >= 2 ? (int)q : 0;
+    ctx->gsq_slen = ctx->gsq_q ? (m + q - 1) / q : 0;
+  }
+  const bool sliced = ctx->gsq_q >= 2;
   bool ok = A(ctx, &idx_dev, m * d, OL) && A(ctx, &y_orig, m, tmp) && A(ctx, &kpre, m, tmp) &&
             A(ctx, &ksuf, m, tmp) && A(ctx, &ktmp, m, tmp) && A(ctx, &vals, m, tmp) &&
             A(ctx, &vals2, m, tmp) && A(ctx, &vtmp, m, tmp) && A(ctx, &inv, m, tmp) &&
             A(ctx, &hist, hl, tmp) && A(ctx, &ctx->Spre, m + 8, OL) && A(ctx, &ctx->ypre, m + 8, OL) &&
             A(ctx, &ctx->g, m + 8, OL) && A(ctx, &ctx->sid_pre, m, OL) && A(ctx, &ctx->pos_suf, m, OL) &&
             A(ctx, &ctx->Psuf, m + 8, OL) && A(ctx, &ctx->sid_suf, m, OL) &&
-            A(ctx, &ctx->g_suf, m + 8, OL) && A(ctx, &ctx->pre2suf, m, OL) &&
+            (sliced || A(ctx, &ctx->g_suf, m + 8, OL)) && A(ctx, &ctx->pre2suf, m, OL) &&
+            (!sliced || (A(ctx, &ctx->sl_pos, m, OL) && A(ctx, &ctx->sl_row, m, OL) &&
+                         A(ctx, &ctx->sl_q, m, OL) && A(ctx, &ctx->stage, m + 8, OL) &&
+                         A(ctx, &ctx->HRq, ctx->gsq_q * NRv, OL))) &&
             A(ctx, &ctx->offsL, NLv + 1 + 40, OL) && A(ctx, &ctx->offsR, NRv + 1 + 40, OL) &&
             A(ctx, &ctx->Ppre, m + 8, OL) &&
             A(ctx, reinterpret_cast<char**>(&ctx->frec), flat_rec_bytes(m), OL) &&
@@ -1433,6 +1466,15 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
     launch_after_sort_suf(s, ko2, vo2, m, bitsP, NRv, inv, ctx->pos_suf, ctx->Psuf, ctx->sid_suf,
                           ctx->pre2suf, ctx->offsR, &lc);
     ptm.mark("after_sorts");
+    if (sliced) {   // scratch: the key buffers other than ko2, all value buffers
+      uint64_t* kf[2];
+      int nf = 0;
+      for (uint64_t* kb : {kpre, ktmp, ksuf})
+        if (kb != ko2 && nf < 2) kf[nf++] = kb;
+      launch_slice_setup(s, ctx->pos_suf, ko2, bitsP, m, ctx->gsq_slen, ctx->gsq_q, kf[0], vals, kf[1],
+                         vtmp, hist, hl, ctx->sl_pos, ctx->sl_row, ctx->sl_q, &lc);
+      ptm.mark("slices");
+    }
   } else {
     CK(cudaMemsetAsync(ctx->offsL, 0, (NLv + 1) * sizeof(int64_t), s));
     CK(cudaMemsetAsync(ctx->offsR, 0, (NRv + 1) * sizeof(int64_t), s));

@@ -498,6 +498,13 @@ __global__ void __launch_bounds__(32 * kPipeWarps) k_spmm_pipe(SegDev a, const S
   int slot = __shfl_sync(kFull, rec.w, 0);
   double2 acc = make_double2(0.0, 0.0);
 
+  // with a permutation (the staged g of the sliced pass A suffix) the index of chunk c + 2 is
+  // loaded while chunk c runs, so the dependent g load of chunk c + 1 issues without waiting on it
+  auto ld_p = [&](int c) -> int {
+    const int t = S0 + 32 * c + lane;
+    return (c < nch && t < S1) ? a.perm[t] : -1;
+  };
+  int pN = a.perm ? ld_p(1) : -1;
   double gC = ld_g(0);
 #pragma unroll
   for (int j = 0; j + 1 < NB; ++j) {   // chunks 0 .. NB-2 in flight
@@ -507,7 +514,13 @@ __global__ void __launch_bounds__(32 * kPipeWarps) k_spmm_pipe(SegDev a, const S
   int colN = ld_col(NB - 1);
   for (int c = 0; c < nch; ++c) {
     const int colNN = ld_col(c + NB);
-    const double gN = ld_g(c + 1);
+    double gN;
+    if (a.perm) {
+      gN = pN >= 0 ? a.g[pN] : 0.0;
+      pN = ld_p(c + 2);
+    } else {
+      gN = ld_g(c + 1);
+    }
     if (c + NB - 1 < nch) issue(c + NB - 1, colN);
     pipe_commit();
     double* gc = gsm + (c % NB) * 32;

@@ -37,6 +37,50 @@ struct Rec {
   int8_t* full;        // the chunk lies inside one bucket that began before and continues after it
 };
 
+// Segmented bucket sums of one 32-sample chunk (lane = sample, v its g^2, rv its bucket; buckets
+// nondecreasing): a segmented warp scan, complete buckets written, straddling ones left as chunk
+// records for k_flat_fix, empty buckets written as zeros.
+__device__ __forceinline__ void seg_bucket_sums(int lane, bool have, double v, int rv, int prev, int next,
+                                                int64_t c, int64_t t, int64_t m, int64_t nrows,
+                                                double* __restrict__ H, const Rec& rec) {
+  const int key = have ? rv : -2;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {            // segmented inclusive scan (buckets contiguous)
+    const double yo = __shfl_up_sync(kFull, v, o);
+    const int ko = __shfl_up_sync(kFull, key, o);
+    if (lane >= o && ko == key) v += yo;
+  }
+  const int kup = __shfl_up_sync(kFull, key, 1), kdn = __shfl_down_sync(kFull, key, 1);
+  const int kprev = lane == 0 ? prev : kup;
+  const int knext = lane == 31 ? next : (kdn == -2 ? -1 : kdn);
+  const unsigned valid = __ballot_sync(kFull, have);
+  const int last = 31 - __clz(valid);                          // last valid lane of the chunk
+  const unsigned ends = __ballot_sync(kFull, have && (key != knext || lane == last));
+  const int first_end = __ffs(ends) - 1;                       // end lane of the first segment
+  if (have) {
+    if (key != kprev)                                          // empty buckets before this one
+      for (int bb = kprev + 1; bb < key; ++bb) H[bb] = 0.0;
+    if ((ends >> lane) & 1u) {
+      // the segment ending here began in the chunk unless it is the first one and continued
+      const bool began = lane != first_end || key != prev;
+      const bool finishes = key != knext;
+      if (began && finishes) H[key] = v;
+      if (lane == first_end) {
+        rec.head_row[c] = began ? -1 : key;
+        rec.head[c] = began ? 0.0 : v;
+        rec.full[c] = (!began && !finishes) ? 1 : 0;
+      }
+      if (lane == last) {
+        const bool tl = began && !finishes;
+        rec.tail_row[c] = tl ? key : -1;
+        rec.tail[c] = tl ? v : 0.0;
+      }
+      if (t == m - 1)                                          // empty buckets after the last sample
+        for (int64_t bb = (int64_t)key + 1; bb < nrows; ++bb) H[bb] = 0.0;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ SDDMM (A1-A2) + H_L (A3)
 // g[t] = rowtab[row[t]] . coltab[col[t]] - y[t],  H[b] = sum_{row[t] = b} g[t]^2.  LPS lanes per
 // sample, V double2 per lane (ld = 2 LPS V); per 32-sample chunk: lane-parallel loads of
@@ -101,43 +145,32 @@ __global__ void __launch_bounds__(kFT, 4) k_flat_sddmm(const int32_t* __restrict
     if (c * 32 + tt < m) g[c * 32 + tt] = gv;
     // natural order: sample `lane` was finished by lane (lane % G) * LPS + lane / G
     const double gn = __shfl_sync(kFull, gv, (lane % G) * LPS + lane / G);
-    double v = have ? gn * gn : 0.0;
-    const int key = have ? rv : -2;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {            // segmented inclusive scan (buckets contiguous)
-      const double yo = __shfl_up_sync(kFull, v, o);
-      const int ko = __shfl_up_sync(kFull, key, o);
-      if (lane >= o && ko == key) v += yo;
-    }
-    const int kup = __shfl_up_sync(kFull, key, 1), kdn = __shfl_down_sync(kFull, key, 1);
-    const int kprev = lane == 0 ? prev : kup;
-    const int knext = lane == 31 ? next : (kdn == -2 ? -1 : kdn);
-    const unsigned valid = __ballot_sync(kFull, have);
-    const int last = 31 - __clz(valid);                          // last valid lane of the chunk
-    const unsigned ends = __ballot_sync(kFull, have && (key != knext || lane == last));
-    const int first_end = __ffs(ends) - 1;                       // end lane of the first segment
-    if (have) {
-      if (key != kprev)                                          // empty buckets before this one
-        for (int bb = kprev + 1; bb < key; ++bb) H[bb] = 0.0;
-      if ((ends >> lane) & 1u) {
-        // the segment ending here began in the chunk unless it is the first one and continued
-        const bool began = lane != first_end || key != prev;
-        const bool finishes = key != knext;
-        if (began && finishes) H[key] = v;
-        if (lane == first_end) {
-          rec.head_row[c] = began ? -1 : key;
-          rec.head[c] = began ? 0.0 : v;
-          rec.full[c] = (!began && !finishes) ? 1 : 0;
-        }
-        if (lane == last) {
-          const bool tl = began && !finishes;
-          rec.tail_row[c] = tl ? key : -1;
-          rec.tail[c] = tl ? v : 0.0;
-        }
-        if (t == m - 1)                                          // empty buckets after the last sample
-          for (int64_t bb = (int64_t)key + 1; bb < nrows; ++bb) H[bb] = 0.0;
-      }
-    }
+    seg_bucket_sums(lane, have, have ? gn * gn : 0.0, rv, prev, next, c, t, m, nrows, H, rec);
+  }
+}
+
+// ------------------------------------------------------------------ pass A suffix, one slice
+// Suffix-order residuals by slices of g ("pass A suffix"): over one slice's
+// samples (suffix order restricted to the samples whose prefix position lies in the slice, so
+// every gather hits a ~48 MB window of g that stays in L2) stage[t] = g[pos[t]] and the slice's
+// bucket sums H[b] = sum_{row[t] = b} stage[t]^2 (rows nondecreasing within a slice).
+__global__ void __launch_bounds__(kFT) k_flat_gsq(const int32_t* __restrict__ row,
+                                                 const int32_t* __restrict__ pos,
+                                                 const double* __restrict__ g, int64_t m, int64_t nrows,
+                                                 double* __restrict__ stage, double* __restrict__ H,
+                                                 Rec rec) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)kFT + threadIdx.x) >> 5;
+  const int64_t nw = (gridDim.x * (int64_t)kFT) >> 5;
+  for (int64_t c = w0; c * 32 < m; c += nw) {
+    const int64_t t = c * 32 + lane;
+    const bool have = t < m;
+    const int rv = have ? row[t] : 0;
+    const double gv = have ? __ldg(g + pos[t]) : 0.0;
+    if (have) stage[t] = gv;
+    const int prev = c == 0 ? -1 : row[c * 32 - 1];
+    const int next = c * 32 + 32 < m ? row[c * 32 + 32] : -1;
+    seg_bucket_sums(lane, have, gv * gv, rv, prev, next, c, t, m, nrows, H, rec);
   }
 }
 
@@ -172,7 +205,36 @@ void sddmm_launch(cudaStream_t s, const FlatArgs& a, const Rec& rec, unsigned gr
                                             a.out, rec);
 }
 
+// H[b] = sum_q Hq[q][b] in slice order (deterministic).
+__global__ void k_sum_slices(const double* __restrict__ Hq, int nq, int64_t n, double* __restrict__ H) {
+  const int64_t b = blockIdx.x * (int64_t)kFT + threadIdx.x;
+  if (b >= n) return;
+  double acc = Hq[b];
+  for (int q = 1; q < nq; ++q) acc += Hq[(int64_t)q * n + b];
+  H[b] = acc;
+}
+
 }  // namespace
+
+void launch_sum_slices(cudaStream_t s, const double* Hq, int nq, int64_t n, double* H, int64_t* launches) {
+  k_sum_slices<<<cdiv(n, kFT), kFT, 0, s>>>(Hq, nq, n, H);
+  ++*launches;
+}
+
+void launch_flat_gsq(cudaStream_t s, const int32_t* row, const int32_t* pos, const double* g, int64_t m,
+                     int64_t nrows, double* stage, double* H, void* recbuf, int64_t* launches) {
+  if (m <= 0) {
+    cudaMemsetAsync(H, 0, (size_t)nrows * sizeof(double), s);
+    return;
+  }
+  const int64_t nc = (m + 31) / 32;
+  const Rec rec = make_rec(recbuf, nc);
+  const int64_t cap = 148 * 8 * (kFT / 32) * 4;
+  const unsigned grid = cdiv((nc < cap ? nc : cap) * 32, kFT);
+  k_flat_gsq<<<grid, kFT, 0, s>>>(row, pos, g, m, nrows, stage, H, rec);
+  k_flat_fix<<<cdiv(nc, kFT), kFT, 0, s>>>(rec, nc, H);
+  *launches += 2;
+}
 
 int64_t flat_rec_bytes(int64_t m) {
   const int64_t nc = (m + 31) / 32 + 1;

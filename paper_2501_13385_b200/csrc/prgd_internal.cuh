@@ -102,6 +102,10 @@ void radix_sort_pairs(cudaStream_t s, uint64_t* keys, uint32_t* vals, uint64_t* 
                       uint32_t* vals_tmp, int64_t m, int bits, int* hist_buf, int64_t hist_len,
                       uint64_t** keys_out, uint32_t** vals_out, int64_t* launches);
 int64_t radix_hist_len(int64_t m);
+void launch_slice_setup(cudaStream_t s, const int32_t* pos_suf, const uint64_t* keys_suf, int bitsP,
+                        int64_t m, int64_t slen, int nslices, uint64_t* kbuf, uint32_t* vbuf,
+                        uint64_t* ktmp, uint32_t* vtmp, int* hist, int64_t hist_len, int32_t* sl_pos,
+                        int32_t* sl_row, int32_t* sl_q, int64_t* launches);
 void launch_after_sort_pre(cudaStream_t s, const uint64_t* keys, const uint32_t* sids, int64_t m,
                            int bitsS, int64_t NL, const double* y_orig, int32_t* Spre,
                            double* ypre, int32_t* sid_pre, int32_t* inv, int64_t* offsL,
@@ -226,6 +230,11 @@ struct FlatArgs {
 };
 int64_t flat_rec_bytes(int64_t m);
 void launch_flat_sddmm(cudaStream_t s, const FlatArgs& a, int64_t* launches);
+// pass A suffix by slices of g (stage[t] = g[pos[t]], bucket sums of stage^2 into H) and the sum
+// of the per-slice bucket sums
+void launch_flat_gsq(cudaStream_t s, const int32_t* row, const int32_t* pos, const double* g, int64_t m,
+                     int64_t nrows, double* stage, double* H, void* recbuf, int64_t* launches);
+void launch_sum_slices(cudaStream_t s, const double* Hq, int nq, int64_t n, double* H, int64_t* launches);
 // n_host / phi_off_host are HOST arrays (values are passed by kernel argument).
 // scratch: >= 32 * (sum of the nmodes mode sizes) doubles
 void launch_marginals(cudaStream_t s, const double* H, int64_t N, int nmodes, const int* n_host,

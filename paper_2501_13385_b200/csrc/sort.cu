@@ -247,10 +247,49 @@ __global__ void k_after_suf(const uint64_t* __restrict__ keys, const uint32_t* _
     for (int64_t q = S + 1; q <= NR; ++q) offsR[q] = m;
 }
 
+// Slices of the suffix order for the sliced pass A suffix (passes_flat.cu k_flat_gsq): slice of
+// a suffix-ordered sample u = its prefix position / slen.
+__global__ void k_slice_keys(const int32_t* __restrict__ pos_suf, int64_t m, int64_t slen,
+                             uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (u >= m) return;
+  keys[u] = (uint64_t)(pos_suf[u] / slen);
+  vals[u] = (uint32_t)u;
+}
+
+// j-th sample of the sliced order (slice-major, suffix order within a slice) = suffix-ordered
+// sample u = vo[j]: its prefix position, its suffix bucket, and u -> j.
+__global__ void k_slice_order(const uint32_t* __restrict__ vo, const uint64_t* __restrict__ keys_suf,
+                              int bitsP, const int32_t* __restrict__ pos_suf, int64_t m,
+                              int32_t* __restrict__ sl_pos, int32_t* __restrict__ sl_row,
+                              int32_t* __restrict__ sl_q) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const uint32_t u = vo[j];
+  sl_pos[j] = pos_suf[u];
+  sl_row[j] = (int32_t)(keys_suf[u] >> bitsP);
+  sl_q[u] = (int32_t)j;
+}
+
 inline unsigned grid_for(int64_t n, int threads) {
   return (unsigned)((n + threads - 1) / threads);
 }
 }  // namespace
+
+void launch_slice_setup(cudaStream_t s, const int32_t* pos_suf, const uint64_t* keys_suf, int bitsP,
+                        int64_t m, int64_t slen, int nslices, uint64_t* kbuf, uint32_t* vbuf,
+                        uint64_t* ktmp, uint32_t* vtmp, int* hist, int64_t hist_len, int32_t* sl_pos,
+                        int32_t* sl_row, int32_t* sl_q, int64_t* launches) {
+  if (m <= 0) return;
+  k_slice_keys<<<grid_for(m, 256), 256, 0, s>>>(pos_suf, m, slen, kbuf, vbuf);
+  int bits = 1;
+  while ((1 << bits) < nslices) ++bits;
+  uint64_t* ko;
+  uint32_t* vo;
+  radix_sort_pairs(s, kbuf, vbuf, ktmp, vtmp, m, bits, hist, hist_len, &ko, &vo, launches);
+  k_slice_order<<<grid_for(m, 256), 256, 0, s>>>(vo, keys_suf, bitsP, pos_suf, m, sl_pos, sl_row, sl_q);
+  *launches += 2;
+}
 
 int64_t radix_hist_len(int64_t m) {
   int64_t nb = (m + kRsTile - 1) / kRsTile;

@@ -475,3 +475,35 @@ def test_rounding_weak_kept_direction(pkg, gap, seed):
           f"cross {int(e1[5 + 14] - e0[5 + 14])}, full {int(e1[5 + 19] - e0[5 + 19])}, "
           f"cert failures {int(e1[5 + 17] - e0[5 + 17])}")
     ctx.close()
+
+
+@pytest.mark.parametrize("cfg,m,nslices", [(5, 400_000, 3), (3, 200_000, 5), (2, None, 7), (4, 200_000, 2)])
+def test_sliced_suffix_pass(pkg, cfg, m, nslices, monkeypatch):
+    """Pass A suffix by slices of g (the default once g exceeds one ~48 MB slice, i.e. at config
+    5's full size) forced at oracle-sized inputs: H_R-based weights, pass B through the staged
+    g, one step and three steps against the oracle, and the same iterates as the row-plan
+    gather up to the summation order of H_R."""
+    pr, y, init = problem(cfg, m)
+    monkeypatch.setenv("PRGD_GSQ_SLICES", str(nslices))
+    ctx = context(pkg, pr, y, init)
+    monkeypatch.setenv("PRGD_GSQ_SLICES", "1")
+    ref_ctx = context(pkg, pr, y, init)
+    ctx.residual_norm()
+    ref, info = oracle.prgd_step(init, pr.idx, y, pr.n, pr.r, 1.0, return_info=True)
+    ctx.step(1.0)
+    ref_ctx.step(1.0)
+    eps = ctx.debug("eps")
+    assert eps[0] == pytest.approx(info["eps"], rel=1e-12)
+    assert eps[2] == pytest.approx(info["alpha"], rel=1e-12)
+    for k in range(pr.d):
+        np.testing.assert_allclose(ctx.debug("phi", k), info["phi"][k], rtol=1e-13)
+    assert oracle.tt_diff_norm(ctx.get_cores(), ref) <= 1e-11
+    assert oracle.tt_diff_norm(ctx.get_cores(), ref_ctx.get_cores()) <= 1e-13
+    step = 0.5 if cfg == 3 else 1.0
+    T = ref
+    for _ in range(2):
+        ctx.step(step)
+        T = oracle.prgd_step(T, pr.idx, y, pr.n, pr.r, step)
+    assert oracle.tt_diff_norm(ctx.get_cores(), T) <= 1e-10
+    ctx.close()
+    ref_ctx.close()
