@@ -133,6 +133,14 @@ PRGD_API int tt_get_path(tt_ctx* ctx, int* path);
  * Sets p = m / prod(n) (reading R3). */
 PRGD_API int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals, int64_t m);
 
+/* The same call for compact multi-indices (the same Omega): h_idx[m][d]
+ * sample-major uint8 (0-based), accepted when every n_k <= 256 (TT_ERR_ARG otherwise) -- true of
+ * all of BASELINE.json's configs (n_k = 2 .. 256).  The indices are a quarter of the int32
+ * bytes on the host link (config 5: 0.3 GB instead of 1.2 GB); they are widened to int32 on the
+ * device and then bucketed exactly as in tt_set_observations (same validation, same errors,
+ * same resulting state).  h_idx / h_vals are host pointers, read before the call returns. */
+PRGD_API int tt_set_observations_u8(tt_ctx* ctx, const uint8_t* h_idx, const double* h_vals, int64_t m);
+
 /* Copy core k (0 <= k < d) in/out, [r[k]][n[k]][r[k+1]] C-order float64.
  * Cores may be in any gauge; after tt_prgd_step cores 0..d-2 are left-orthogonal
  * (L(T_k)^T L(T_k) = I) and core d-1 carries the norm.

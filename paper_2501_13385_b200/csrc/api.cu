@@ -1075,7 +1075,19 @@ void apply_plan(tt_ctx* ctx, const Plan& pl) {
 // Observations on the chain path: the multi-indices stay in the ABI layout,
 // the values in the original order; A0 builds the per-mode buckets (stable radix sort of the
 // sample ids by x_k, k = 0..d-1) and cuts them into pieces of <= P samples.
-int set_obs_chain(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals, int64_t m) {
+// Host multi-indices -> idx_dev (int32): copied as they are, or (ib = 1, tt_set_observations_u8)
+// uploaded as bytes into `stage8` and widened on the device.
+cudaError_t upload_idx(cudaStream_t s, const void* h_idx, int ib, int64_t count, uint8_t* stage8,
+                       int32_t* idx_dev, int64_t* lc) {
+  if (ib == 4)
+    return cudaMemcpyAsync(idx_dev, h_idx, (size_t)count * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+  cudaError_t e = cudaMemcpyAsync(stage8, h_idx, (size_t)count, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return e;
+  launch_widen_u8(s, stage8, count, idx_dev, lc);
+  return cudaSuccess;
+}
+
+int set_obs_chain(tt_ctx* ctx, const void* h_idx, int ib, const double* h_vals, int64_t m) {
   const int d = ctx->d;
   auto& OL = ctx->obs_allocs;
   std::vector<void*> tmp;
@@ -1104,7 +1116,9 @@ int set_obs_chain(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals, int64
   long long* bsum = nullptr;
   const int64_t hl = radix_hist_len(m);
   const int64_t noffs = pc.nbuckets + d;
-  bool ok = A(ctx, &ctx->idx_dev, m * d, OL) && A(ctx, &ctx->yobs, m, OL) && A(ctx, &ctx->g, m, OL) &&
+  uint8_t* stage8 = nullptr;
+  bool ok = (ib == 4 || A(ctx, &stage8, m * d + 16, tmp)) &&
+            A(ctx, &ctx->idx_dev, m * d, OL) && A(ctx, &ctx->yobs, m, OL) && A(ctx, &ctx->g, m, OL) &&
             A(ctx, &ctx->ghat, m, OL) && A(ctx, &ctx->IL, iface, OL) && A(ctx, &ctx->IR, iface, OL) &&
             A(ctx, &pc.perm, (int64_t)d * m, OL) && A(ctx, &pc.offs, noffs, OL) &&
             A(ctx, &pc.pbase, pc.nbuckets + 1, OL) && (!adapt_by_chains(ctx) || A(ctx, &ctx->dval, m, OL)) &&
@@ -1120,7 +1134,7 @@ int set_obs_chain(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals, int64
   int64_t lc = 0;
   CK(cudaMemsetAsync(&ctx->sc->index_err, 0, sizeof(int), s));
   if (m > 0) {
-    CK(cudaMemcpyAsync(ctx->idx_dev, h_idx, (size_t)m * d * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    CK(upload_idx(s, h_idx, ib, m * d, stage8, ctx->idx_dev, &lc));
     CK(cudaMemcpyAsync(ctx->yobs, h_vals, (size_t)m * sizeof(double), cudaMemcpyHostToDevice, s));
     for (int k = 0; k < d; ++k) {
       int bits = 1;
@@ -1357,8 +1371,21 @@ int tt_get_core(tt_ctx* ctx, int k, double* h_core_out) {
   return read_scalars(ctx);
 }
 
+static int set_observations_impl(tt_ctx* ctx, const void* h_idx, int ib, const double* h_vals, int64_t m);
+
 int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals, int64_t m) {
   if (!ctx) return TT_ERR_ARG;
+  return set_observations_impl(ctx, h_idx, 4, h_vals, m);
+}
+
+int tt_set_observations_u8(tt_ctx* ctx, const uint8_t* h_idx, const double* h_vals, int64_t m) {
+  if (!ctx) return TT_ERR_ARG;
+  for (int k = 0; k < ctx->d; ++k)
+    if (ctx->n[k] > 256) return fail(ctx, TT_ERR_ARG, "byte indices need every n_k <= 256");
+  return set_observations_impl(ctx, h_idx, 1, h_vals, m);
+}
+
+static int set_observations_impl(tt_ctx* ctx, const void* h_idx, int ib, const double* h_vals, int64_t m) {
   PhaseTimer ptm(ctx->stream, "set_observations");
   if (m < 0 || m >= ((int64_t)1 << 31)) return fail(ctx, TT_ERR_ARG, "m must be in [0, 2^31)");
   if (m > 0 && (!h_idx || !h_vals)) return fail(ctx, TT_ERR_ARG, "NULL idx or vals");
@@ -1371,7 +1398,7 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
   ctx->evalValid = false;
   ctx->m = 0;
   ctx->idx_dev = nullptr;
-  if (ctx->plan.chain) return set_obs_chain(ctx, h_idx, h_vals, m);
+  if (ctx->plan.chain) return set_obs_chain(ctx, h_idx, ib, h_vals, m);
   const int d = ctx->d, KL = ctx->plan.KL;
   const int64_t NL = ctx->plan.NL, NR = ctx->plan.NR;
   const int64_t NLv = NL, NRv = NR;
@@ -1396,7 +1423,9 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
     ctx->gsq_slen = ctx->gsq_q ? (m + q - 1) / q : 0;
   }
   const bool sliced = ctx->gsq_q >= 2;
-  bool ok = A(ctx, &idx_dev, m * d, OL) && A(ctx, &y_orig, m, tmp) && A(ctx, &kpre, m, tmp) &&
+  uint8_t* stage8 = nullptr;
+  bool ok = (ib == 4 || A(ctx, &stage8, m * d + 16, tmp)) &&
+            A(ctx, &idx_dev, m * d, OL) && A(ctx, &y_orig, m, tmp) && A(ctx, &kpre, m, tmp) &&
             A(ctx, &ksuf, m, tmp) && A(ctx, &ktmp, m, tmp) && A(ctx, &vals, m, tmp) &&
             A(ctx, &vals2, m, tmp) && A(ctx, &vtmp, m, tmp) && A(ctx, &inv, m, tmp) &&
             A(ctx, &hist, hl, tmp) && A(ctx, &ctx->Spre, m + 8, OL) && A(ctx, &ctx->ypre, m + 8, OL) &&
@@ -1433,7 +1462,7 @@ int tt_set_observations(tt_ctx* ctx, const int32_t* h_idx, const double* h_vals,
     }
     // idx first on the main stream; the values follow on the side stream (the link carries one
     // copy at a time) while the keys are built and sorted; after_sort_pre waits for them.
-    CK(cudaMemcpyAsync(idx_dev, h_idx, (size_t)m * d * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    CK(upload_idx(s, h_idx, ib, m * d, stage8, idx_dev, &lc));
     CK(cudaEventRecord(ctx->ev_side[0], s));
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_side[0], 0));
     CK(cudaMemcpyAsync(y_orig, h_vals, (size_t)m * sizeof(double), cudaMemcpyHostToDevice, ctx->side));

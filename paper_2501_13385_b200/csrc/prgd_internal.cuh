@@ -98,6 +98,7 @@ struct DenseArgs {
 void launch_make_keys(cudaStream_t s, const int32_t* idx, int64_t m, int d, const int* n_dev,
                       int KL, int bitsP, int bitsS, uint64_t* kpre, uint64_t* ksuf, uint32_t* vals,
                       Scalars* sc, int64_t* launches);
+void launch_widen_u8(cudaStream_t s, const uint8_t* in, int64_t count, int32_t* out, int64_t* launches);
 void radix_sort_pairs(cudaStream_t s, uint64_t* keys, uint32_t* vals, uint64_t* keys_tmp,
                       uint32_t* vals_tmp, int64_t m, int bits, int* hist_buf, int64_t hist_len,
                       uint64_t** keys_out, uint32_t** vals_out, int64_t* launches);

@@ -298,6 +298,28 @@ int64_t radix_hist_len(int64_t m) {
   return len + 2 + 2 * ((len + kScanSeg - 1) / kScanSeg + 1);   // + segment sums (int64)
 }
 
+// Compact multi-indices (tt_set_observations_u8): one byte per index widened to the int32
+// layout every consumer reads; 16 indices per thread (one 16-byte load, four 16-byte stores).
+__global__ void k_widen_u8(const uint8_t* __restrict__ in, int64_t count, int32_t* __restrict__ out) {
+  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 16;
+  if (i + 16 <= count) {
+    const uint4 v = *reinterpret_cast<const uint4*>(in + i);
+    const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      *reinterpret_cast<int4*>(out + i + 4 * q) =
+          make_int4(w[q] & 255u, (w[q] >> 8) & 255u, (w[q] >> 16) & 255u, w[q] >> 24);
+  } else {
+    for (int64_t j = i; j < count; ++j) out[j] = in[j];
+  }
+}
+
+void launch_widen_u8(cudaStream_t s, const uint8_t* in, int64_t count, int32_t* out, int64_t* launches) {
+  if (count <= 0) return;
+  k_widen_u8<<<grid_for((count + 15) / 16, 256), 256, 0, s>>>(in, count, out);
+  ++*launches;
+}
+
 void launch_make_keys(cudaStream_t s, const int32_t* idx, int64_t m, int d, const int* n_dev,
                       int KL, int bitsP, int bitsS, uint64_t* kpre, uint64_t* ksuf, uint32_t* vals,
                       Scalars* sc, int64_t* launches) {

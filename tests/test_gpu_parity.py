@@ -507,3 +507,50 @@ def test_sliced_suffix_pass(pkg, cfg, m, nslices, monkeypatch):
     assert oracle.tt_diff_norm(ctx.get_cores(), T) <= 1e-10
     ctx.close()
     ref_ctx.close()
+
+
+# tt_set_observations_u8 (include/prgd.h): byte multi-indices are widened on the device and then
+# bucketed exactly like the int32 call, so everything downstream must be bit-identical -- the
+# bucketing, the residual vector, and the iterates of two steps -- on both paths; sizes with a
+# ragged tail of the 16-indices-per-thread widening kernel (m d not a multiple of 16).
+@pytest.mark.parametrize("cfg,m,path", [(2, 50_001, "tables"), (2, 50_001, "chains"), (3, 100_003, "tables"),
+                                        (5, 200_001, "tables"), (1, None, "tables")])
+def test_byte_indices_identical_to_int32(pkg, cfg, m, path):
+    pr, y, init = problem(cfg, m)
+    assert pr.idx.max() < 256
+    outs = []
+    for dt in (np.int32, np.uint8):
+        ctx = pkg.TTContext(pr.n, pr.r, path=path)
+        ctx.set_observations(pr.idx.astype(dt), y)
+        ctx.set_cores(init)
+        res = [ctx.residual_norm()]
+        g = ctx.debug("resid")
+        for _ in range(2):
+            ctx.step(0.5 if cfg == 3 else 1.0)
+            res.append(ctx.residual_norm())
+        outs.append((ctx.get_cores(), res, g))
+        ctx.close()
+    (c0, r0, g0), (c1, r1, g1) = outs
+    assert r0 == r1
+    assert np.array_equal(g0, g1)
+    assert all(np.array_equal(a, b) for a, b in zip(c0, c1))
+
+
+def test_byte_indices_errors(pkg):
+    # an index outside [0, n_k) is reported like the int32 call; mode sizes above 256 are refused
+    pr, y, init = problem(2, 1000)
+    ctx = pkg.TTContext(pr.n, pr.r)
+    bad = pr.idx.astype(np.uint8)
+    bad[17, 2] = pr.n[2]
+    with pytest.raises(pkg.PRGDError) as ei:
+        ctx.set_observations(bad, y)
+    assert ei.value.code == pkg.TT_ERR_INDEX
+    ctx.set_observations(pr.idx.astype(np.uint8), y)        # the context stays usable
+    ctx.set_cores(init)
+    assert np.isfinite(ctx.residual_norm())
+    ctx.close()
+    ctx = pkg.TTContext([300, 20, 20], [1, 2, 2, 1])
+    with pytest.raises(pkg.PRGDError) as ei:
+        ctx.set_observations(np.zeros((4, 3), np.uint8), np.zeros(4))
+    assert ei.value.code == pkg.TT_ERR_ARG
+    ctx.close()

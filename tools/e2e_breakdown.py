@@ -16,7 +16,10 @@ t = pkg.TTContext(pr.n, pr.r)
 t.set_cores(pr.truth)
 y = pr.observations(t.eval_at(pr.idx))
 t.close()
-idx_p = torch.from_numpy(np.ascontiguousarray(pr.idx)).pin_memory()
+# E2E_IDX=i32 forces the int32 upload (default: bytes when every mode size is <= 256, like bench.py)
+idt = np.uint8 if os.environ.get("E2E_IDX", "u8") == "u8" and max(pr.n) <= 256 else np.int32
+idx_p = torch.from_numpy(np.ascontiguousarray(pr.idx, dtype=idt)).pin_memory()
+print("index dtype", idx_p.dtype)
 y_p = torch.from_numpy(np.ascontiguousarray(y)).pin_memory()
 cores_p = [torch.from_numpy(np.ascontiguousarray(c)).pin_memory() for c in pr.init]
 for rep in range(3):
