@@ -58,7 +58,7 @@ def make(case: str) -> str:
             start = int(z["it"]) + 1
             T = [z[f"T{k}"] for k in range(len(pr.n))]
             res = [float(v) for v in z["res"]]
-            out = {k: z[k] for k in z.files if k.startswith("s")}
+            out = {k: z[k] for k in z.files if k.startswith("s") and "_c" in k}   # saved iterates s<it>_c<k>
             print(f"{case}: resuming after step {start - 1}", flush=True)
     for it in range(start, steps + 1):
         T, info = oracle.prgd_step(T, pr.idx, y, pr.n, pr.r, step, return_info=True)

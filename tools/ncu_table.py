@@ -59,6 +59,8 @@ def group_of(seq):
         elif "k_tab" in k or "k_table" in k:
             g = "tables_U" if phase in ("orth", "tabU") else "tables_C"
             phase = "tabU" if phase in ("orth", "tabU") else "tabC"
+        elif "k_flat_gsq" in k or "k_sum_slices" in k or ("k_flat_fix" in k and phase == "passA_sfx"):
+            phase, g = "passA_sfx", "passA_suffix"   # sliced pass A suffix (gather, fix-up, slice sum)
         elif "k_flat" in k:                        # pass A prefix (flat SDDMM + fix-up)
             phase, nseg, g = "passA", 1, "passA_prefix"
         elif "k_seg" in k or "k_spmm_pipe" in k:
@@ -78,7 +80,7 @@ def group_of(seq):
             phase, g = "back", "backward_Y"
         elif "k_project" in k or "k_round" in k or "k_dense_round" in k or "k_unweight" in k:
             phase, g = "round", "dense_round"
-        elif "k_marg" in k or "k_gather_sq" in k:
+        elif "k_marg" in k or "k_gather_sq" in k or "k_sumsq" in k:
             g = "marginals"
         elif "k_chain" in k or "k_piece" in k:
             g = "chains"
