@@ -20,6 +20,9 @@ GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 CASES = {
     # full config 5 (3e7 draws, BASELINE.json:11), one step from the perturbed-truth init
     "cfg5_full_1step": (5, None, 1.0, 1, (1,)),
+    # full config 5, 10 steps (~5 min of oracle per step on 8 cores; the 50-step bar at config
+    # 5's shape is the 4e6 case below)
+    "cfg5_full_10steps": (5, None, 1.0, 10, (1, 10)),
     # config 5's shape at 4e6 draws (OS ~ 120), 50 steps (north star: 1e-8 after 50).  At 1e6
     # draws (OS ~ 30) the theory step at 1.0 stops converging after 8 steps (residual 0.44 ->
     # 13), which would turn a 50-step comparison into a test of error amplification.

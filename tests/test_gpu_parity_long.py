@@ -24,9 +24,11 @@ def pkg():
 
 @pytest.mark.parametrize("case,path", [("cfg3_full_50steps", "tables"), ("cfg4_full_50steps", "tables"),
                                        ("cfg5_4e6_50steps", "tables"), ("cfg5_full_1step", "tables"),
+                                       ("cfg5_full_10steps", "tables"),
                                        # the per-sample chain path on the same references
                                        ("cfg3_full_50steps", "chains"), ("cfg4_full_50steps", "chains"),
-                                       ("cfg5_4e6_50steps", "chains"), ("cfg5_full_1step", "chains")])
+                                       ("cfg5_4e6_50steps", "chains"), ("cfg5_full_1step", "chains"),
+                                       ("cfg5_full_10steps", "chains")])
 def test_golden_iterates(pkg, case, path):
     cfg, m, step, steps, keep = G.CASES[case]
     gold = G.load(case)                     # a missing file fails the test (no skip)

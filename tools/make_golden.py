@@ -36,9 +36,6 @@ def _ckpt(case: str) -> str:
 PENDING = {
     # full config 5, 50 steps (BASELINE.json:11 "50 iterations"; north star: 1e-8 after 50)
     "cfg5_full_50steps": (5, None, 1.0, 50, (1, 10, 50)),
-    # full config 5, 10 steps (~5 min of oracle per step on this container's 8 cores: the
-    # 50-step run does not fit one session; the 50-step bar is covered at 4e6 samples)
-    "cfg5_full_10steps": (5, None, 1.0, 10, (1, 10)),
 }
 
 
