@@ -577,6 +577,7 @@ void enqueue_evaluate(tt_ctx* ctx, int64_t* lc, bool with_sumsq = true) {
       a.g = ctx->g;
       a.m = ctx->m;
       a.nrows = ctx->plan.NL;
+      a.ncols = ctx->plan.NR;
       a.ld = ctx->ldr[KL];
       a.rowtab = ctx->LT[KL];
       a.coltab = ctx->RT[KL];

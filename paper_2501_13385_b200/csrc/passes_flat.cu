@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kFT, 4) k_flat_sddmm(const int32_t* __restrict
                                                       int64_t nrows, const double* __restrict__ rowtab,
                                                       const double* __restrict__ coltab,
                                                       double* __restrict__ g, double* __restrict__ H,
-                                                      Rec rec) {
+                                                      Rec rec, bool pf) {
   constexpr int G = 32 / LPS, STEPS = LPS, ld = 2 * LPS * V;
   constexpr int UNR = STEPS < 4 ? STEPS : 4;
   const int lane = threadIdx.x & 31, grp = lane / LPS, sub = lane - grp * LPS;
@@ -111,9 +111,10 @@ __global__ void __launch_bounds__(kFT, 4) k_flat_sddmm(const int32_t* __restrict
     // the gathered rows of this warp's next chunk are prefetched into L2 when this one is done
     // (measured at config 5: 0.716 -> 0.636 ms; two chunks ahead 0.703 ms, the row-table rows as
     // well 0.653 ms; the same prefetch in k_spmm_pipe, whose rows already travel a chunk ahead by
-    // cp.async, made pass B 2 % slower)
+    // cp.async, made pass B 2 % slower).  Only for tables that do not stay in L2 by themselves
+    // (pf): on config 5's Omega at r = 1, a 16 MB table, the prefetch costs 0.295 -> 0.355 ms.
     const int64_t tn = (c + nw) * 32 + lane;
-    const int cvn = tn < m ? col[tn] : -1;
+    const int cvn = (pf && tn < m) ? col[tn] : -1;
     double pd[STEPS];
 #pragma unroll
     for (int s0 = 0; s0 < STEPS; s0 += UNR) {
@@ -208,8 +209,10 @@ Rec make_rec(void* base, int64_t nchunks) {
 
 template <int LPS, int V>
 void sddmm_launch(cudaStream_t s, const FlatArgs& a, const Rec& rec, unsigned grid) {
+  // L2 prefetch of the gathered rows when the gathered table exceeds ~40 MB
+  const bool pf = a.ncols * (int64_t)a.ld * 8 > (40ll << 20);
   k_flat_sddmm<LPS, V><<<grid, kFT, 0, s>>>(a.row, a.col, a.x, a.m, a.nrows, a.rowtab, a.coltab, a.g,
-                                            a.out, rec);
+                                            a.out, rec, pf);
 }
 
 // H[b] = sum_q Hq[q][b] in slice order (deterministic).

@@ -223,6 +223,7 @@ struct FlatArgs {
   const double* x = nullptr;        // [m] y
   double* g = nullptr;              // [m] output g = v - y
   int64_t m = 0, nrows = 0;
+  int64_t ncols = 0;                // rows of the gathered table
   int ld = 2;                       // table row stride (pad(r))
   const double* rowtab = nullptr;   // row vectors (left table)
   const double* coltab = nullptr;   // gathered table (right table)
